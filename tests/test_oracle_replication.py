@@ -1,0 +1,104 @@
+"""Oracle O5 pinned: Eq. 9 coefficients and example, soundness on true momentum vectors,
+Eq. 6-8 reordering, Div_max limits, mirror-boundary consistency."""
+import json
+import math
+import os
+
+import numpy as np
+
+from oracle.plan import plan
+from oracle.replication import divergence_bound
+from tests.instances import random_instance, to_oracle
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def momentum_run(w_prev, w0, updates, gamma):
+    """Eq. 2: w_{t+1} = w_t + u + gamma (w_t - w_{t-1}), applied in order."""
+    a, b = w_prev.copy(), w0.copy()
+    for u in updates:
+        a, b = b, b + u + gamma * (b - a)
+    return b
+
+
+def test_eq9_golden():
+    g = json.load(open(os.path.join(GOLD, "eq9_divergence.json")))
+    d = divergence_bound(g["lead_norms"], g["gamma"], g["hist_norm"])
+    assert math.isclose(d, g["expected_bound"], rel_tol=1e-12)
+    c = g["expected_coefficients"]
+    # coefficients recovered by probing with unit norms in one slot at a time
+    assert math.isclose(divergence_bound([0.0, 0.0], g["gamma"], 1.0), c["h0"], rel_tol=1e-12)
+    assert math.isclose(divergence_bound([1.0, 0.0], g["gamma"], 0.0), c["u1"], rel_tol=1e-12)
+    assert math.isclose(divergence_bound([0.0, 1.0], g["gamma"], 0.0), c["u2"], rel_tol=1e-12)
+    assert divergence_bound([3.0, 4.0], 0.0, 9.0) == 7.0       # gamma = 0: sum of lead norms
+    assert divergence_bound([], 0.9, 5.0) == 0.0
+
+
+def test_coefficients_match_momentum_recurrence_and_bound_is_sound():
+    rng = np.random.default_rng(0)
+    for trial in range(200):
+        gamma = float(rng.choice([0.0, 0.3, 0.9, 0.99]))
+        m = int(rng.integers(1, 7))
+        d = 16
+        w_prev = rng.normal(size=d)
+        h0 = rng.normal(size=d) * rng.uniform(0, 2)
+        w0 = w_prev + h0
+        us = [rng.normal(size=d) * rng.uniform(0, 3) for _ in range(m)]
+        ws = momentum_run(w_prev, w0, us, gamma)
+        # exact expansion: (sum_{j=1..m} g^j) h0 + sum_i (sum_{j=0..m-i} g^j) u_i
+        exp = sum(gamma**j for j in range(1, m + 1)) * h0
+        for i, u in enumerate(us, start=1):
+            exp = exp + sum(gamma**j for j in range(0, m - i + 1)) * u
+        assert np.allclose(ws - w0, exp, atol=1e-9)
+        bound = divergence_bound([float(np.linalg.norm(u)) for u in us], gamma, float(np.linalg.norm(h0)))
+        assert np.linalg.norm(ws - w0) <= bound * (1 + 1e-12) + 1e-12
+
+
+def test_eq6_8_reordering_divergence():
+    rng = np.random.default_rng(1)
+    gamma = 0.9
+    w_prev, w0 = rng.normal(size=8), rng.normal(size=8)
+    u1, u2 = rng.normal(size=8), rng.normal(size=8)
+    ws = momentum_run(w_prev, w0, [u1, u2], gamma)
+    wr = momentum_run(w_prev, w0, [u2, u1], gamma)
+    assert np.allclose(ws - wr, gamma * (u1 - u2), atol=1e-12)
+
+
+def _replica_instances(n, seed):
+    out = []
+    i = 0
+    while len(out) < n:
+        inst = random_instance(seed, i, max_n=7, replica=True)
+        i += 1
+        if inst.replicas:
+            out.append(inst)
+    return out
+
+
+def test_divmax_limits_and_mirror_consistency():
+    for inst in _replica_instances(150, 4242):
+        # Div_max = inf: the bound never binds, so no server delay
+        inst.div_max = math.inf
+        net, batch, prm = to_oracle(inst)
+        p = plan(net, batch, prm)
+        assert p["delayed_last"] == 0
+        total = len(inst.carried) + p["n_commit"]
+        assert p["replica_frozen"] + p["n_punted"] == total
+        assert p["punted"] == list(range(p["replica_frozen"], total))
+        # Div_max = 0, gamma = 0: lead must be empty at T_last unless all lead norms are 0
+        inst.div_max, inst.gamma = 0.0, 0.0
+        net, batch, prm = to_oracle(inst)
+        p = plan(net, batch, prm)
+        items = list(prm.carried) + [batch[g] for g in p["order"]]
+        lead = [it.norm for it in items[p["replica_frozen"]:]]
+        assert divergence_bound(lead, 0.0, 0.0) == 0.0
+        # the mirror boundary covers exactly replica_frozen items
+        b = p["replica_boundary_commit"]
+        nc = len(inst.carried)
+        if b == -1:
+            assert p["replica_frozen"] == 0
+        elif b == 0:
+            assert p["replica_frozen"] == nc
+        else:
+            assert p["replica_frozen"] == nc + sum(p["commit_count"][:b])
+            assert b <= p["n_server_commits"]
