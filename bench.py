@@ -1,0 +1,350 @@
+#!/usr/bin/env python
+"""bench.py — committed update-GB/s of the MLfabric plan-execution hot path on B200.
+
+Metric (BASELINE.json): aggregated update GB/s committed (device-timed, max over
+ranks), with the roofline fraction of the dominant kernel (fused_commit).
+
+Step = one batch through the whole hot path: every virtual worker pushes
+(mlf_submit_update), mlf_plan orders / aggregates / replicates (host C++),
+mlf_execute runs the fused reduce + scale + apply (+ mirror) pass on the GPU.
+value = committed update bytes of K steps / sum of the K device-timed executes
+(CUDA events on the launching stream, L2 flushed before every step, inputs
+resident in HBM).  Planning is host-side, pipelined in a deployment, and
+reported separately as planner_ms.
+
+N = 1: BASELINE config 2 (32 virtual workers, 25.6M-element fp32 updates,
+tau_max = 4 as written).  N > 1 (torchrun): config 3 (64 workers, VGG-19
+143.67M-element updates) sharded over N PS shards, one process per GPU.
+`--impl reference` times the CPU oracle on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+HBM_FALLBACK = 6650.0
+
+
+def hbm_peak():
+    try:
+        d = json.load(open(PEAKS))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return HBM_FALLBACK, "fallback (B200_PROFILING.md)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=None)
+    ap.add_argument("--tau", type=int, default=None)
+    ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
+    ap.add_argument("--no-variants", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.p is not None:
+            time.sleep(0.25)
+            self.p.terminate()
+            try:
+                out, _ = self.p.communicate(timeout=5)
+            except Exception:
+                out = ""
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ---------------------------------------------------------------- reference arm (CPU oracle)
+def run_reference(a):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import numpy as np
+
+    import synthgen as sg
+    from oracle.numerics import execute_plan
+    from oracle.plan import Item, Params, make_net, plan as oracle_plan
+    from synthgen import configs
+
+    cid = a.config or (2 if a.gpus == 1 else 3)
+    cfg = configs.config(cid, G=None if cid < 3 else a.gpus, tau=a.tau, dtype=a.dtype)
+    S_sample = min(cfg["S"], 1 << 20)
+    idx = np.arange(S_sample)
+    dt = sg.DTYPE_BF16 if a.dtype == "bf16" else sg.DTYPE_F32
+    w = sg.w0_values(cfg["seed"], idx)
+    v_init = v_prev = 0
+    tot_bytes, tot_s = 0, 0.0
+    for it in range(a.warmup + a.steps):
+        up, down, site = configs.network(cfg, it)
+        draws = configs.batch_draws(cfg, it, v_init, v_prev)
+        ops = {g: sg.update_values(cfg["seed"], g, it, idx, dt) for g in range(cfg["W"])}
+        t0 = time.perf_counter()
+        batch = [Item(g, cfg["S"] * cfg["e"], d["version"], d["t_avail"], d["norm"]) for g, d in enumerate(draws)]
+        weights = [n for (_, n) in cfg["shards"]] if cfg["G"] > 1 else None
+        p = oracle_plan(make_net(cfg["n_nodes"], up, down, None, site), batch,
+                        Params(servers=cfg["servers"], aggs=cfg["aggs"], v_init=v_init, tau_max=cfg["tau"],
+                               shard_weights=weights))
+        w, _, _ = execute_plan(w, p, lambda g: ops[g], cfg["lr"])
+        dt_s = time.perf_counter() - t0
+        v_prev, v_init = v_init, v_init + p["n_commit"]
+        if it >= a.warmup:
+            tot_bytes += p["n_commit"] * S_sample * cfg["e"]
+            tot_s += dt_s
+    val = tot_bytes / tot_s / 1e9
+    sample = f"oracle plan (full batch) + numerics on the first {S_sample} of {cfg['S']} elements per update"
+    line = {"impl": "reference", "metric": "aggregated update GB/s committed", "value": round(val, 4),
+            "unit": "GB/s", "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": round(tot_s / a.steps * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"config{cid}", "workers": cfg["W"], "update_elems": cfg["S"],
+                       "tau_max": cfg["tau"], "update_dtype": a.dtype},
+            "cpu_baseline": {"value": round(val, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": round(val, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- our arm
+def cpu_baseline_oracle(cfg, dt, budget_s=15.0):
+    """The oracle as it stands on this host: plan + numerics of config batches on a sample."""
+    import numpy as np
+
+    import synthgen as sg
+    from oracle.numerics import execute_plan
+    from oracle.plan import Item, Params, make_net, plan as oracle_plan
+    from synthgen import configs
+
+    S_sample = min(cfg["S"], 4 << 20)
+    idx = np.arange(S_sample)
+    w = sg.w0_values(cfg["seed"], idx)
+    v_init = v_prev = 0
+    tot_b, tot_s, it = 0, 0.0, 0
+    t_start = time.perf_counter()
+    while time.perf_counter() - t_start < budget_s and it < 50:
+        up, down, site = configs.network(cfg, it)
+        draws = configs.batch_draws(cfg, it, v_init, v_prev)
+        ops = {g: sg.update_values(cfg["seed"], g, it, idx, dt) for g in range(cfg["W"])}
+        t0 = time.perf_counter()
+        batch = [Item(g, cfg["S"] * cfg["e"], d["version"], d["t_avail"], d["norm"]) for g, d in enumerate(draws)]
+        p = oracle_plan(make_net(cfg["n_nodes"], up, down, None, site), batch,
+                        Params(servers=cfg["servers"], aggs=cfg["aggs"], v_init=v_init, tau_max=cfg["tau"]))
+        w, _, _ = execute_plan(w, p, lambda g: ops[g], cfg["lr"])
+        tot_s += time.perf_counter() - t0
+        tot_b += p["n_commit"] * S_sample * cfg["e"]
+        v_prev, v_init = v_init, v_init + p["n_commit"]
+        it += 1
+    return {"value": round(tot_b / tot_s / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "sample": f"{it} batches of config{cfg['cid']}: full oracle plan + numpy numerics on the first "
+                      f"{S_sample} of {cfg['S']} elements of every update (single-threaded numpy)"}
+
+
+def run_single(a):
+    import numpy as np
+    import torch
+
+    from paper_1907_00434_b200 import mlfabric as m
+    from paper_1907_00434_b200.harness import Workload, committed_bytes
+    from synthgen import configs
+
+    cid = a.config or 2
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    peak, peak_src = hbm_peak()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def measure(tau, dtype, steps, warmup, clocks=False):
+        cfg = configs.config(cid, tau=tau, dtype=dtype)
+        wl = Workload(cfg, device=0)
+        wl.fill_updates(0)
+        torch.cuda.synchronize()
+        recs = []
+        ck = Clocks(0)
+        kl0 = 0
+        for s in range(warmup + steps):
+            timed = s >= warmup
+            if timed and s == warmup:
+                kl0 = wl.ctx.stats()[0]
+                if clocks:
+                    ck.__enter__()
+            draws = wl.submit_all(s)
+            t0 = time.perf_counter()
+            pb = wl.plan(s)
+            plan_ms = (time.perf_counter() - t0) * 1e3
+            pd = pb.to_dict(cfg["W"])
+            flush.zero_()
+            wl.ctx.execute(pb)
+            ms = wl.ctx.sync()
+            wl.after_commit(pd, draws)
+            if timed:
+                n_ops = sum(pd["commit_count"])
+                alg = n_ops * wl.shard_elems * cfg["e"] + 2 * wl.shard_elems * 4
+                if pd["replica_boundary_commit"] >= 0:
+                    alg += wl.shard_elems * 4
+                recs.append(dict(ms=ms, bytes=committed_bytes(cfg, pd), alg=alg, plan_ms=plan_ms,
+                                 commits=pd["n_commit"], groups=pd["n_groups"]))
+        if clocks:
+            ck.__exit__()
+        kl = wl.ctx.stats()[0] - kl0
+        wl.ctx.close()
+        T = sum(r["ms"] for r in recs)
+        return cfg, recs, T, ck, kl
+
+    # warm-up + timed region (barrier + synchronize on both sides: single process)
+    torch.cuda.synchronize()
+    cfg, recs, T, ck, kl = measure(a.tau, a.dtype, a.steps, a.warmup, clocks=True)
+    torch.cuda.synchronize()
+    tot_bytes = sum(r["bytes"] for r in recs)
+    value = tot_bytes / (T / 1e3) / 1e9
+    alg = sum(r["alg"] for r in recs)
+    achieved = alg / (T / 1e3) / 1e9
+    kernel_launches = kl
+    line = {
+        "metric": "aggregated update GB/s committed (device-timed, max over ranks)",
+        "value": round(value, 2), "unit": "GB/s", "n_gpus": 1, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": round(T / a.steps, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": a.dtype, "data": "synthetic",
+        "config": {"workload": f"config{cid}", "workers": cfg["W"], "update_elems": cfg["S"],
+                   "tau_max": cfg["tau"], "update_dtype": a.dtype, "shards": 1,
+                   "committed_per_step": round(sum(r["commits"] for r in recs) / len(recs), 2),
+                   "groups_per_step": round(sum(r["groups"] for r in recs) / len(recs), 2),
+                   "l2": "flushed (256 MiB write) before every step; operands >> L2"},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_src,
+                     "kernel": "fused_commit_ldg",
+                     "algorithmic_bytes_per_step": int(alg / len(recs))},
+        "planner_ms": round(sum(r["plan_ms"] for r in recs) / len(recs), 3),
+        "gpu_launches": int(kernel_launches),
+        "clocks": ck.summary(),
+    }
+    # variant: tau = #workers (the paper's practice)
+    if not a.no_variants and cid == 2 and (a.tau is None or a.tau != 32):
+        cfg2, recs2, T2, _, _ = measure(32, a.dtype, max(5, a.steps // 2), 3)
+        v2 = sum(r["bytes"] for r in recs2) / (T2 / 1e3) / 1e9
+        ach2 = sum(r["alg"] for r in recs2) / (T2 / 1e3) / 1e9
+        line["variants"] = {"tau32": {"value": round(v2, 2), "unit": "GB/s", "ms_per_step": round(T2 / len(recs2), 4),
+                                      "roofline_frac": round(ach2 / peak, 4), "achieved_GBps": round(ach2, 1)}}
+    # e2e through the public API with host buffers
+    if not a.no_e2e:
+        line["e2e"] = e2e_single(cid, a)
+    if not a.no_cpu_baseline:
+        import synthgen as sg
+        line["cpu_baseline"] = cpu_baseline_oracle(configs.config(cid, tau=a.tau, dtype=a.dtype),
+                                                   sg.DTYPE_BF16 if a.dtype == "bf16" else sg.DTYPE_F32)
+    print(json.dumps(line), flush=True)
+
+
+def e2e_single(cid, a):
+    """Same metric end to end: pinned host updates -> (H2D of committed ones) -> commit -> D2H pull."""
+    import torch
+
+    from paper_1907_00434_b200 import mlfabric as m
+    from paper_1907_00434_b200.harness import Workload, committed_bytes
+    from synthgen import configs
+
+    cfg = configs.config(cid, tau=a.tau, dtype=a.dtype)
+    wl = Workload(cfg, device=0)
+    wl.fill_updates(0)
+    hosts = {}
+    for w, t in wl.slots.items():
+        hosts[w] = t.cpu().pin_memory()
+        wl.ctx.set_update_host(w, hosts[w].data_ptr())
+    pulled = torch.empty(cfg["S"], dtype=torch.float32).pin_memory()
+    torch.cuda.synchronize()
+    steps = max(3, a.steps // 4)
+    tot_b, tot_s, h2d0 = 0, 0.0, wl.ctx.stats()[1]
+    for s in range(2 + steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        draws = wl.submit_all(s)
+        pb = wl.plan(s)
+        pd = pb.to_dict(cfg["W"])
+        wl.ctx.execute(pb)
+        wl.ctx.sync()
+        wl.ctx.pull(pulled.data_ptr(), True)
+        dt_s = time.perf_counter() - t0
+        wl.after_commit(pd, draws)
+        if s == 1:
+            h2d0 = wl.ctx.stats()[1]
+            d2h0 = wl.ctx.stats()[2]
+        if s >= 2:
+            tot_b += committed_bytes(cfg, pd)
+            tot_s += dt_s
+    _, h2d, d2h = wl.ctx.stats()
+    wl.ctx.close()
+    return {"value": round(tot_b / tot_s / 1e9, 3), "unit": "GB/s",
+            "h2d_bytes_per_step": int((h2d - h2d0) / steps), "d2h_bytes_per_step": int((d2h - d2h0) / steps),
+            "includes": "submit + plan (host) + H2D of committed updates + fused commit + D2H model pull"}
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+        return
+    rank, world, local = dist_env()
+    if world > 1 or a.gpus > 1:
+        from paper_1907_00434_b200.multigpu import run_bench_multi
+        run_bench_multi(a)
+        return
+    run_single(a)
+
+
+if __name__ == "__main__":
+    main()

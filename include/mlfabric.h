@@ -1,0 +1,269 @@
+/*
+ * mlfabric.h — C ABI of the B200-native MLfabric plan-execution hot path.
+ *
+ * MLfabric (Viswanathan & Akella, arXiv 1907.00434; /root/reference/PAPER.md,
+ * cited P:line) intercepts every worker push, decides per batch an ordering of
+ * the updates under the delay bound tau_max, an in-network aggregation
+ * partition and a bounded-divergence replica set, then the updates flow to the
+ * parameter server in that order (§3; §5).  This library
+ * is that data path on one B200 box:
+ *
+ *   mlf_plan        host C++, pure: Alg. 1-2 ordering, Alg. 3
+ *                   aggregation, App. B.2 multi-server
+ *                   components, §5.3 replication.
+ *   mlf_execute     sm_100a CUDA: for every commit of the plan, in order,
+ *                   w <- w - lr * (left fold of the commit's updates), one HBM
+ *                   pass over w, each operand read once, the replica mirror
+ *                   stored in the same pass (Eq. 2 P:278 with gamma = 0).
+ *   mlf_init / mlf_submit_update / mlf_batch_view / mlf_sync /
+ *   mlf_pull_model  the PS API around it (Table 1: push with
+ *                   update_norm, get; registerAsServer/Replica params tau_max,
+ *                   Div_max).
+ *
+ * Conventions
+ *   - Every function returns mlf_status and never throws or aborts; on error
+ *     mlf_last_error() (thread-local) describes it, outputs are unspecified and
+ *     no device work has been enqueued.
+ *   - Times are integer nanoseconds relative to the batch start, sizes are
+ *     bytes, rates are bytes/second (reading R8).  Plans are
+ *     deterministic and bit-exact across implementations.
+ *   - All device memory is allocated by the caller (PyTorch) and borrowed for
+ *     the lifetime of the context.  Host arrays passed in are borrowed only for
+ *     the duration of the call.
+ *   - Planner node ids: the caller numbers the network's nodes; by convention
+ *     virtual worker w of a context is node w (mlf_batch_view reports node = w).
+ *
+ * Readings of silent or ambiguous passages (R1-R20) are listed in DESIGN.md §3.
+ */
+#ifndef MLFABRIC_H
+#define MLFABRIC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  MLF_OK = 0,
+  MLF_E_INVALID = 1,        /* null pointer, id out of range, duplicate submit, plan inconsistent with the batch */
+  MLF_E_STATE = 2,          /* call not legal in the context's current state (slot in flight, ...) */
+  MLF_E_CUDA = 3,           /* any CUDA runtime error; sticky, destroy the context */
+  MLF_E_UNSCHEDULABLE = 4,  /* an update's path to a server/replica is down forever (R9) */
+  MLF_E_CAPACITY = 5        /* caller-provided output arrays too small */
+} mlf_status;
+
+typedef enum { MLF_F32 = 0, MLF_BF16 = 1 } mlf_dtype;
+
+/* ======================================================================
+ * Planning (pure host C++, reentrant, no CUDA)
+ * ====================================================================== */
+
+/* The network G = (V, E) of App. B.1 in the per-node NIC model the
+ * evaluation uses (incoming and outgoing NIC limits treated
+ * independently, congestion-free core; reading R9).  Path i->j is
+ * [up(i), pair(i,j), down(j)]; a capacity of 0 means uncapped (not on the
+ * path), < 0 means the link is down.  Nodes with the same site id (or i == j)
+ * exchange data in zero time.  Capacities are constant over the batch. */
+typedef struct {
+  int32_t n_nodes;
+  const int64_t *nic_up;    /* [n_nodes] egress cap, bytes/s */
+  const int64_t *nic_down;  /* [n_nodes] ingress cap, bytes/s */
+  const int64_t *bw;        /* [n_nodes*n_nodes] pair-path caps (row = src) or NULL */
+  const int32_t *site;      /* [n_nodes] co-location ids or NULL */
+} mlf_net;
+
+/* One batch U: the pushes accumulated since the last plan.
+ * node = worker node, bytes = sz(g), version = v(g) (the model version the
+ * update was computed from), t_avail_ns = when the update is ready,
+ * norm = ||u|| as passed to push(server, update, update_norm) (Table 1). */
+typedef struct {
+  int32_t n;
+  const int32_t *node;
+  const int64_t *bytes;
+  const int64_t *version;
+  const int64_t *t_avail_ns;
+  const double *norm;
+} mlf_batch;
+
+typedef struct {
+  /* parameter-server shards (App. B.2): component j of every update goes to
+   * server[j]; component sizes are proportional to shard_weight (NULL = equal):
+   * comp_j = floor(B*cum_{j+1}/W) - floor(B*cum_j/W). */
+  int32_t n_servers;
+  const int32_t *server;
+  const int64_t *shard_weight;
+  /* pre-assigned aggregators (R13): group i uses agg[i-1] */
+  int32_t k;
+  const int32_t *agg;
+  /* replica: 0 = none, else one node per shard, plus k_r
+   * separate replica aggregators */
+  int32_t n_replicas;
+  const int32_t *replica;
+  int32_t k_r;
+  const int32_t *replica_agg;
+  /* model version after the previous batch and delay bound (Table 1) */
+  int64_t v_init;
+  int32_t tau_max;
+  /* Div_max (Table 1) >= 0, may be +inf; momentum gamma in [0,1) and
+   * ||h0|| for the Eq. 9/12 bound (gamma = 0 on the hot path, R15) */
+  double div_max, gamma, hist_norm;
+  /* replica items punted by the previous batch, in order */
+  int32_t n_carried;
+  const int32_t *carried_node;
+  const int64_t *carried_bytes;
+  const double *carried_norm;
+} mlf_plan_params;
+
+/* Plan outputs.  All arrays are caller-allocated; `capacity` is their length
+ * and must be >= batch n + n_carried, else MLF_E_CAPACITY. */
+typedef struct {
+  int32_t capacity;
+  int32_t n_commit;          /* |O(U)| */
+  int32_t *order;            /* [n_commit] batch indices in commit order O(U) (Alg. 2) */
+  uint8_t *drop_reason;      /* [n] 0 kept, 1 expired (dl(g) < position), 2 look-ahead drop (Alg. 2 line 10) */
+  int32_t *group;            /* [n] 0 direct to server, i >= 1 aggregated in group i (at agg[i-1]), -1 dropped */
+  int32_t n_direct;          /* n* of Alg. 3: the first n_direct updates of O(U) go direct */
+  int32_t n_groups;
+  int32_t *group_node;       /* [n_groups] aggregator node of group i+1 */
+  int32_t n_server_commits;  /* commits at the server: n_direct singles, then one per group */
+  int32_t *commit_first;     /* [n_server_commits] first position in order[] */
+  int32_t *commit_count;     /* [n_server_commits] members (runs over order[]) */
+  int64_t *commit_t_ns;      /* [n_server_commits] model commit times (R7), informational */
+  int32_t replica_frozen;    /* items of carried ++ order covered by this batch's replica write */
+  int32_t replica_boundary_commit; /* mirror point (R16): backup <- w after this many server
+                                      commits; 0 = the pre-batch w; -1 = no replica write */
+  int32_t n_punted;
+  int32_t *punted;           /* [n_punted] indices into carried ++ order, carried to the next batch */
+  uint8_t delayed_last;      /* 1 if the last server commit was delayed to meet Div_max (§5.3) */
+  int64_t t_total_ns;        /* model time of the last server commit */
+} mlf_plan_out;
+
+/* Alg. 2 -> Alg. 3 -> §5.3 on one batch.  Pure; may run concurrently. */
+mlf_status mlf_plan(const mlf_net *net, const mlf_batch *batch,
+                    const mlf_plan_params *params, mlf_plan_out *out);
+
+/* ======================================================================
+ * Execution (CUDA, one context per process/device; a context is single-threaded)
+ * ====================================================================== */
+
+typedef struct {
+  int32_t device;              /* CUDA device this context launches on */
+  int32_t rank, world;         /* this process serves shard `rank` of `world` PS shards */
+  int64_t model_elems;         /* S: full model length in fp32 elements */
+  int64_t shard_begin;         /* first element of this rank's shard (multiple of 64) */
+  int64_t shard_elems;         /* length of this rank's shard */
+  int32_t n_workers;           /* virtual workers; worker w is planner node w */
+  mlf_dtype update_dtype;      /* dtype of every update vector */
+  float lr;                    /* w <- w - lr * x (R18) */
+  float *model_shard;          /* [shard_elems] fp32, on `device` */
+  float *backup_shard;         /* [shard_elems] fp32 mirror target of this shard (local or a
+                                  mapped peer pointer), or NULL if replication is off */
+  void *const *update_slot;    /* [n_workers] full-length update vectors (S elements), each a
+                                  device pointer valid on `device` (local or mapped peer) */
+  const int32_t *worker_rank;  /* [n_workers] home rank of each worker, or NULL (all local) */
+  int32_t n_nodes;             /* planner nodes known to the executor (>= n_workers) */
+  const int32_t *node_rank;    /* [n_nodes] rank hosting each node (aggregators), or NULL (all 0) */
+  int32_t agg_slots;           /* fp32 aggregate buffers per rank for cross-GPU groups (0 = fold groups
+                                  inside the commit kernel, no materialised aggregates) */
+  float *const *agg_scratch;   /* [world*agg_slots] S-element fp32 buffers valid on `device` */
+  void *stream;                /* cudaStream_t (borrowed) */
+} mlf_config;
+
+typedef struct mlf_ctx mlf_ctx;
+
+/* Validate the configuration and create a context at model version v0. */
+mlf_status mlf_init(const mlf_config *cfg, int64_t v0, mlf_ctx **out);
+
+/* push(server, update, update_norm) (Table 1): the update vector already
+ * sits in the worker's slot; append its descriptor to the current batch.  The
+ * slot belongs to the library until the mlf_execute that commits or drops it
+ * has completed on-stream (mlf_sync).  Resubmitting a worker already in the
+ * batch or still in flight -> MLF_E_STATE.  *index_in_batch (may be NULL)
+ * receives the update's batch index. */
+mlf_status mlf_submit_update(mlf_ctx *ctx, int32_t worker, int64_t version,
+                             int64_t t_avail_ns, double norm, int32_t *index_in_batch);
+
+/* Optional: worker `worker`'s update lives in pinned host memory `host_ptr`;
+ * mlf_execute copies it to the worker's device slot only if the plan commits
+ * it (dropped updates are "dropped at the worker itself", and move
+ * no bytes).  NULL unregisters. */
+mlf_status mlf_set_update_host(mlf_ctx *ctx, int32_t worker, const void *host_ptr);
+
+/* Borrow the current batch as planner input (arrays valid until the next
+ * submit/execute).  bytes = model_elems * sizeof(dtype), node = worker. */
+mlf_status mlf_batch_view(mlf_ctx *ctx, mlf_batch *out);
+
+/* Current model version v_init. */
+mlf_status mlf_version(mlf_ctx *ctx, int64_t *version);
+
+/* Execute a plan for the current batch (asynchronously, on cfg.stream).
+ * Validates the plan against the batch (MLF_E_INVALID if inconsistent), then
+ * launches the fused reduce+scale+apply kernel over this rank's shard: for each
+ * server commit c in order, x_c = left fold of its members (O(U) order),
+ * w <- w - lr*x_c (two fp32 roundings, R17); backup <- w at the boundary
+ * commit (R16).  Version += n_commit; the batch is cleared.
+ * With agg_slots > 0 and world > 1 the call is split in two phases (see
+ * mlf_execute_phase). */
+mlf_status mlf_execute(mlf_ctx *ctx, const mlf_plan_out *plan);
+
+/* Two-phase execution for materialised cross-GPU aggregation trees:
+ * phase 1 = tree_reduce of the groups whose aggregator lives on this rank into
+ * agg_scratch; phase 2 = the ordered commit reading aggregates (local or peer).
+ * The caller must make every rank's phase 1 complete before any rank's phase 2
+ * starts (mlf_phase_event + a host barrier).  mlf_execute == phase 1 then 2 when
+ * world == 1. */
+#define MLF_PHASE_AGGREGATE 1
+#define MLF_PHASE_COMMIT 2
+mlf_status mlf_execute_phase(mlf_ctx *ctx, const mlf_plan_out *plan, int32_t phase);
+
+/* Wait for the last execute; *device_ms (may be NULL) = CUDA-event time from its
+ * first to its last kernel on this device.  Releases the batch's slots. */
+mlf_status mlf_sync(mlf_ctx *ctx, float *device_ms);
+
+/* get(server, model) (Table 1): copy this rank's shard of the latest
+ * committed model to dst + shard_begin (device or host memory, dst_is_host)
+ * after the last execute; *version = batch-boundary version (R19). */
+mlf_status mlf_pull_model(mlf_ctx *ctx, void *dst, int32_t dst_is_host, int64_t *version);
+
+/* Counters: kernels this context launched, and bytes it moved host<->device. */
+mlf_status mlf_stats(mlf_ctx *ctx, int64_t *kernel_launches, int64_t *h2d_bytes, int64_t *d2h_bytes);
+
+void mlf_destroy(mlf_ctx *ctx);
+
+const char *mlf_last_error(void);
+
+/* ======================================================================
+ * Peer memory (one process per GPU; NVLink through NVSwitch)
+ * ====================================================================== */
+typedef struct {
+  uint8_t handle[64];        /* cudaIpcMemHandle_t of the allocation containing the pointer */
+  int64_t offset;            /* pointer - allocation base */
+} mlf_ipc_handle;
+
+mlf_status mlf_ipc_export(int32_t device, const void *dev_ptr, mlf_ipc_handle *out);
+/* Map a peer allocation into this process on `device`; *dev_ptr = base + offset. */
+mlf_status mlf_ipc_open(int32_t device, const mlf_ipc_handle *h, void **dev_ptr);
+mlf_status mlf_ipc_close(int32_t device, void *dev_ptr, int64_t offset);
+
+/* ======================================================================
+ * Test infrastructure kernels (not on the hot path)
+ * ====================================================================== */
+
+/* Fill dst[0..n) with elements [elem_offset, elem_offset+n) of the synthgen
+ * stream (seed, kind, a, b): kind 1 = update of worker a in iteration b,
+ * kind 2 = w0.  variant 0 = "normal", 1 = "exact"; dtype F32 or BF16 (kind 2
+ * is always F32).  Same counter-based splitmix64 as synthgen/__init__.py,
+ * implemented independently.  Launches on `stream`. */
+mlf_status mlf_synth_fill(int32_t device, void *dst, int64_t n, int64_t elem_offset,
+                          mlf_dtype dtype, uint64_t seed, int32_t kind, int64_t a, int64_t b,
+                          int32_t variant, void *stream);
+
+/* Device copy kernel (HBM / NVLink peer roofline denominators): dst <- src, bytes % 16 == 0. */
+mlf_status mlf_copy_kernel(int32_t device, void *dst, const void *src, int64_t bytes, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MLFABRIC_H */

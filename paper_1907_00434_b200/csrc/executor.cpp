@@ -1,0 +1,526 @@
+// executor.cpp — the C-ABI execution half of libmlfabric: context, batch
+// admission (push, Table 1), plan validation, operand tables, kernel
+// launches, version accounting, pull (get), peer memory.
+//
+// One context per process and device.  Single GPU: the whole plan runs as one
+// fused commit pass (groups folded in registers).  With
+// world > 1 PS shards (App. B.2) every rank runs the same plan on
+// its own slice; operands are full-length update vectors on their home GPU and
+// are read through NVLink peer mappings (P2P loads inside the commit kernel), or,
+// in tree mode (agg_slots > 0), groups are first summed on their aggregator's
+// GPU (tree_reduce) and shards read slices of the aggregate.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+#include "planner.h"
+
+using namespace mlf;
+
+static thread_local std::string g_err;
+void mlf_set_error(const char *msg) { g_err = msg ? msg : ""; }
+extern "C" const char *mlf_last_error(void) { return g_err.c_str(); }
+
+namespace {
+
+struct Fail {
+  mlf_status code;
+  std::string msg;
+};
+
+#define CK(call)                                                                                      \
+  do {                                                                                                \
+    cudaError_t e_ = (call);                                                                          \
+    if (e_ != cudaSuccess)                                                                            \
+      throw Fail{MLF_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)};                     \
+  } while (0)
+
+template <class F>
+mlf_status guard(F &&f) {
+  try {
+    g_err.clear();
+    f();
+    return MLF_OK;
+  } catch (const Fail &e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::exception &e) {
+    g_err = e.what();
+    return MLF_E_INVALID;
+  } catch (...) {
+    g_err = "unknown error";
+    return MLF_E_INVALID;
+  }
+}
+
+}  // namespace
+
+struct mlf_ctx {
+  mlf_config cfg{};
+  std::vector<void *> slot;
+  std::vector<int32_t> worker_rank, node_rank;
+  std::vector<float *> agg_scratch;
+  int sm_count = 148;
+  int64_t version = 0;
+  size_t elem_bytes = 4;
+  cudaStream_t stream = nullptr;
+  // current batch
+  std::vector<int32_t> b_worker, b_node;
+  std::vector<int64_t> b_bytes, b_version, b_tavail;
+  std::vector<double> b_norm;
+  std::vector<uint8_t> in_batch, in_flight;
+  std::vector<const void *> host_src;
+  // execution state
+  cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
+  bool started = false, pending = false, sticky = false, phase1_done = false;
+  int64_t launches = 0, h2d = 0, d2h = 0;
+  CommitImpl impl = CommitImpl::kLdg;
+};
+
+static void check_ctx(mlf_ctx *c) {
+  if (!c) throw Fail{MLF_E_INVALID, "null context"};
+  if (c->sticky) throw Fail{MLF_E_CUDA, "context has a sticky CUDA error; destroy it"};
+}
+
+extern "C" mlf_status mlf_init(const mlf_config *cfg, int64_t v0, mlf_ctx **out) {
+  return guard([&] {
+    if (!cfg || !out) throw Fail{MLF_E_INVALID, "null argument"};
+    *out = nullptr;
+    const mlf_config &k = *cfg;
+    if (k.world < 1 || k.rank < 0 || k.rank >= k.world) throw Fail{MLF_E_INVALID, "rank/world"};
+    if (k.model_elems < 1 || k.shard_begin < 0 || k.shard_elems < 0 || k.shard_begin + k.shard_elems > k.model_elems)
+      throw Fail{MLF_E_INVALID, "model/shard extents"};
+    if (k.shard_begin % 64 != 0) throw Fail{MLF_E_INVALID, "shard_begin must be a multiple of 64 elements"};
+    if (k.n_workers < 0 || (k.n_workers > 0 && !k.update_slot)) throw Fail{MLF_E_INVALID, "update slots"};
+    if (k.update_dtype != MLF_F32 && k.update_dtype != MLF_BF16) throw Fail{MLF_E_INVALID, "update dtype"};
+    if (k.shard_elems > 0 && !k.model_shard) throw Fail{MLF_E_INVALID, "model shard"};
+    if (k.agg_slots < 0 || (k.agg_slots > 0 && !k.agg_scratch)) throw Fail{MLF_E_INVALID, "aggregate scratch"};
+    if (k.n_nodes < k.n_workers) throw Fail{MLF_E_INVALID, "n_nodes < n_workers"};
+    auto c = new mlf_ctx();
+    c->cfg = k;
+    c->version = v0;
+    c->elem_bytes = k.update_dtype == MLF_BF16 ? 2 : 4;
+    c->stream = static_cast<cudaStream_t>(k.stream);
+    for (int w = 0; w < k.n_workers; ++w) {
+      if (!k.update_slot[w]) {
+        delete c;
+        throw Fail{MLF_E_INVALID, "null update slot"};
+      }
+      c->slot.push_back(k.update_slot[w]);
+      int r = k.worker_rank ? k.worker_rank[w] : 0;
+      if (r < 0 || r >= k.world) {
+        delete c;
+        throw Fail{MLF_E_INVALID, "worker_rank out of range"};
+      }
+      c->worker_rank.push_back(r);
+    }
+    for (int i = 0; i < k.n_nodes; ++i) {
+      int r = k.node_rank ? k.node_rank[i] : 0;
+      if (r < 0 || r >= k.world) {
+        delete c;
+        throw Fail{MLF_E_INVALID, "node_rank out of range"};
+      }
+      c->node_rank.push_back(r);
+    }
+    for (int i = 0; i < k.world * k.agg_slots; ++i) c->agg_scratch.push_back(k.agg_scratch[i]);
+    c->in_batch.assign(k.n_workers, 0);
+    c->in_flight.assign(k.n_workers, 0);
+    c->host_src.assign(k.n_workers, nullptr);
+    const char *impl = getenv("MLF_COMMIT_IMPL");
+    if (impl && std::string(impl) == "bulk") c->impl = CommitImpl::kBulk;
+    try {
+      CK(cudaSetDevice(k.device));
+      CK(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, k.device));
+      CK(cudaEventCreate(&c->ev_start));
+      CK(cudaEventCreate(&c->ev_stop));
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
+extern "C" void mlf_destroy(mlf_ctx *c) {
+  if (!c) return;
+  if (c->ev_start) cudaEventDestroy(c->ev_start);
+  if (c->ev_stop) cudaEventDestroy(c->ev_stop);
+  delete c;
+}
+
+static void release_if_done(mlf_ctx *c) {
+  if (!c->pending) return;
+  cudaError_t q = cudaEventQuery(c->ev_stop);
+  if (q == cudaSuccess) {
+    c->pending = false;
+    std::fill(c->in_flight.begin(), c->in_flight.end(), 0);
+  } else if (q != cudaErrorNotReady) {
+    c->sticky = true;
+    throw Fail{MLF_E_CUDA, std::string("cudaEventQuery: ") + cudaGetErrorString(q)};
+  }
+}
+
+extern "C" mlf_status mlf_submit_update(mlf_ctx *c, int32_t worker, int64_t version, int64_t t_avail_ns, double norm,
+                                        int32_t *index_in_batch) {
+  return guard([&] {
+    check_ctx(c);
+    if (worker < 0 || worker >= c->cfg.n_workers) throw Fail{MLF_E_INVALID, "worker out of range"};
+    if (t_avail_ns < 0 || !(norm >= 0)) throw Fail{MLF_E_INVALID, "t_avail / norm"};
+    if (c->phase1_done) throw Fail{MLF_E_STATE, "batch is being executed (phase 1 done)"};
+    if (c->in_batch[worker]) throw Fail{MLF_E_STATE, "worker already submitted in this batch"};
+    release_if_done(c);
+    if (c->in_flight[worker]) throw Fail{MLF_E_STATE, "worker slot still in flight (call mlf_sync)"};
+    c->in_batch[worker] = 1;
+    if (index_in_batch) *index_in_batch = (int32_t)c->b_worker.size();
+    c->b_worker.push_back(worker);
+    c->b_node.push_back(worker);
+    c->b_bytes.push_back(c->cfg.model_elems * (int64_t)c->elem_bytes);
+    c->b_version.push_back(version);
+    c->b_tavail.push_back(t_avail_ns);
+    c->b_norm.push_back(norm);
+  });
+}
+
+extern "C" mlf_status mlf_set_update_host(mlf_ctx *c, int32_t worker, const void *host_ptr) {
+  return guard([&] {
+    check_ctx(c);
+    if (worker < 0 || worker >= c->cfg.n_workers) throw Fail{MLF_E_INVALID, "worker out of range"};
+    c->host_src[worker] = host_ptr;
+  });
+}
+
+extern "C" mlf_status mlf_batch_view(mlf_ctx *c, mlf_batch *out) {
+  return guard([&] {
+    check_ctx(c);
+    if (!out) throw Fail{MLF_E_INVALID, "null output"};
+    out->n = (int32_t)c->b_worker.size();
+    out->node = c->b_node.data();
+    out->bytes = c->b_bytes.data();
+    out->version = c->b_version.data();
+    out->t_avail_ns = c->b_tavail.data();
+    out->norm = c->b_norm.data();
+  });
+}
+
+extern "C" mlf_status mlf_version(mlf_ctx *c, int64_t *v) {
+  return guard([&] {
+    check_ctx(c);
+    if (!v) throw Fail{MLF_E_INVALID, "null output"};
+    *v = c->version;
+  });
+}
+
+// --------------------------------------------------------------- plan checks
+static void validate_plan(const mlf_ctx *c, const mlf_plan_out *p) {
+  const int n = (int)c->b_worker.size();
+  if (!p) throw Fail{MLF_E_INVALID, "null plan"};
+  if (p->n_commit < 0 || p->n_commit > n) throw Fail{MLF_E_INVALID, "plan n_commit inconsistent with the batch"};
+  if (p->n_commit > 0 && (!p->order || !p->commit_first || !p->commit_count || !p->group))
+    throw Fail{MLF_E_INVALID, "plan arrays missing"};
+  std::vector<uint8_t> seen(n, 0);
+  for (int i = 0; i < p->n_commit; ++i) {
+    int g = p->order[i];
+    if (g < 0 || g >= n || seen[g]) throw Fail{MLF_E_INVALID, "plan order is not a subset of the batch"};
+    seen[g] = 1;
+  }
+  int pos = 0;
+  if (p->n_server_commits < 0) throw Fail{MLF_E_INVALID, "n_server_commits"};
+  for (int ci = 0; ci < p->n_server_commits; ++ci) {
+    if (p->commit_first[ci] != pos || p->commit_count[ci] < 1) throw Fail{MLF_E_INVALID, "commit runs not contiguous"};
+    int gid = p->group[p->order[pos]];
+    for (int q = pos; q < pos + p->commit_count[ci]; ++q) {
+      if (q >= p->n_commit) throw Fail{MLF_E_INVALID, "commit runs exceed n_commit"};
+      if (p->group[p->order[q]] != gid) throw Fail{MLF_E_INVALID, "commit mixes groups"};
+    }
+    if (gid < 0 || gid > p->n_groups) throw Fail{MLF_E_INVALID, "group id out of range"};
+    if (gid > 0) {
+      int node = p->group_node ? p->group_node[gid - 1] : -1;
+      if (node < 0 || node >= (int)c->node_rank.size()) throw Fail{MLF_E_INVALID, "aggregator node unknown to the executor"};
+    }
+    pos += p->commit_count[ci];
+  }
+  if (pos != p->n_commit) throw Fail{MLF_E_INVALID, "commit runs do not cover O(U)"};
+  if (p->replica_boundary_commit < -1 || p->replica_boundary_commit > p->n_server_commits)
+    throw Fail{MLF_E_INVALID, "replica boundary out of range"};
+  if (p->replica_boundary_commit >= 0 && !c->cfg.backup_shard)
+    throw Fail{MLF_E_INVALID, "plan writes the replica but the context has no backup shard"};
+}
+
+static bool tree_mode(const mlf_ctx *c) { return c->cfg.world > 1 && c->cfg.agg_slots > 0; }
+
+// slot of group gid among the groups aggregated on the same rank
+static int agg_slot_of(const mlf_ctx *c, const mlf_plan_out *p, int gid, int *rank_out) {
+  int node = p->group_node[gid - 1];
+  int r = c->node_rank[node], s = 0;
+  for (int g = 1; g < gid; ++g)
+    if (c->node_rank[p->group_node[g - 1]] == r) ++s;
+  if (s >= c->cfg.agg_slots) throw Fail{MLF_E_CAPACITY, "more groups on one rank than agg_slots"};
+  *rank_out = r;
+  return s;
+}
+
+static void record_start(mlf_ctx *c) {
+  if (!c->started) {
+    CK(cudaEventRecord(c->ev_start, c->stream));
+    c->started = true;
+  }
+}
+
+static void phase_stage(mlf_ctx *c, const mlf_plan_out *p) {
+  CK(cudaSetDevice(c->cfg.device));
+  record_start(c);
+  const size_t bytes = (size_t)c->cfg.model_elems * c->elem_bytes;
+  // committed host-resident updates homed on this rank move host -> device;
+  // dropped ones never move ("dropped at the worker itself")
+  for (int i = 0; i < p->n_commit; ++i) {
+    int w = c->b_worker[p->order[i]];
+    if (c->host_src[w] && c->worker_rank[w] == c->cfg.rank) {
+      CK(cudaMemcpyAsync(c->slot[w], c->host_src[w], bytes, cudaMemcpyHostToDevice, c->stream));
+      c->h2d += (int64_t)bytes;
+    }
+  }
+  if (!tree_mode(c)) return;
+  // tree_reduce of the groups aggregated on this rank
+  for (int ci = 0; ci < p->n_server_commits; ++ci) {
+    int first = p->commit_first[ci], cnt = p->commit_count[ci];
+    int gid = p->group[p->order[first]];
+    if (gid <= 0) continue;
+    int r;
+    int s = agg_slot_of(c, p, gid, &r);
+    if (r != c->cfg.rank) continue;
+    if (cnt > kMaxOps) throw Fail{MLF_E_CAPACITY, "group larger than kMaxOps"};
+    ReduceArgs a;
+    a.out = c->agg_scratch[(size_t)r * c->cfg.agg_slots + s];
+    a.n = c->cfg.model_elems;
+    a.src_off = 0;
+    a.n_ops = cnt;
+    for (int q = 0; q < cnt; ++q) {
+      a.op[q] = c->slot[c->b_worker[p->order[first + q]]];
+      a.flag[q] = c->cfg.update_dtype == MLF_BF16 ? kOpBf16 : 0;
+    }
+    CK(launch_reduce(a, c->stream, c->sm_count));
+    ++c->launches;
+  }
+}
+
+static void phase_commit(mlf_ctx *c, const mlf_plan_out *p) {
+  CK(cudaSetDevice(c->cfg.device));
+  record_start(c);
+  const bool tree = tree_mode(c);
+  const uint8_t dflag = c->cfg.update_dtype == MLF_BF16 ? kOpBf16 : 0;
+  // operand table in commit order
+  struct Op {
+    const void *ptr;
+    uint8_t flag;
+    int commit;
+  };
+  std::vector<Op> ops;
+  for (int ci = 0; ci < p->n_server_commits; ++ci) {
+    int first = p->commit_first[ci], cnt = p->commit_count[ci];
+    int gid = p->group[p->order[first]];
+    if (tree && gid > 0) {
+      int r;
+      int s = agg_slot_of(c, p, gid, &r);
+      ops.push_back({c->agg_scratch[(size_t)r * c->cfg.agg_slots + s], (uint8_t)(kOpFirst | kOpLast), ci + 1});
+      continue;
+    }
+    for (int q = 0; q < cnt; ++q) {
+      uint8_t f = dflag;
+      if (q == 0) f |= kOpFirst;
+      if (q == cnt - 1) f |= kOpLast;
+      ops.push_back({c->slot[c->b_worker[p->order[first + q]]], f, ci + 1});
+    }
+  }
+  const int boundary = c->cfg.backup_shard ? p->replica_boundary_commit : -1;
+  // launches, split at commit boundaries when the list exceeds kMaxOps
+  size_t i0 = 0;
+  bool first_launch = true;
+  while (i0 < ops.size() || (first_launch && c->cfg.shard_elems > 0 && (boundary == 0))) {
+    size_t i1 = std::min(ops.size(), i0 + (size_t)kMaxOps);
+    if (i1 < ops.size())
+      while (i1 > i0 && !(ops[i1 - 1].flag & kOpLast)) --i1;
+    if (i1 == i0 && i0 < ops.size()) throw Fail{MLF_E_CAPACITY, "a single commit has more than kMaxOps members"};
+    CommitArgs a;
+    a.w = c->cfg.model_shard;
+    a.backup = c->cfg.backup_shard;
+    a.n = c->cfg.shard_elems;
+    a.src_off = c->cfg.shard_begin;
+    a.lr = c->cfg.lr;
+    a.n_ops = (int32_t)(i1 - i0);
+    a.backup_after = -2;
+    if (first_launch && boundary == 0) a.backup_after = -1;
+    for (size_t q = i0; q < i1; ++q) {
+      a.op[q - i0] = ops[q].ptr;
+      a.flag[q - i0] = ops[q].flag;
+      if (boundary > 0 && ops[q].commit == boundary && (ops[q].flag & kOpLast)) a.backup_after = (int32_t)(q - i0);
+    }
+    if (a.n > 0) {
+      CK(launch_commit(a, c->stream, c->sm_count, c->impl));
+      ++c->launches;
+    }
+    first_launch = false;
+    i0 = i1;
+    if (ops.empty()) break;
+  }
+  CK(cudaEventRecord(c->ev_stop, c->stream));
+  c->started = false;
+  c->pending = true;
+  // version accounting (R2): every committed update advances the version
+  c->version += p->n_commit;
+  for (int w : c->b_worker) {
+    c->in_flight[w] = 1;
+    c->in_batch[w] = 0;
+  }
+  c->b_worker.clear();
+  c->b_node.clear();
+  c->b_bytes.clear();
+  c->b_version.clear();
+  c->b_tavail.clear();
+  c->b_norm.clear();
+  c->phase1_done = false;
+}
+
+extern "C" mlf_status mlf_execute_phase(mlf_ctx *c, const mlf_plan_out *p, int32_t phase) {
+  mlf_status st = guard([&] {
+    check_ctx(c);
+    validate_plan(c, p);
+    if (phase & MLF_PHASE_AGGREGATE) {
+      if (c->phase1_done) throw Fail{MLF_E_STATE, "phase 1 already ran for this batch"};
+      phase_stage(c, p);
+      c->phase1_done = true;
+    }
+    if (phase & MLF_PHASE_COMMIT) {
+      if (!c->phase1_done) throw Fail{MLF_E_STATE, "phase 2 before phase 1"};
+      phase_commit(c, p);
+    }
+  });
+  if (st == MLF_E_CUDA && c) c->sticky = true;
+  return st;
+}
+
+extern "C" mlf_status mlf_execute(mlf_ctx *c, const mlf_plan_out *p) {
+  return mlf_execute_phase(c, p, MLF_PHASE_AGGREGATE | MLF_PHASE_COMMIT);
+}
+
+extern "C" mlf_status mlf_sync(mlf_ctx *c, float *device_ms) {
+  mlf_status st = guard([&] {
+    check_ctx(c);
+    if (device_ms) *device_ms = 0.f;
+    if (!c->pending) return;
+    CK(cudaEventSynchronize(c->ev_stop));
+    if (device_ms) CK(cudaEventElapsedTime(device_ms, c->ev_start, c->ev_stop));
+    c->pending = false;
+    std::fill(c->in_flight.begin(), c->in_flight.end(), 0);
+  });
+  if (st == MLF_E_CUDA && c) c->sticky = true;
+  return st;
+}
+
+extern "C" mlf_status mlf_pull_model(mlf_ctx *c, void *dst, int32_t dst_is_host, int64_t *version) {
+  mlf_status st = guard([&] {
+    check_ctx(c);
+    if (!dst) throw Fail{MLF_E_INVALID, "null destination"};
+    CK(cudaSetDevice(c->cfg.device));
+    const size_t bytes = (size_t)c->cfg.shard_elems * 4;
+    char *d = static_cast<char *>(dst) + (size_t)c->cfg.shard_begin * 4;
+    if (bytes) {
+      CK(cudaMemcpyAsync(d, c->cfg.model_shard, bytes, dst_is_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
+                         c->stream));
+      if (dst_is_host) c->d2h += (int64_t)bytes;
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    if (version) *version = c->version;
+  });
+  if (st == MLF_E_CUDA && c) c->sticky = true;
+  return st;
+}
+
+extern "C" mlf_status mlf_stats(mlf_ctx *c, int64_t *kl, int64_t *h2d, int64_t *d2h) {
+  return guard([&] {
+    if (!c) throw Fail{MLF_E_INVALID, "null context"};
+    if (kl) *kl = c->launches;
+    if (h2d) *h2d = c->h2d;
+    if (d2h) *d2h = c->d2h;
+  });
+}
+
+// --------------------------------------------------------------- peer memory
+typedef CUresult (*PFN_range)(CUdeviceptr *, size_t *, CUdeviceptr);
+
+static void alloc_base(const void *p, char **base) {
+  static PFN_range fn = nullptr;
+  if (!fn) {
+    void *f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CK(cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q));
+    if (!f || q != cudaDriverEntryPointSuccess) throw Fail{MLF_E_CUDA, "cuMemGetAddressRange unavailable"};
+    fn = reinterpret_cast<PFN_range>(f);
+  }
+  CUdeviceptr b = 0;
+  size_t sz = 0;
+  if (fn(&b, &sz, (CUdeviceptr)p) != CUDA_SUCCESS) throw Fail{MLF_E_CUDA, "cuMemGetAddressRange failed"};
+  *base = reinterpret_cast<char *>(b);
+}
+
+extern "C" mlf_status mlf_ipc_export(int32_t device, const void *ptr, mlf_ipc_handle *out) {
+  return guard([&] {
+    if (!ptr || !out) throw Fail{MLF_E_INVALID, "null argument"};
+    CK(cudaSetDevice(device));
+    char *base = nullptr;
+    alloc_base(ptr, &base);
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, base));
+    static_assert(sizeof(h) == 64, "ipc handle size");
+    std::memcpy(out->handle, &h, 64);
+    out->offset = static_cast<const char *>(ptr) - base;
+  });
+}
+
+extern "C" mlf_status mlf_ipc_open(int32_t device, const mlf_ipc_handle *h, void **ptr) {
+  return guard([&] {
+    if (!h || !ptr) throw Fail{MLF_E_INVALID, "null argument"};
+    CK(cudaSetDevice(device));
+    cudaIpcMemHandle_t hh;
+    std::memcpy(&hh, h->handle, 64);
+    void *base = nullptr;
+    CK(cudaIpcOpenMemHandle(&base, hh, cudaIpcMemLazyEnablePeerAccess));
+    *ptr = static_cast<char *>(base) + h->offset;
+  });
+}
+
+extern "C" mlf_status mlf_ipc_close(int32_t device, void *ptr, int64_t offset) {
+  return guard([&] {
+    CK(cudaSetDevice(device));
+    CK(cudaIpcCloseMemHandle(static_cast<char *>(ptr) - offset));
+  });
+}
+
+// --------------------------------------------------------------- test infrastructure
+extern "C" mlf_status mlf_synth_fill(int32_t device, void *dst, int64_t n, int64_t elem_offset, mlf_dtype dtype,
+                                     uint64_t seed, int32_t kind, int64_t a, int64_t b, int32_t variant,
+                                     void *stream) {
+  return guard([&] {
+    if (!dst && n > 0) throw Fail{MLF_E_INVALID, "null destination"};
+    if (kind != 1 && kind != 2) throw Fail{MLF_E_INVALID, "kind must be 1 (update) or 2 (w0)"};
+    if (variant != 0 && variant != 1) throw Fail{MLF_E_INVALID, "variant"};
+    CK(cudaSetDevice(device));
+    uint64_t key = synth_stream_key(seed, (uint64_t)kind, (uint64_t)a, (uint64_t)b);
+    CK(launch_synth(dst, n, elem_offset, (int)dtype, key, kind, variant, static_cast<cudaStream_t>(stream)));
+  });
+}
+
+extern "C" mlf_status mlf_copy_kernel(int32_t device, void *dst, const void *src, int64_t bytes, void *stream) {
+  return guard([&] {
+    if (bytes % 16 != 0) throw Fail{MLF_E_INVALID, "bytes % 16 != 0"};
+    CK(cudaSetDevice(device));
+    int sm = 148;
+    CK(cudaDeviceGetAttribute(&sm, cudaDevAttrMultiProcessorCount, device));
+    CK(launch_copy(dst, src, bytes, static_cast<cudaStream_t>(stream), sm));
+  });
+}

@@ -1,0 +1,52 @@
+// kernels.h — launch interface between the executor (host C++) and the sm_100a kernels.
+#pragma once
+#include <cstdint>
+
+#include <cuda_runtime_api.h>
+
+namespace mlf {
+
+// Operands per fused-commit launch (kernel parameter space, CUDA >= 12.1 allows
+// 32 KB of parameters).  Longer commit lists are split at commit boundaries.
+constexpr int kMaxOps = 1024;
+
+// flag bits per operand
+constexpr uint8_t kOpFirst = 1;   // first member of its commit: x = u (not x += u)
+constexpr uint8_t kOpLast = 2;    // last member of its commit: w <- w - lr*x after it
+constexpr uint8_t kOpBf16 = 4;    // operand is bf16 (widened exactly), else fp32
+
+// The fused reduce + scale + apply (+ mirror store) pass over one shard slice.
+struct CommitArgs {
+  float *w;             // [n] shard slice, read once, written once
+  float *backup;        // [n] mirror target (local or peer), or nullptr
+  int64_t n;            // slice length (elements)
+  int64_t src_off;      // element offset of the slice inside every operand vector
+  float lr;
+  int32_t n_ops;
+  int32_t backup_after; // -2: no mirror store; -1: store the loaded w; k: store w after op k
+  const void *op[kMaxOps];
+  uint8_t flag[kMaxOps];
+};
+
+// tree_reduce: out[i] = left fold of members, fp32 (an aggregator's sum).
+struct ReduceArgs {
+  float *out;           // [n]
+  int64_t n;
+  int64_t src_off;
+  int32_t n_ops;
+  const void *op[kMaxOps];
+  uint8_t flag[kMaxOps];
+};
+
+enum class CommitImpl : int { kLdg = 0, kBulk = 1 };
+
+cudaError_t launch_commit(const CommitArgs &a, cudaStream_t s, int sm_count, CommitImpl impl);
+cudaError_t launch_reduce(const ReduceArgs &a, cudaStream_t s, int sm_count);
+cudaError_t launch_synth(void *dst, int64_t n, int64_t elem_offset, int dtype, uint64_t key, int kind,
+                         int variant, cudaStream_t s);
+cudaError_t launch_copy(void *dst, const void *src, int64_t bytes, cudaStream_t s, int sm_count);
+
+// host-side splitmix64 key derivation (same definition as synthgen.stream_key)
+uint64_t synth_stream_key(uint64_t seed, uint64_t kind, uint64_t a, uint64_t b);
+
+}  // namespace mlf

@@ -1,0 +1,715 @@
+// planner.cpp — mlf_plan: MLfabric's per-batch scheduler in host C++.
+//
+// PAPER.md (cited P:line): §5 decomposition; Alg. 1 ShrtUp and
+// t_en water-filling / NetUp (Fig. 5); deadlines;
+// Alg. 2 look-ahead drop; Alg. 3 DetAgg + enumeration over n
+// (P:1050-1159); App. B.2 multi-server components; §5.3
+// replication with the Eq. 9/12 divergence bound.
+// Readings R1-R20 are in DESIGN.md §3; the integer-time model is R8: times in
+// ns (int64), sizes in bytes, rates in bytes/s, byte*ns products in __int128.
+// Compiled with -ffp-contract=off so the only floating point (the divergence
+// bound) is evaluated exactly in the documented order.
+//
+// Performance: planning is O(#U^2 * G) transfer evaluations.
+// Candidate evaluations never copy the network: a transfer's tentative
+// reservation lives in a small overlay of the <= 3G links it touches.  The
+// #U+1 DetAgg cases are independent ("can be parallelized") and run
+// on a thread pool, reduced in case order so the result equals the sequential
+// argmin with ties to the smallest n (R14).
+#include "planner.h"
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <utility>
+#include <vector>
+
+namespace mlf {
+
+using i64 = int64_t;
+using i128 = __int128;
+static constexpr i64 NS_PER_S = 1000000000LL;
+static constexpr i64 T_INF = std::numeric_limits<i64>::max();
+static constexpr i64 T_LIMIT = std::numeric_limits<i64>::max() / 4;   // time overflow guard
+
+struct PlanFail {
+  mlf_status code;
+  std::string msg;
+};
+
+struct Seg {
+  i64 t, r;
+};
+using Profile = std::vector<Seg>;
+
+// ---------------------------------------------------------------- network
+struct NetDef {
+  int n = 0;
+  const int64_t *up = nullptr, *down = nullptr, *bw = nullptr;
+  const int32_t *site = nullptr;
+};
+
+// link keys: up(i) = i, down(j) = n + j, pair(i, j) = 2n + i*n + j
+struct Net {
+  const NetDef *def = nullptr;
+  std::vector<Profile> ud;                         // 2n up/down profiles
+  std::unordered_map<i64, Profile> pair;           // pair links touched so far
+
+  explicit Net(const NetDef *d) : def(d), ud(2 * d->n) {
+    for (int i = 0; i < d->n; ++i) {
+      ud[i] = Profile{{0, std::max<i64>(d->up[i], 0)}};
+      ud[d->n + i] = Profile{{0, std::max<i64>(d->down[i], 0)}};
+    }
+  }
+  i64 capacity(i64 key) const {
+    const i64 n = def->n;
+    if (key < n) return def->up[key];
+    if (key < 2 * n) return def->down[key - n];
+    return def->bw[key - 2 * n];
+  }
+  const Profile *get(i64 key) const {
+    if (key < 2 * (i64)def->n) return &ud[key];
+    auto it = pair.find(key);
+    return it == pair.end() ? nullptr : &it->second;
+  }
+  Profile &mut(i64 key) {
+    if (key < 2 * (i64)def->n) return ud[key];
+    auto it = pair.find(key);
+    if (it == pair.end()) it = pair.emplace(key, Profile{{0, std::max<i64>(capacity(key), 0)}}).first;
+    return it->second;
+  }
+};
+
+struct Path {
+  int nk = 0;       // 0 = zero-time transfer
+  i64 key[3];
+};
+
+static bool same_site(const NetDef &d, int a, int b) {
+  if (a == b) return true;
+  return d.site && d.site[a] == d.site[b];
+}
+
+static Path path_of(const NetDef &d, int src, int dst) {
+  Path p;
+  if (same_site(d, src, dst)) return p;
+  const i64 n = d.n;
+  if (d.up[src] != 0) p.key[p.nk++] = src;
+  if (d.bw && d.bw[(i64)src * n + dst] != 0) p.key[p.nk++] = 2 * n + (i64)src * n + dst;
+  if (d.down[dst] != 0) p.key[p.nk++] = n + dst;
+  return p;
+}
+
+static bool path_dead(const NetDef &d, int src, int dst) {
+  if (same_site(d, src, dst)) return false;
+  const i64 n = d.n;
+  if (d.up[src] < 0) return true;
+  if (d.bw && d.bw[(i64)src * n + dst] < 0) return true;
+  if (d.down[dst] < 0) return true;
+  return false;
+}
+
+// A view = base network + overlay of modified profiles (copy-on-write).
+struct View {
+  Net *base;
+  std::vector<std::pair<i64, Profile>> ov;
+  explicit View(Net *b) : base(b) {}
+  const Profile &prof(i64 key) const {
+    for (auto &kv : ov)
+      if (kv.first == key) return kv.second;
+    const Profile *p = base->get(key);
+    if (p) return *p;
+    // untouched pair link: constant capacity
+    static thread_local Profile tmp;
+    tmp.assign(1, Seg{0, std::max<i64>(base->capacity(key), 0)});
+    return tmp;
+  }
+  Profile &mut(i64 key) {
+    for (auto &kv : ov)
+      if (kv.first == key) return kv.second;
+    ov.emplace_back(key, prof(key));
+    return ov.back().second;
+  }
+  void commit() {
+    for (auto &kv : ov) base->mut(kv.first) = std::move(kv.second);
+    ov.clear();
+  }
+};
+
+static inline i64 rate_at(const Profile &p, i64 t) {
+  // last segment with start <= t (profiles start at 0, t >= 0)
+  auto it = std::upper_bound(p.begin(), p.end(), t, [](i64 v, const Seg &s) { return v < s.t; });
+  return (it == p.begin()) ? p.front().r : std::prev(it)->r;
+}
+static inline i64 next_bp(const Profile &p, i64 t) {
+  auto it = std::upper_bound(p.begin(), p.end(), t, [](i64 v, const Seg &s) { return v < s.t; });
+  return it == p.end() ? T_INF : it->t;
+}
+
+struct TSeg {
+  i64 a, b, r;
+};
+struct Transfer {
+  i64 t_st = 0, t_en = 0;
+  Path path;
+  std::vector<TSeg> segs;
+};
+
+// O1: water-fill `size` bytes from t_avail along the path residual (Fig. 5(b)).
+// Returns false if the path residual is zero forever after t_avail.
+template <class V>
+static bool transfer(const V &v, const NetDef &d, i64 size, int src, int dst, i64 t_avail, Transfer &out) {
+  out.segs.clear();
+  out.path = path_of(d, src, dst);
+  if (size == 0 || out.path.nk == 0) {
+    out.path.nk = 0;
+    out.t_st = out.t_en = t_avail;
+    return true;
+  }
+  const Profile *pr[3];
+  for (int k = 0; k < out.path.nk; ++k) pr[k] = &v.prof(out.path.key[k]);
+  i128 need = (i128)size * NS_PER_S;
+  i64 cur = t_avail;
+  bool started = false;
+  for (;;) {
+    i64 r = T_INF, nb = T_INF;
+    for (int k = 0; k < out.path.nk; ++k) {
+      r = std::min(r, rate_at(*pr[k], cur));
+      nb = std::min(nb, next_bp(*pr[k], cur));
+    }
+    if (r > 0) {
+      if (!started) {
+        out.t_st = cur;
+        started = true;
+      }
+      if (nb == T_INF || (i128)r * (nb - cur) >= need) {
+        i128 dt = (need + r - 1) / r;
+        if ((i128)cur + dt > (i128)T_LIMIT) throw PlanFail{MLF_E_INVALID, "model time overflow"};
+        out.t_en = cur + (i64)dt;
+        out.segs.push_back({cur, out.t_en, r});
+        return true;
+      }
+      need -= (i128)r * (nb - cur);
+      out.segs.push_back({cur, nb, r});
+    } else if (nb == T_INF) {
+      return false;
+    }
+    cur = nb;
+  }
+}
+
+// O2: NetUp — subtract the transfer's rate profile on every link of its path.
+static void split_at(Profile &p, i64 t) {
+  auto it = std::lower_bound(p.begin(), p.end(), t, [](const Seg &s, i64 v) { return s.t < v; });
+  if (it != p.end() && it->t == t) return;
+  i64 r = (it == p.begin()) ? p.front().r : std::prev(it)->r;
+  p.insert(it, Seg{t, r});
+}
+static void subtract(Profile &p, i64 a, i64 b, i64 r) {
+  split_at(p, a);
+  split_at(p, b);
+  for (auto &s : p)
+    if (s.t >= a && s.t < b) {
+      s.r -= r;
+      if (s.r < 0) throw PlanFail{MLF_E_INVALID, "internal: residual went negative"};
+    }
+}
+template <class V>
+static void reserve(V &v, const Transfer &tr) {
+  for (int k = 0; k < tr.path.nk; ++k) {
+    Profile &p = v.mut(tr.path.key[k]);
+    for (auto &s : tr.segs) subtract(p, s.a, s.b, s.r);
+  }
+}
+
+// App. B.2: component sizes proportional to the shard weights.
+static void component_bytes(i64 size, const std::vector<i64> &w, i64 wsum, std::vector<i64> &out) {
+  out.resize(w.size());
+  i64 cum = 0;
+  for (size_t j = 0; j < w.size(); ++j) {
+    i64 lo = (i64)((i128)size * cum / wsum);
+    cum += w[j];
+    out[j] = (i64)((i128)size * cum / wsum) - lo;
+  }
+}
+
+struct Send {
+  i64 t_st = 0, t_en = 0;
+};
+
+struct Ctx {
+  NetDef d;
+  std::vector<int> servers, aggs, replicas, raggs;
+  std::vector<i64> weights;
+  i64 wsum = 0;
+};
+
+// Multi-component transfer: components reserved sequentially in destination
+// order (R11) into view v; t_en = max, t_st = min.  False if unschedulable.
+static bool send(View &v, const Ctx &c, const std::vector<int> &dsts, int src, i64 size, i64 t_avail, Send &out) {
+  std::vector<i64> comp;
+  component_bytes(size, c.weights, c.wsum, comp);
+  Transfer tr;
+  out.t_st = T_INF;
+  out.t_en = 0;
+  for (size_t j = 0; j < dsts.size(); ++j) {
+    if (!transfer(v, c.d, comp[j], src, dsts[j], t_avail, tr)) return false;
+    reserve(v, tr);
+    out.t_st = std::min(out.t_st, tr.t_st);
+    out.t_en = std::max(out.t_en, tr.t_en);
+  }
+  return true;
+}
+
+struct Item {
+  int node;
+  i64 size, version, t_avail;
+  double norm;
+};
+
+// ---------------------------------------------------------------- O3 ordering
+struct OrderRes {
+  std::vector<int> order;
+  std::vector<uint8_t> reason;
+};
+
+static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 tau, i64 v_init) {
+  const int n = (int)batch.size();
+  std::vector<i64> dl(n);
+  for (int g = 0; g < n; ++g) dl[g] = batch[g].version + tau - v_init;
+  std::vector<int> unproc(n);
+  for (int g = 0; g < n; ++g) unproc[g] = g;
+  OrderRes res;
+  res.reason.assign(n, 0);
+  Net nw(&c.d);
+  i64 p = 1;
+
+  // ShrtDline(pos, cands, NW): due set argmin if any, else ShrtUp (R4, R6).
+  auto pick = [&](i64 pos, const std::vector<int> &cands, View &base_view, int &g_out, Send &s_out,
+                  View *view_out) {
+    bool any_due = false;
+    for (int g : cands)
+      if (dl[g] == pos) {
+        any_due = true;
+        break;
+      }
+    g_out = -1;
+    for (int g : cands) {
+      if (any_due && dl[g] != pos) continue;
+      View v = base_view;                          // copies only the overlay
+      Send s;
+      if (!send(v, c, c.servers, batch[g].node, batch[g].size, batch[g].t_avail, s))
+        throw PlanFail{MLF_E_UNSCHEDULABLE, "update path to a server is down"};
+      if (g_out < 0 || s.t_en < s_out.t_en) {
+        g_out = g;
+        s_out = s;
+        if (view_out) *view_out = std::move(v);
+      }
+    }
+  };
+
+  for (;;) {
+    std::vector<int> keep;
+    for (int g : unproc) {
+      if (dl[g] < p)
+        res.reason[g] = 1;                          // expired (R4)
+      else
+        keep.push_back(g);
+    }
+    unproc.swap(keep);
+    if (unproc.empty()) break;
+    View base(&nw);
+    View star(&nw);
+    int g_star;
+    Send s_star;
+    pick(p, unproc, base, g_star, s_star, &star);
+    std::vector<int> cands;
+    for (int g : unproc)
+      if (g != g_star && dl[g] >= p + 1) cands.push_back(g);
+    bool drop = false;
+    if (!cands.empty()) {
+      int g_next;
+      Send s_next;
+      pick(p + 1, cands, star, g_next, s_next, nullptr);   // on NetUp(NW, g*)
+      if (s_star.t_en > s_next.t_en) drop = true;          // Alg. 2 line 10
+    }
+    unproc.erase(std::find(unproc.begin(), unproc.end(), g_star));
+    if (drop) {
+      res.reason[g_star] = 2;
+      continue;
+    }
+    res.order.push_back(g_star);
+    star.commit();
+    ++p;
+  }
+  return res;
+}
+
+// ---------------------------------------------------------------- O4 aggregation
+struct CommitRec {
+  int first, count, group;
+  Send send;
+};
+struct AggCase {
+  int n = 0;
+  bool feasible = false;
+  i64 total = 0;
+  std::vector<CommitRec> commits;
+};
+
+// Alg. 3 DetAgg(n) on a copy of `net0` (R10-R12).  If net_out is given, the
+// final network is stored there.
+static AggCase det_agg(int n, const std::vector<Item> &items, const Net &net0, const Ctx &c,
+                       const std::vector<int> &dsts, const std::vector<int> &aggs, Net *net_out) {
+  AggCase cs;
+  cs.n = n;
+  Net nw = net0;
+  i64 t_max = 0;
+  bool have = n > 0;
+  const int k = (int)aggs.size();
+  for (int i = 0; i < n; ++i) {                               // lines 3-7
+    View v(&nw);
+    Send s;
+    if (!send(v, c, dsts, items[i].node, items[i].size, items[i].t_avail, s)) return cs;
+    v.commit();
+    t_max = std::max(t_max, s.t_en);
+    cs.commits.push_back({i, 1, 0, s});
+  }
+  int aid = 1, i = n, gfirst = n, gcount = 0;
+  i64 gsize = 0, garr = 0;
+  auto flush = [&]() -> bool {                                // lines 11-12
+    View v(&nw);
+    Send s;
+    if (!send(v, c, dsts, aggs[aid - 1], gsize, garr, s)) return false;
+    v.commit();
+    t_max = std::max(t_max, s.t_en);
+    have = true;
+    cs.commits.push_back({gfirst, gcount, aid, s});
+    ++aid;
+    gfirst += gcount;
+    gcount = 0;
+    gsize = 0;
+    garr = 0;
+    return true;
+  };
+  Transfer tr;
+  View direct(&nw);
+  while (i < (int)items.size()) {
+    if (aid > k) return cs;
+    if (!transfer(direct, c.d, items[i].size, items[i].node, aggs[aid - 1], items[i].t_avail, tr)) return cs;
+    if (have && tr.t_en > t_max) {                            // line 10
+      if (gcount == 0) return cs;
+      if (!flush()) return cs;
+      continue;
+    }
+    reserve(direct, tr);                                      // lines 16-18
+    direct.commit();
+    if (gcount == 0) gfirst = i;
+    ++gcount;
+    gsize = std::max(gsize, items[i].size);
+    garr = std::max(garr, tr.t_en);
+    ++i;
+  }
+  if (gcount > 0 && !flush()) return cs;
+  cs.feasible = true;
+  cs.total = t_max;
+  if (net_out) *net_out = std::move(nw);
+  return cs;
+}
+
+static int n_threads_for(int cases) {
+  unsigned hw = std::thread::hardware_concurrency();
+  int t = (int)std::min<unsigned>(hw ? hw : 1, 16);
+  if (cases < 16) t = 1;
+  return std::max(1, std::min(t, cases));
+}
+
+// Alg. 3 lines 21-24: all |U|+1 cases, argmin total, ties -> smallest n (R14).
+static AggCase plan_aggregation(const std::vector<Item> &items, const Net &net0, const Ctx &c,
+                                const std::vector<int> &dsts, const std::vector<int> &aggs, Net *net_out) {
+  const int N = (int)items.size();
+  std::vector<i64> totals(N + 1, -1);
+  const int nt = n_threads_for(N + 1);
+  std::atomic<int> next{0};
+  std::vector<PlanFail> errs;
+  std::atomic<bool> failed{false};
+  PlanFail first_err{MLF_OK, ""};
+  auto worker = [&]() {
+    for (;;) {
+      int n = next.fetch_add(1);
+      if (n > N || failed.load()) return;
+      try {
+        AggCase cs = det_agg(n, items, net0, c, dsts, aggs, nullptr);
+        totals[n] = cs.feasible ? cs.total : -1;
+      } catch (const PlanFail &e) {
+        if (!failed.exchange(true)) first_err = e;
+      }
+    }
+  };
+  if (nt == 1) {
+    worker();
+  } else {
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t) th.emplace_back(worker);
+    for (auto &t : th) t.join();
+  }
+  if (failed.load()) throw first_err;
+  int best = -1;
+  for (int n = 0; n <= N; ++n)
+    if (totals[n] >= 0 && (best < 0 || totals[n] < totals[best])) best = n;
+  if (best < 0) throw PlanFail{MLF_E_UNSCHEDULABLE, "no feasible aggregation case"};
+  return det_agg(best, items, net0, c, dsts, aggs, net_out);
+}
+
+static std::vector<i64> chained_times(const std::vector<CommitRec> &cm) {
+  std::vector<i64> out;
+  i64 prev = 0;
+  for (auto &x : cm) {
+    prev = std::max(prev, x.send.t_en);
+    out.push_back(prev);
+  }
+  return out;
+}
+
+// ---------------------------------------------------------------- O5 replication
+// Eq. 9/12 bound with the momentum coefficients (R15); fixed evaluation order.
+static double divergence_bound(const double *norms, int m, double gamma, double h0) {
+  if (m == 0) return 0.0;
+  std::vector<double> pw(m + 1);
+  pw[0] = 1.0;
+  for (int j = 1; j <= m; ++j) pw[j] = pw[j - 1] * gamma;
+  double coef_h = 0.0;
+  for (int j = 1; j <= m; ++j) coef_h += pw[j];
+  double d = coef_h * h0;
+  for (int i = 1; i <= m; ++i) {
+    double cf = 0.0;
+    for (int j = 0; j <= m - i; ++j) cf += pw[j];
+    d += cf * norms[i - 1];
+  }
+  return d;
+}
+
+}  // namespace mlf
+
+using namespace mlf;
+
+static thread_local std::string g_plan_err;
+const char *mlf_planner_last_error() { return g_plan_err.c_str(); }
+
+static mlf_status plan_impl(const mlf_net *net, const mlf_batch *batch, const mlf_plan_params *prm,
+                            mlf_plan_out *out) {
+  if (!net || !batch || !prm || !out) throw PlanFail{MLF_E_INVALID, "null argument"};
+  if (net->n_nodes < 1 || !net->nic_up || !net->nic_down) throw PlanFail{MLF_E_INVALID, "bad network"};
+  Ctx c;
+  c.d.n = net->n_nodes;
+  c.d.up = net->nic_up;
+  c.d.down = net->nic_down;
+  c.d.bw = net->bw;
+  c.d.site = net->site;
+  const int nn = net->n_nodes;
+  auto node_ok = [&](int x) { return x >= 0 && x < nn; };
+  const int n = batch->n;
+  if (n < 0) throw PlanFail{MLF_E_INVALID, "batch n < 0"};
+  if (n > 0 && (!batch->node || !batch->bytes || !batch->version || !batch->t_avail_ns || !batch->norm))
+    throw PlanFail{MLF_E_INVALID, "null batch array"};
+  if (prm->n_servers < 1 || !prm->server) throw PlanFail{MLF_E_INVALID, "no server"};
+  for (int j = 0; j < prm->n_servers; ++j) {
+    if (!node_ok(prm->server[j])) throw PlanFail{MLF_E_INVALID, "server node out of range"};
+    c.servers.push_back(prm->server[j]);
+  }
+  if (prm->k < 0 || (prm->k > 0 && !prm->agg)) throw PlanFail{MLF_E_INVALID, "aggregators"};
+  for (int i = 0; i < prm->k; ++i) {
+    if (!node_ok(prm->agg[i])) throw PlanFail{MLF_E_INVALID, "aggregator node out of range"};
+    c.aggs.push_back(prm->agg[i]);
+  }
+  if (prm->n_replicas != 0 && prm->n_replicas != prm->n_servers)
+    throw PlanFail{MLF_E_INVALID, "replica count must equal server count"};
+  if (prm->n_replicas > 0 && !prm->replica) throw PlanFail{MLF_E_INVALID, "replica nodes"};
+  for (int j = 0; j < prm->n_replicas; ++j) {
+    if (!node_ok(prm->replica[j])) throw PlanFail{MLF_E_INVALID, "replica node out of range"};
+    c.replicas.push_back(prm->replica[j]);
+  }
+  if (prm->k_r < 0 || (prm->k_r > 0 && !prm->replica_agg)) throw PlanFail{MLF_E_INVALID, "replica aggregators"};
+  for (int i = 0; i < prm->k_r; ++i) {
+    if (!node_ok(prm->replica_agg[i])) throw PlanFail{MLF_E_INVALID, "replica aggregator out of range"};
+    c.raggs.push_back(prm->replica_agg[i]);
+  }
+  if (prm->tau_max < 0 || !(prm->div_max >= 0) || !(prm->gamma >= 0.0 && prm->gamma < 1.0))
+    throw PlanFail{MLF_E_INVALID, "tau_max / div_max / gamma"};
+  if (!(prm->hist_norm >= 0 && std::isfinite(prm->hist_norm))) throw PlanFail{MLF_E_INVALID, "hist_norm"};
+  if (prm->n_carried < 0 || (prm->n_carried > 0 && (!prm->carried_node || !prm->carried_bytes || !prm->carried_norm)))
+    throw PlanFail{MLF_E_INVALID, "carried items"};
+  for (int j = 0; j < prm->n_servers; ++j) {
+    i64 w = prm->shard_weight ? prm->shard_weight[j] : 1;
+    if (w <= 0) throw PlanFail{MLF_E_INVALID, "shard weights"};
+    c.weights.push_back(w);
+    c.wsum += w;
+  }
+  std::vector<Item> items(n), carried(prm->n_carried);
+  for (int g = 0; g < n; ++g) {
+    items[g] = {batch->node[g], batch->bytes[g], batch->version[g], batch->t_avail_ns[g], batch->norm[g]};
+    if (!node_ok(items[g].node)) throw PlanFail{MLF_E_INVALID, "update node out of range"};
+    if (items[g].size < 0 || items[g].t_avail < 0 || !(items[g].norm >= 0 && std::isfinite(items[g].norm)))
+      throw PlanFail{MLF_E_INVALID, "bad update descriptor"};
+  }
+  for (int g = 0; g < prm->n_carried; ++g) {
+    carried[g] = {prm->carried_node[g], prm->carried_bytes[g], 0, 0, prm->carried_norm[g]};
+    if (!node_ok(carried[g].node)) throw PlanFail{MLF_E_INVALID, "carried node out of range"};
+    if (carried[g].size < 0 || !(carried[g].norm >= 0 && std::isfinite(carried[g].norm)))
+      throw PlanFail{MLF_E_INVALID, "bad carried descriptor"};
+  }
+  if (out->capacity < n + prm->n_carried ||
+      (n > 0 && (!out->order || !out->drop_reason || !out->group || !out->commit_first || !out->commit_count ||
+                 !out->commit_t_ns)) ||
+      ((n + prm->n_carried) > 0 && !out->punted) || (n > 0 && prm->k > 0 && !out->group_node))
+    throw PlanFail{MLF_E_CAPACITY, "output arrays too small or missing"};
+  // unschedulable pre-check (R9)
+  std::vector<i64> comp;
+  for (auto &it : items) {
+    component_bytes(it.size, c.weights, c.wsum, comp);
+    for (size_t j = 0; j < c.servers.size(); ++j)
+      if (comp[j] > 0 && path_dead(c.d, it.node, c.servers[j]))
+        throw PlanFail{MLF_E_UNSCHEDULABLE, "update path to a server is down"};
+  }
+  if (!c.replicas.empty()) {
+    auto chk = [&](const Item &it) {
+      component_bytes(it.size, c.weights, c.wsum, comp);
+      for (size_t j = 0; j < c.replicas.size(); ++j)
+        if (comp[j] > 0 && path_dead(c.d, it.node, c.replicas[j]))
+          throw PlanFail{MLF_E_UNSCHEDULABLE, "update path to a replica is down"};
+    };
+    for (auto &it : carried) chk(it);
+    for (auto &it : items) chk(it);
+  }
+
+  // 1. ordering
+  OrderRes ores = order_final(c, items, prm->tau_max, prm->v_init);
+  std::vector<Item> ordered;
+  for (int g : ores.order) ordered.push_back(items[g]);
+  // 2. aggregation on the batch-start network (R10)
+  Net net0(&c.d);
+  Net after(&c.d);
+  AggCase cs = plan_aggregation(ordered, net0, c, c.servers, c.aggs, &after);
+  std::vector<i64> times = chained_times(cs.commits);
+
+  out->n_commit = (int)ores.order.size();
+  for (int g = 0; g < n; ++g) {
+    out->drop_reason[g] = ores.reason[g];
+    out->group[g] = -1;
+  }
+  for (size_t p = 0; p < ores.order.size(); ++p) out->order[p] = ores.order[p];
+  int n_groups = 0;
+  for (size_t ci = 0; ci < cs.commits.size(); ++ci) {
+    auto &cm = cs.commits[ci];
+    out->commit_first[ci] = cm.first;
+    out->commit_count[ci] = cm.count;
+    out->commit_t_ns[ci] = times[ci];
+    for (int p = cm.first; p < cm.first + cm.count; ++p) out->group[ores.order[p]] = cm.group;
+    if (cm.group > 0) ++n_groups;
+  }
+  out->n_direct = cs.n;
+  out->n_groups = n_groups;
+  for (int i = 0; i < n_groups; ++i) out->group_node[i] = c.aggs[i];
+  out->n_server_commits = (int)cs.commits.size();
+  out->replica_frozen = 0;
+  out->replica_boundary_commit = -1;
+  out->n_punted = 0;
+  out->delayed_last = 0;
+  out->t_total_ns = times.empty() ? 0 : times.back();
+
+  // 3. replication (§5.3) on the network after the server plan
+  if (!c.replicas.empty()) {
+    std::vector<Item> ritems(carried);
+    ritems.insert(ritems.end(), ordered.begin(), ordered.end());
+    const int n_c = (int)carried.size();
+    AggCase rc = plan_aggregation(ritems, after, c, c.replicas, c.raggs, nullptr);
+    std::vector<i64> rtimes = chained_times(rc.commits);
+    i64 t_last = times.empty() ? 0 : times.back();
+    std::vector<int> ends;
+    int acc = 0;
+    for (auto &x : rc.commits) {
+      acc += x.count;
+      ends.push_back(acc);
+    }
+    size_t n_pre = 0;
+    while (n_pre < rtimes.size() && rtimes[n_pre] <= t_last) ++n_pre;
+    int frozen = n_pre ? ends[n_pre - 1] : 0;
+    std::vector<double> norms;
+    for (auto &it : ritems) norms.push_back(it.norm);
+    const int R = (int)ritems.size();
+    double bound = divergence_bound(norms.data() + frozen, R - frozen, prm->gamma, prm->hist_norm);
+    bool delayed = false;
+    if (bound > prm->div_max) {
+      int a_e = -1;
+      for (size_t ci = n_pre; ci < rc.commits.size(); ++ci) {
+        if (divergence_bound(norms.data() + ends[ci], R - ends[ci], prm->gamma, prm->hist_norm) <= prm->div_max) {
+          a_e = (int)ci;
+          break;
+        }
+      }
+      if (a_e < 0) throw PlanFail{MLF_E_INVALID, "internal: no replica commit meets Div_max"};
+      frozen = ends[a_e];
+      if (!cs.commits.empty()) {
+        delayed = true;
+        const Send &last = cs.commits.back().send;
+        i64 shift = std::max<i64>(0, rtimes[a_e] - last.t_st);
+        i64 new_end = last.t_en + shift;
+        i64 prev = times.size() > 1 ? times[times.size() - 2] : 0;
+        t_last = std::max(prev, new_end);
+      }
+    }
+    // R16 mirror boundary
+    int f_o = std::max(0, frozen - n_c), boundary, covered;
+    if (frozen == 0) {
+      boundary = -1;
+      covered = 0;
+    } else if (f_o == 0) {
+      boundary = 0;
+      covered = n_c;
+    } else {
+      int a2 = 0;
+      boundary = -1;
+      for (size_t ci = 0; ci < cs.commits.size(); ++ci) {
+        a2 += cs.commits[ci].count;
+        if (a2 >= f_o) {
+          boundary = (int)ci + 1;
+          break;
+        }
+      }
+      covered = n_c + a2;
+    }
+    out->replica_frozen = covered;
+    out->replica_boundary_commit = boundary;
+    out->n_punted = R - covered;
+    for (int i = covered; i < R; ++i) out->punted[i - covered] = i;
+    out->delayed_last = delayed ? 1 : 0;
+    if (delayed) out->commit_t_ns[cs.commits.size() - 1] = t_last;
+    out->t_total_ns = t_last;
+  }
+  return MLF_OK;
+}
+
+extern "C" mlf_status mlf_plan(const mlf_net *net, const mlf_batch *batch, const mlf_plan_params *params,
+                               mlf_plan_out *out) {
+  try {
+    g_plan_err.clear();
+    return plan_impl(net, batch, params, out);
+  } catch (const PlanFail &e) {
+    g_plan_err = e.msg;
+    mlf_set_error(e.msg.c_str());
+    return e.code;
+  } catch (const std::exception &e) {
+    g_plan_err = e.what();
+    mlf_set_error(e.what());
+    return MLF_E_INVALID;
+  } catch (...) {
+    mlf_set_error("unknown planner error");
+    return MLF_E_INVALID;
+  }
+}

@@ -1,0 +1,86 @@
+// synth.cu — test-infrastructure kernels: the counter-based input generator and
+// a plain device copy (HBM / NVLink denominators).  Not on the hot path.
+//
+// The generator is splitmix64 used as a counter-based stream:
+//   key          = sm64(sm64(sm64(seed ^ kind) ^ a) ^ b),  sm64(x) = mix64(x + GOLDEN)
+//   word(key, i) = mix64(key + (i + 1) * GOLDEN)
+// with the value maps documented in synthgen/__init__.py (an independent
+// NumPy implementation of the same definition; tests compare them bit for bit).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.h"
+
+namespace mlf {
+
+static constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+static uint64_t sm64(uint64_t x) { return mix64(x + kGolden); }
+
+uint64_t synth_stream_key(uint64_t seed, uint64_t kind, uint64_t a, uint64_t b) {
+  uint64_t k = sm64(seed ^ kind);
+  k = sm64(k ^ a);
+  return sm64(k ^ b);
+}
+
+// kind 1 = update, 2 = w0; variant 0 normal, 1 exact; dtype 0 f32, 1 bf16
+__global__ void synth_fill_kernel(void *dst, int64_t n, int64_t off, int dtype, uint64_t key, int kind,
+                                  int variant) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint64_t w = mix64(key + (uint64_t)(off + i + 1) * kGolden);
+    float v;
+    if (kind == 2) {
+      v = variant == 0 ? (float)((int64_t)(w >> 40) - (1ll << 23)) * 0x1p-24f
+                       : (float)((int64_t)(w >> 42) - (1ll << 21)) * 0x1p-24f;
+    } else if (dtype == 0) {
+      v = variant == 0 ? (float)((int64_t)(w >> 40) - (1ll << 23)) * 0x1p-31f
+                       : (float)((int64_t)(w >> 53) - 1024) * 0x1p-20f;
+    } else {
+      v = (float)((int64_t)(w >> 56) - 128) * (variant == 0 ? 0x1p-14f : 0x1p-17f);
+    }
+    if (dtype == 1 && kind != 2)
+      static_cast<uint16_t *>(dst)[i] = (uint16_t)(__float_as_uint(v) >> 16);
+    else
+      static_cast<float *>(dst)[i] = v;
+  }
+}
+
+cudaError_t launch_synth(void *dst, int64_t n, int64_t elem_offset, int dtype, uint64_t key, int kind, int variant,
+                         cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  synth_fill_kernel<<<(int)blocks, 256, 0, s>>>(dst, n, elem_offset, dtype, key, kind, variant);
+  return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(256) copy_kernel(float4 *__restrict__ dst, const float4 *__restrict__ src, int64_t nv) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < nv; i += 4 * stride) {
+    float4 a = __ldcs(src + i), b = __ldcs(src + i + stride), c = __ldcs(src + i + 2 * stride),
+           d = __ldcs(src + i + 3 * stride);
+    __stcs(dst + i, a);
+    __stcs(dst + i + stride, b);
+    __stcs(dst + i + 2 * stride, c);
+    __stcs(dst + i + 3 * stride, d);
+  }
+  for (; i < nv; i += stride) __stcs(dst + i, __ldcs(src + i));
+}
+
+cudaError_t launch_copy(void *dst, const void *src, int64_t bytes, cudaStream_t s, int sm_count) {
+  int64_t nv = bytes / 16;
+  if (nv <= 0) return cudaSuccess;
+  copy_kernel<<<sm_count * 8, 256, 0, s>>>(static_cast<float4 *>(dst), static_cast<const float4 *>(src), nv);
+  return cudaGetLastError();
+}
+
+}  // namespace mlf

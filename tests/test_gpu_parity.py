@@ -1,0 +1,250 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the oracle, element by element.
+
+Bit-exact in pinned-order mode (R17): the kernel folds each commit's members
+left to right in O(U) order with fp32 adds and applies w - (lr*x) with two
+roundings, exactly like oracle/numerics.py, so fp32 and bf16 results must be
+memcmp-equal; the exact-arithmetic variant additionally equals the exact rational
+result for ANY order (data movement pinned independently of order).
+"""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import synthgen as sg  # noqa: E402
+from oracle.numerics import commit_batch, execute_plan  # noqa: E402
+from oracle.plan import Item, Params, make_net, plan as oracle_plan  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_1907_00434_b200 import mlfabric as m
+    from paper_1907_00434_b200.harness import Workload
+    from synthgen import configs
+
+SEED = 0x4D4C46
+
+
+def bits(a):
+    return np.ascontiguousarray(a).view(np.uint32)
+
+
+def gpu_run(S, W, dtype, plan_d, *, lr=0.01, variant=0, iteration=0, backup=False, host_updates=False):
+    """Fill W slots + w0 on cuda:0 with the generator, submit every worker, execute plan_d."""
+    dev = torch.device("cuda", 0)
+    tdt = torch.bfloat16 if dtype == sg.DTYPE_BF16 else torch.float32
+    slots = [torch.empty(S, dtype=tdt, device=dev) for _ in range(W)]
+    for w, t in enumerate(slots):
+        m.synth_fill(0, t.data_ptr(), S, dtype=dtype, seed=SEED, kind=1, a=w, b=iteration, variant=variant)
+    wt = torch.empty(S, dtype=torch.float32, device=dev)
+    m.synth_fill(0, wt.data_ptr(), S, dtype=m.MLF_F32, seed=SEED, kind=2, variant=variant)
+    bk = torch.full((S,), float("nan"), dtype=torch.float32, device=dev) if backup else None
+    hosts = []
+    if host_updates:
+        for t in slots:
+            hosts.append(t.cpu().pin_memory())
+            t.zero_()
+    ctx = m.Context(device=0, model_shard=wt, update_slots=slots, lr=lr, model_elems=S, dtype=dtype,
+                    backup_shard=bk, stream=torch.cuda.current_stream().cuda_stream)
+    for w in range(W):
+        ctx.submit(w, 0, 0, 1.0)
+        if host_updates:
+            ctx.set_update_host(w, hosts[w].data_ptr())
+    pb = m.plan_from_dict(plan_d)
+    ctx.execute(pb)
+    ms = ctx.sync()
+    out = wt.cpu().numpy()
+    b = bk.cpu().numpy() if backup else None
+    stats = ctx.stats()
+    ctx.close()
+    return out, b, ms, stats
+
+
+def oracle_run(S, dtype, plan_d, *, lr=0.01, variant=0, iteration=0, idx=None):
+    idx = np.arange(S) if idx is None else idx
+    w0 = sg.w0_values(SEED, idx, ["normal", "exact"][variant])
+    op = lambda g: sg.update_values(SEED, g, iteration, idx, dtype, ["normal", "exact"][variant])  # noqa: E731
+    w, b, _ = execute_plan(w0, plan_d, op, lr)
+    return w, b
+
+
+def random_plan(rng, W, n_commit=None, max_group=4, boundary=None):
+    n_commit = int(rng.integers(0, W + 1)) if n_commit is None else n_commit
+    order = [int(x) for x in rng.permutation(W)[:n_commit]]
+    first, count, pos = [], [], 0
+    n_direct = int(rng.integers(0, n_commit + 1))
+    for _ in range(n_direct):
+        first.append(pos)
+        count.append(1)
+        pos += 1
+    gid = 0
+    group = [-1] * W
+    for g in order[:n_direct]:
+        group[g] = 0
+    while pos < n_commit:
+        c = int(min(rng.integers(1, max_group + 1), n_commit - pos))
+        gid += 1
+        first.append(pos)
+        count.append(c)
+        for q in range(pos, pos + c):
+            group[order[q]] = gid
+        pos += c
+    if boundary is None:
+        boundary = int(rng.integers(-1, len(first) + 1))
+    return {"n_commit": n_commit, "order": order, "drop_reason": [0 if group[g] >= 0 else 1 for g in range(W)],
+            "group": group, "n_direct": n_direct, "n_groups": gid, "group_node": [0] * gid,
+            "n_server_commits": len(first), "commit_first": first, "commit_count": count,
+            "replica_boundary_commit": boundary, "n_punted": 0, "punted": []}
+
+
+def test_synth_fill_matches_generator():
+    dev = torch.device("cuda", 0)
+    n, off = 100_003, 12_345_678
+    for dtype, tdt in ((sg.DTYPE_F32, torch.float32), (sg.DTYPE_BF16, torch.bfloat16)):
+        for variant, vn in ((0, "normal"), (1, "exact")):
+            t = torch.empty(n, dtype=tdt, device=dev)
+            m.synth_fill(0, t.data_ptr(), n, elem_offset=off, dtype=dtype, seed=SEED, kind=1, a=7, b=3,
+                         variant=variant)
+            ref = sg.update_values(SEED, 7, 3, np.arange(off, off + n), dtype, vn)
+            got = t.cpu().view(torch.int16 if dtype else torch.int32).numpy()
+            assert np.array_equal(got.view(ref.dtype), ref)
+    t = torch.empty(n, dtype=torch.float32, device=dev)
+    m.synth_fill(0, t.data_ptr(), n, elem_offset=off, dtype=0, seed=SEED, kind=2)
+    assert np.array_equal(bits(t.cpu().numpy()), bits(sg.w0_values(SEED, np.arange(off, off + n))))
+
+
+@pytest.mark.parametrize("dtype", [sg.DTYPE_F32, sg.DTYPE_BF16])
+def test_random_plans_bitwise(dtype):
+    rng = np.random.default_rng(dtype + 11)
+    for trial in range(8):
+        S = int(rng.choice([1, 3, 4, 257, 4099, 65_537, 300_001]))
+        W = int(rng.integers(1, 24))
+        p = random_plan(rng, W)
+        w, b, _, _ = gpu_run(S, W, dtype, p, backup=True)
+        wr, br = oracle_run(S, dtype, p)
+        assert np.array_equal(bits(w), bits(wr)), (trial, S, W)
+        if p["replica_boundary_commit"] >= 0:
+            assert np.array_equal(bits(b), bits(br))
+        else:
+            assert np.all(np.isnan(b))                     # no replica write
+
+
+def test_exact_variant_any_order():
+    rng = np.random.default_rng(3)
+    S, W = 131_075, 256
+    p = random_plan(rng, W, n_commit=256, max_group=16, boundary=3)
+    w, b, _, _ = gpu_run(S, W, sg.DTYPE_F32, p, lr=2.0**-4, variant=1, backup=True)
+    wr, br = oracle_run(S, sg.DTYPE_F32, p, lr=2.0**-4, variant=1)
+    assert np.array_equal(bits(w), bits(wr)) and np.array_equal(bits(b), bits(br))
+    # same updates in reverse order, all direct: identical bits (no rounding occurs)
+    rev = random_plan(rng, W, n_commit=0)
+    rev.update(order=p["order"][::-1], n_commit=256, n_direct=256, n_groups=0, group=[0] * W,
+               commit_first=list(range(256)), commit_count=[1] * 256, n_server_commits=256,
+               replica_boundary_commit=-1, drop_reason=[0] * W, group_node=[])
+    w2, _, _, _ = gpu_run(S, W, sg.DTYPE_F32, rev, lr=2.0**-4, variant=1)
+    assert np.array_equal(bits(w2), bits(w))
+
+
+def test_operand_list_longer_than_one_launch():
+    # > kMaxOps operands: split at commit boundaries, still one logical pass per commit
+    rng = np.random.default_rng(5)
+    S, W = 1031, 1100
+    p = random_plan(rng, W, n_commit=1100, max_group=7, boundary=150)
+    w, b, _, stats = gpu_run(S, W, sg.DTYPE_BF16, p, backup=True)
+    wr, br = oracle_run(S, sg.DTYPE_BF16, p)
+    assert np.array_equal(bits(w), bits(wr)) and np.array_equal(bits(b), bits(br))
+    assert stats[0] == 2
+
+
+def test_degenerate_batches():
+    rng = np.random.default_rng(9)
+    S = 5000
+    empty = random_plan(rng, 6, n_commit=0, boundary=-1)
+    w, _, _, stats = gpu_run(S, 6, sg.DTYPE_F32, empty)
+    assert np.array_equal(bits(w), bits(sg.w0_values(SEED, np.arange(S)))) and stats[0] == 0
+    snap = random_plan(rng, 6, n_commit=0, boundary=0)      # all dropped, carried items frozen
+    w, b, _, _ = gpu_run(S, 6, sg.DTYPE_F32, snap, backup=True)
+    assert np.array_equal(bits(b), bits(w))
+    one = random_plan(rng, 1, n_commit=1, boundary=1)
+    w, b, _, _ = gpu_run(1, 1, sg.DTYPE_F32, one, backup=True)
+    wr, br = oracle_run(1, sg.DTYPE_F32, one)
+    assert np.array_equal(bits(w), bits(wr)) and np.array_equal(bits(b), bits(br))
+
+
+def test_host_resident_updates_move_only_when_committed():
+    rng = np.random.default_rng(12)
+    S, W = 70_001, 10
+    p = random_plan(rng, W, n_commit=4, boundary=-1)
+    w, _, _, stats = gpu_run(S, W, sg.DTYPE_F32, p, host_updates=True)
+    wr, _ = oracle_run(S, sg.DTYPE_F32, p)
+    assert np.array_equal(bits(w), bits(wr))
+    assert stats[1] == 4 * S * 4                             # h2d bytes: committed updates only
+
+
+def test_invalid_plan_rejected_without_device_work():
+    dev = torch.device("cuda", 0)
+    S = 64
+    slots = [torch.zeros(S, device=dev) for _ in range(3)]
+    wt = torch.ones(S, device=dev)
+    ctx = m.Context(device=0, model_shard=wt, update_slots=slots, lr=0.5, model_elems=S,
+                    stream=torch.cuda.current_stream().cuda_stream)
+    ctx.submit(0, 0)
+    ctx.submit(1, 0)
+    with pytest.raises(m.MlfError) as e:
+        ctx.submit(1, 0)
+    assert e.value.code == m.MLF_E_STATE
+    bad = random_plan(np.random.default_rng(0), 2, n_commit=2)
+    bad["order"] = [0, 5]
+    with pytest.raises(m.MlfError) as e:
+        ctx.execute(m.plan_from_dict(bad))
+    assert e.value.code == m.MLF_E_INVALID
+    rep = random_plan(np.random.default_rng(0), 2, n_commit=2, boundary=1)
+    with pytest.raises(m.MlfError) as e:                     # replica write without a backup shard
+        ctx.execute(m.plan_from_dict(rep))
+    assert e.value.code == m.MLF_E_INVALID
+    assert ctx.stats()[0] == 0 and torch.all(wt == 1)
+    ctx.close()
+
+
+@pytest.mark.parametrize("it_count", [3])
+def test_config1_end_to_end_vs_oracle(it_count):
+    cfg = configs.config(1)
+    wl = Workload(cfg, device=0)
+    S = cfg["S"]
+    idx = np.arange(S)
+    w_ref = sg.w0_values(cfg["seed"], idx)
+    for it in range(it_count):
+        v_init = wl.v_init
+        pb, pd, draws = wl.step(it)
+        wl.ctx.sync()
+        up, down, site = configs.network(cfg, it)
+        batch = [Item(w, S * 4, d["version"], d["t_avail"], d["norm"]) for w, d in enumerate(draws)]
+        op = oracle_plan(make_net(cfg["n_nodes"], up, down, None, site), batch,
+                         Params(servers=cfg["servers"], aggs=cfg["aggs"], v_init=v_init, tau_max=cfg["tau"]))
+        assert op == pd
+        w_ref, _, _ = execute_plan(w_ref, op, lambda g: sg.update_values(cfg["seed"], g, it, idx), cfg["lr"])
+        got = wl.w.cpu().numpy()
+        assert np.array_equal(bits(got), bits(w_ref))
+    assert wl.ctx.version() == wl.v_init
+
+
+@pytest.mark.parametrize("tau,dtype", [(4, "f32"), (32, "f32"), (32, "bf16")])
+def test_config2_full_size_sampled(tau, dtype):
+    """BASELINE config 2 at full size (25.6M elements, 32 workers) in the launch configuration bench.py
+    times; every element checked bitwise against the oracle at 20k sampled indices (incl. the tail)."""
+    cfg = configs.config(2, tau=tau, dtype=dtype)
+    wl = Workload(cfg, device=0)
+    S = cfg["S"]
+    rng = np.random.default_rng(tau)
+    idx = np.unique(np.concatenate([rng.integers(0, S, 20_000), np.arange(S - 37, S), np.arange(0, 37)]))
+    dt = sg.DTYPE_BF16 if dtype == "bf16" else sg.DTYPE_F32
+    w_ref = sg.w0_values(cfg["seed"], idx)
+    for it in range(2):
+        pb, pd, draws = wl.step(it)
+        wl.ctx.sync()
+        w_ref, _, _ = execute_plan(w_ref, pd, lambda g: sg.update_values(cfg["seed"], g, it, idx, dt), cfg["lr"])
+        got = wl.w.cpu().numpy()[idx]
+        assert np.array_equal(bits(got), bits(w_ref))
+        assert pd["n_commit"] == min(tau, 32)
