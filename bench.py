@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--no-variants", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--kernel", default=os.environ.get("MLF_COMMIT_IMPL", "ldg"), choices=["ldg", "bulk"])
     return ap.parse_args()
 
 
@@ -207,9 +208,17 @@ def run_single(a):
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
     peak, peak_src = hbm_peak()
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush_w = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush_r = torch.ones(64 << 20, dtype=torch.float32, device=dev)
 
-    def measure(tau, dtype, steps, warmup, clocks=False):
+    def l2_flush():
+        # evict L2 with a 256 MiB write, then leave it holding clean unrelated lines (256 MiB read)
+        # so the timed kernel neither hits stale operands nor pays for write-backs of dirty flush data
+        flush_w.zero_()
+        flush_r.sum()
+
+    def measure(tau, dtype, steps, warmup, kernel, clocks=False):
+        os.environ["MLF_COMMIT_IMPL"] = kernel
         cfg = configs.config(cid, tau=tau, dtype=dtype)
         wl = Workload(cfg, device=0)
         wl.fill_updates(0)
@@ -228,7 +237,7 @@ def run_single(a):
             pb = wl.plan(s)
             plan_ms = (time.perf_counter() - t0) * 1e3
             pd = pb.to_dict(cfg["W"])
-            flush.zero_()
+            l2_flush()
             wl.ctx.execute(pb)
             ms = wl.ctx.sync()
             wl.after_commit(pd, draws)
@@ -246,15 +255,26 @@ def run_single(a):
         T = sum(r["ms"] for r in recs)
         return cfg, recs, T, ck, kl
 
+    def summarize(recs, T):
+        v = sum(r["bytes"] for r in recs) / (T / 1e3) / 1e9
+        ach = sum(r["alg"] for r in recs) / (T / 1e3) / 1e9
+        return {"value": round(v, 2), "unit": "GB/s", "ms_per_step": round(T / len(recs), 4),
+                "roofline_frac": round(ach / peak, 4), "achieved_GBps": round(ach, 1)}
+
     # warm-up + timed region (barrier + synchronize on both sides: single process)
     torch.cuda.synchronize()
-    cfg, recs, T, ck, kl = measure(a.tau, a.dtype, a.steps, a.warmup, clocks=True)
+    cfg, recs, T, ck, kl = measure(a.tau, a.dtype, a.steps, a.warmup, a.kernel, clocks=True)
     torch.cuda.synchronize()
     tot_bytes = sum(r["bytes"] for r in recs)
     value = tot_bytes / (T / 1e3) / 1e9
     alg = sum(r["alg"] for r in recs)
     achieved = alg / (T / 1e3) / 1e9
-    kernel_launches = kl
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        tj = json.load(open(tpath))
+        key = f"config{cid}_tau{cfg['tau']}_{a.dtype}_{a.kernel}"
+        traffic = tj.get(key)
     line = {
         "metric": "aggregated update GB/s committed (device-timed, max over ranks)",
         "value": round(value, 2), "unit": "GB/s", "n_gpus": 1, "steps": a.steps, "warmup": a.warmup,
@@ -264,22 +284,27 @@ def run_single(a):
                    "tau_max": cfg["tau"], "update_dtype": a.dtype, "shards": 1,
                    "committed_per_step": round(sum(r["commits"] for r in recs) / len(recs), 2),
                    "groups_per_step": round(sum(r["groups"] for r in recs) / len(recs), 2),
-                   "l2": "flushed (256 MiB write) before every step; operands >> L2"},
+                   "l2": "flushed before every step (256 MiB write + 256 MiB read); operands >> L2"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_src,
-                     "kernel": "fused_commit_ldg",
+                     "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
+                     "kernel": f"fused_commit_{a.kernel}",
                      "algorithmic_bytes_per_step": int(alg / len(recs))},
         "planner_ms": round(sum(r["plan_ms"] for r in recs) / len(recs), 3),
-        "gpu_launches": int(kernel_launches),
+        "gpu_launches": int(kl),
         "clocks": ck.summary(),
     }
-    # variant: tau = #workers (the paper's practice)
-    if not a.no_variants and cid == 2 and (a.tau is None or a.tau != 32):
-        cfg2, recs2, T2, _, _ = measure(32, a.dtype, max(5, a.steps // 2), 3)
-        v2 = sum(r["bytes"] for r in recs2) / (T2 / 1e3) / 1e9
-        ach2 = sum(r["alg"] for r in recs2) / (T2 / 1e3) / 1e9
-        line["variants"] = {"tau32": {"value": round(v2, 2), "unit": "GB/s", "ms_per_step": round(T2 / len(recs2), 4),
-                                      "roofline_frac": round(ach2 / peak, 4), "achieved_GBps": round(ach2, 1)}}
+    if not a.no_variants:
+        var = {}
+        other = "bulk" if a.kernel == "ldg" else "ldg"
+        nv = max(5, a.steps // 2)
+        _, r2, T2, _, _ = measure(a.tau, a.dtype, nv, 3, other)
+        var[f"kernel_{other}"] = summarize(r2, T2)
+        if cid == 2 and (a.tau is None or a.tau != 32):
+            for k in (a.kernel, other):
+                _, r3, T3, _, _ = measure(32, a.dtype, nv, 3, k)
+                var[f"tau32_{k}"] = summarize(r3, T3)
+        line["variants"] = var
+        os.environ["MLF_COMMIT_IMPL"] = a.kernel
     # e2e through the public API with host buffers
     if not a.no_e2e:
         line["e2e"] = e2e_single(cid, a)

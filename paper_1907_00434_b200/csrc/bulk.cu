@@ -1,2 +1,221 @@
-// bulk.cu — placeholder translation unit for the TMA bulk-copy commit pipeline.
+// bulk.cu — fused ordered commit with TMA bulk copies (cp.async.bulk) into a
+// shared-memory ring, warp-specialised (sm_100a).
+//
+// Same arithmetic as fused_commit_ldg (commit.cu; Eq. 2 P:278 with
+// gamma = 0, in-group left fold in O(U) order P:712-715/P:1069-1070, two fp32
+// roundings per commit R17, mirror store R16), different data movement:
+//   * one persistent CTA per SM; a producer warp (one elected lane) streams, for
+//     every tile of kTile elements of the shard, the w tile and then each
+//     operand's tile, in commit order, into a kStages-deep ring of shared-memory
+//     stages with cp.async.bulk.shared::cluster.global.mbarrier::complete_tx
+//     (SASS UBLKCP) — tens of KB in flight per SM independent of register
+//     pressure and operand count, one instruction per 8 KB;
+//   * 8 consumer warps wait on the stage's full mbarrier, fold the tile from
+//     shared memory in the pinned order, release the stage (empty mbarrier),
+//     and write w (and the mirror) back with 128-bit streaming stores.
+// Tiles are dealt round-robin to the persistent CTAs (tile = cta + k * grid).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
 #include "kernels.h"
+
+namespace mlf {
+namespace bulk {
+
+constexpr int kTile = 2048;                     // elements per tile
+constexpr int kStageBytes = kTile * 4;          // an fp32 tile (bf16 tiles use half a stage)
+constexpr int kStages = 24;                     // 192 KB ring
+constexpr int kConsumerWarps = 8;
+constexpr int kConsumers = kConsumerWarps * 32;
+constexpr int kThreads = kConsumers + 32;       // + 1 producer warp
+constexpr int kChunks = kTile / 4 / kConsumers; // float4 chunks per consumer thread per tile (2)
+constexpr size_t kSmem = (size_t)kStages * kStageBytes + 2 * kStages * sizeof(uint64_t);
+
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ float4 add4(float4 a, float4 b) {
+  return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
+}
+__device__ __forceinline__ float4 apply4(float4 w, float lr, float4 x) {
+  return make_float4(__fsub_rn(w.x, __fmul_rn(lr, x.x)), __fsub_rn(w.y, __fmul_rn(lr, x.y)),
+                     __fsub_rn(w.z, __fmul_rn(lr, x.z)), __fsub_rn(w.w, __fmul_rn(lr, x.w)));
+}
+__device__ __forceinline__ float4 widen_bf16x4(uint2 u) {
+  return make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xffff0000u), __uint_as_float(u.y << 16),
+                     __uint_as_float(u.y & 0xffff0000u));
+}
+
+__global__ void __launch_bounds__(kThreads, 1) fused_commit_bulk(const __grid_constant__ CommitArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)kStages * kStageBytes);
+  uint64_t *empty = full + kStages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t n_bulk = a.n & ~int64_t(7);       // bulk region: whole 8-element groups (16 B for bf16)
+  const int64_t n_tiles = (n_bulk + kTile - 1) / kTile;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kConsumerWarps) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      uint32_t L = 0;
+      for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        const int64_t e0 = t * kTile;
+        const uint32_t cnt = (uint32_t)(n_bulk - e0 < kTile ? n_bulk - e0 : kTile);
+        for (int j = -1; j < a.n_ops; ++j, ++L) {
+          const uint32_t s = L % kStages;
+          if (L >= (uint32_t)kStages) mbar_wait(&empty[s], ((L / kStages) & 1) ^ 1);
+          const void *src;
+          uint32_t bytes;
+          if (j < 0) {
+            src = a.w + e0;
+            bytes = cnt * 4;
+          } else if (a.flag[j] & kOpBf16) {
+            src = static_cast<const uint16_t *>(a.op[j]) + a.src_off + e0;
+            bytes = cnt * 2;
+          } else {
+            src = static_cast<const float *>(a.op[j]) + a.src_off + e0;
+            bytes = cnt * 4;
+          }
+          mbar_expect_tx(&full[s], bytes);
+          bulk_g2s(smem + (size_t)s * kStageBytes, src, bytes, &full[s]);
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ consumers
+    const int tid = threadIdx.x;
+    uint32_t L = 0;
+    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      const int64_t e0 = t * kTile;
+      const int cnt = (int)(n_bulk - e0 < kTile ? n_bulk - e0 : kTile);
+      float4 w[kChunks], x[kChunks];
+      {
+        const uint32_t s = L % kStages;
+        mbar_wait(&full[s], (L / kStages) & 1);
+        const float4 *sw = reinterpret_cast<const float4 *>(smem + (size_t)s * kStageBytes);
+#pragma unroll
+        for (int k = 0; k < kChunks; ++k) {
+          const int c = tid + k * kConsumers;
+          if (c * 4 < cnt) w[k] = sw[c];
+          x[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        ++L;
+      }
+      if (a.backup_after == -1) {
+#pragma unroll
+        for (int k = 0; k < kChunks; ++k) {
+          const int c = tid + k * kConsumers;
+          if (c * 4 < cnt) __stcs(reinterpret_cast<float4 *>(a.backup + e0) + c, w[k]);
+        }
+      }
+      for (int j = 0; j < a.n_ops; ++j, ++L) {
+        const uint32_t s = L % kStages;
+        const uint8_t f = a.flag[j];
+        mbar_wait(&full[s], (L / kStages) & 1);
+        const uint8_t *st = smem + (size_t)s * kStageBytes;
+#pragma unroll
+        for (int k = 0; k < kChunks; ++k) {
+          const int c = tid + k * kConsumers;
+          if (c * 4 < cnt) {
+            const float4 u = (f & kOpBf16) ? widen_bf16x4(reinterpret_cast<const uint2 *>(st)[c])
+                                           : reinterpret_cast<const float4 *>(st)[c];
+            x[k] = (f & kOpFirst) ? u : add4(x[k], u);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (f & kOpLast) {
+#pragma unroll
+          for (int k = 0; k < kChunks; ++k) w[k] = apply4(w[k], a.lr, x[k]);
+          if (j == a.backup_after) {
+#pragma unroll
+            for (int k = 0; k < kChunks; ++k) {
+              const int c = tid + k * kConsumers;
+              if (c * 4 < cnt) __stcs(reinterpret_cast<float4 *>(a.backup + e0) + c, w[k]);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kChunks; ++k) {
+        const int c = tid + k * kConsumers;
+        if (c * 4 < cnt) __stcs(reinterpret_cast<float4 *>(a.w + e0) + c, w[k]);
+      }
+    }
+    // ragged tail (< 8 elements) on CTA 0
+    const int64_t tail = a.n - n_bulk;
+    if (blockIdx.x == 0 && tid < tail) {
+      const int64_t e = n_bulk + tid;
+      float wv = a.w[e];
+      if (a.backup_after == -1) a.backup[e] = wv;
+      float xv = 0.f;
+      for (int j = 0; j < a.n_ops; ++j) {
+        const uint8_t f = a.flag[j];
+        const float u = (f & kOpBf16)
+                            ? __uint_as_float(uint32_t(static_cast<const uint16_t *>(a.op[j])[a.src_off + e]) << 16)
+                            : static_cast<const float *>(a.op[j])[a.src_off + e];
+        xv = (f & kOpFirst) ? u : __fadd_rn(xv, u);
+        if (f & kOpLast) {
+          wv = __fsub_rn(wv, __fmul_rn(a.lr, xv));
+          if (j == a.backup_after) a.backup[e] = wv;
+        }
+      }
+      a.w[e] = wv;
+    }
+  }
+}
+
+}  // namespace bulk
+
+cudaError_t launch_commit_bulk(const CommitArgs &a, cudaStream_t s, int sm_count) {
+  static bool init = false;
+  if (!init) {
+    cudaError_t e = cudaFuncSetAttribute(bulk::fused_commit_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)bulk::kSmem);
+    if (e != cudaSuccess) return e;
+    init = true;
+  }
+  const int64_t n_tiles = ((a.n & ~int64_t(7)) + bulk::kTile - 1) / bulk::kTile;
+  int grid = (int)(n_tiles < sm_count ? (n_tiles > 0 ? n_tiles : 1) : sm_count);
+  bulk::fused_commit_bulk<<<grid, bulk::kThreads, bulk::kSmem, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace mlf

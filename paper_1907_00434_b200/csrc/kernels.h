@@ -41,6 +41,7 @@ struct ReduceArgs {
 enum class CommitImpl : int { kLdg = 0, kBulk = 1 };
 
 cudaError_t launch_commit(const CommitArgs &a, cudaStream_t s, int sm_count, CommitImpl impl);
+cudaError_t launch_commit_bulk(const CommitArgs &a, cudaStream_t s, int sm_count);
 cudaError_t launch_reduce(const ReduceArgs &a, cudaStream_t s, int sm_count);
 cudaError_t launch_synth(void *dst, int64_t n, int64_t elem_offset, int dtype, uint64_t key, int kind,
                          int variant, cudaStream_t s);

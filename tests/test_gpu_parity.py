@@ -6,7 +6,7 @@ roundings, exactly like oracle/numerics.py, so fp32 and bf16 results must be
 memcmp-equal; the exact-arithmetic variant additionally equals the exact rational
 result for ANY order (data movement pinned independently of order).
 """
-import math
+import os
 
 import numpy as np
 import pytest
@@ -31,8 +31,10 @@ def bits(a):
     return np.ascontiguousarray(a).view(np.uint32)
 
 
-def gpu_run(S, W, dtype, plan_d, *, lr=0.01, variant=0, iteration=0, backup=False, host_updates=False):
+def gpu_run(S, W, dtype, plan_d, *, lr=0.01, variant=0, iteration=0, backup=False, host_updates=False,
+            impl="ldg"):
     """Fill W slots + w0 on cuda:0 with the generator, submit every worker, execute plan_d."""
+    os.environ["MLF_COMMIT_IMPL"] = impl                     # read at mlf_init
     dev = torch.device("cuda", 0)
     tdt = torch.bfloat16 if dtype == sg.DTYPE_BF16 else torch.float32
     slots = [torch.empty(S, dtype=tdt, device=dev) for _ in range(W)]
@@ -115,14 +117,18 @@ def test_synth_fill_matches_generator():
     assert np.array_equal(bits(t.cpu().numpy()), bits(sg.w0_values(SEED, np.arange(off, off + n))))
 
 
+IMPLS = ["ldg", "bulk"]
+
+
+@pytest.mark.parametrize("impl", IMPLS)
 @pytest.mark.parametrize("dtype", [sg.DTYPE_F32, sg.DTYPE_BF16])
-def test_random_plans_bitwise(dtype):
+def test_random_plans_bitwise(dtype, impl):
     rng = np.random.default_rng(dtype + 11)
     for trial in range(8):
-        S = int(rng.choice([1, 3, 4, 257, 4099, 65_537, 300_001]))
+        S = int(rng.choice([1, 3, 4, 9, 257, 2055, 4099, 65_537, 300_001]))
         W = int(rng.integers(1, 24))
         p = random_plan(rng, W)
-        w, b, _, _ = gpu_run(S, W, dtype, p, backup=True)
+        w, b, _, _ = gpu_run(S, W, dtype, p, backup=True, impl=impl)
         wr, br = oracle_run(S, dtype, p)
         assert np.array_equal(bits(w), bits(wr)), (trial, S, W)
         if p["replica_boundary_commit"] >= 0:
@@ -131,11 +137,12 @@ def test_random_plans_bitwise(dtype):
             assert np.all(np.isnan(b))                     # no replica write
 
 
-def test_exact_variant_any_order():
+@pytest.mark.parametrize("impl", IMPLS)
+def test_exact_variant_any_order(impl):
     rng = np.random.default_rng(3)
     S, W = 131_075, 256
     p = random_plan(rng, W, n_commit=256, max_group=16, boundary=3)
-    w, b, _, _ = gpu_run(S, W, sg.DTYPE_F32, p, lr=2.0**-4, variant=1, backup=True)
+    w, b, _, _ = gpu_run(S, W, sg.DTYPE_F32, p, lr=2.0**-4, variant=1, backup=True, impl=impl)
     wr, br = oracle_run(S, sg.DTYPE_F32, p, lr=2.0**-4, variant=1)
     assert np.array_equal(bits(w), bits(wr)) and np.array_equal(bits(b), bits(br))
     # same updates in reverse order, all direct: identical bits (no rounding occurs)
@@ -143,32 +150,34 @@ def test_exact_variant_any_order():
     rev.update(order=p["order"][::-1], n_commit=256, n_direct=256, n_groups=0, group=[0] * W,
                commit_first=list(range(256)), commit_count=[1] * 256, n_server_commits=256,
                replica_boundary_commit=-1, drop_reason=[0] * W, group_node=[])
-    w2, _, _, _ = gpu_run(S, W, sg.DTYPE_F32, rev, lr=2.0**-4, variant=1)
+    w2, _, _, _ = gpu_run(S, W, sg.DTYPE_F32, rev, lr=2.0**-4, variant=1, impl=impl)
     assert np.array_equal(bits(w2), bits(w))
 
 
-def test_operand_list_longer_than_one_launch():
+@pytest.mark.parametrize("impl", IMPLS)
+def test_operand_list_longer_than_one_launch(impl):
     # > kMaxOps operands: split at commit boundaries, still one logical pass per commit
     rng = np.random.default_rng(5)
     S, W = 1031, 1100
     p = random_plan(rng, W, n_commit=1100, max_group=7, boundary=150)
-    w, b, _, stats = gpu_run(S, W, sg.DTYPE_BF16, p, backup=True)
+    w, b, _, stats = gpu_run(S, W, sg.DTYPE_BF16, p, backup=True, impl=impl)
     wr, br = oracle_run(S, sg.DTYPE_BF16, p)
     assert np.array_equal(bits(w), bits(wr)) and np.array_equal(bits(b), bits(br))
     assert stats[0] == 2
 
 
-def test_degenerate_batches():
+@pytest.mark.parametrize("impl", IMPLS)
+def test_degenerate_batches(impl):
     rng = np.random.default_rng(9)
     S = 5000
     empty = random_plan(rng, 6, n_commit=0, boundary=-1)
-    w, _, _, stats = gpu_run(S, 6, sg.DTYPE_F32, empty)
+    w, _, _, stats = gpu_run(S, 6, sg.DTYPE_F32, empty, impl=impl)
     assert np.array_equal(bits(w), bits(sg.w0_values(SEED, np.arange(S)))) and stats[0] == 0
     snap = random_plan(rng, 6, n_commit=0, boundary=0)      # all dropped, carried items frozen
-    w, b, _, _ = gpu_run(S, 6, sg.DTYPE_F32, snap, backup=True)
+    w, b, _, _ = gpu_run(S, 6, sg.DTYPE_F32, snap, backup=True, impl=impl)
     assert np.array_equal(bits(b), bits(w))
     one = random_plan(rng, 1, n_commit=1, boundary=1)
-    w, b, _, _ = gpu_run(1, 1, sg.DTYPE_F32, one, backup=True)
+    w, b, _, _ = gpu_run(1, 1, sg.DTYPE_F32, one, backup=True, impl=impl)
     wr, br = oracle_run(1, sg.DTYPE_F32, one)
     assert np.array_equal(bits(w), bits(wr)) and np.array_equal(bits(b), bits(br))
 
@@ -210,6 +219,7 @@ def test_invalid_plan_rejected_without_device_work():
 
 @pytest.mark.parametrize("it_count", [3])
 def test_config1_end_to_end_vs_oracle(it_count):
+    os.environ["MLF_COMMIT_IMPL"] = "ldg"
     cfg = configs.config(1)
     wl = Workload(cfg, device=0)
     S = cfg["S"]
@@ -230,10 +240,12 @@ def test_config1_end_to_end_vs_oracle(it_count):
     assert wl.ctx.version() == wl.v_init
 
 
+@pytest.mark.parametrize("impl", IMPLS)
 @pytest.mark.parametrize("tau,dtype", [(4, "f32"), (32, "f32"), (32, "bf16")])
-def test_config2_full_size_sampled(tau, dtype):
+def test_config2_full_size_sampled(tau, dtype, impl):
     """BASELINE config 2 at full size (25.6M elements, 32 workers) in the launch configuration bench.py
     times; every element checked bitwise against the oracle at 20k sampled indices (incl. the tail)."""
+    os.environ["MLF_COMMIT_IMPL"] = impl
     cfg = configs.config(2, tau=tau, dtype=dtype)
     wl = Workload(cfg, device=0)
     S = cfg["S"]
