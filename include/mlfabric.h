@@ -247,6 +247,19 @@ mlf_status mlf_ipc_export(int32_t device, const void *dev_ptr, mlf_ipc_handle *o
 mlf_status mlf_ipc_open(int32_t device, const mlf_ipc_handle *h, void **dev_ptr);
 mlf_status mlf_ipc_close(int32_t device, void *dev_ptr, int64_t offset);
 
+/* Cross-process ordering of the two execution phases without a device-idle host
+ * barrier: every context owns an interprocess "phase 1 done" event, recorded on
+ * its stream at the end of mlf_execute_phase(MLF_PHASE_AGGREGATE).  Before its
+ * phase 2 launches a context waits (cudaStreamWaitEvent) on the events opened
+ * with mlf_phase_events_open.  The caller must order the calls: every rank's
+ * phase-1 call returns (record enqueued) before any rank calls phase 2 — a host
+ * barrier between the two calls, which overlaps with the GPUs' phase-1 work. */
+typedef struct {
+  uint8_t handle[64];        /* cudaIpcEventHandle_t */
+} mlf_ipc_event;
+mlf_status mlf_phase_event_export(mlf_ctx *ctx, mlf_ipc_event *out);
+mlf_status mlf_phase_events_open(mlf_ctx *ctx, int32_t n, const mlf_ipc_event *peer_events);
+
 /* ======================================================================
  * Test infrastructure kernels (not on the hot path)
  * ====================================================================== */

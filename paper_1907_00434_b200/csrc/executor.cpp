@@ -78,6 +78,8 @@ struct mlf_ctx {
   std::vector<const void *> host_src;
   // execution state
   cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
+  cudaEvent_t ev_phase = nullptr;                 // interprocess "phase 1 done" (world > 1)
+  std::vector<cudaEvent_t> peer_events;           // opened peers' phase events
   bool started = false, pending = false, sticky = false, phase1_done = false;
   int64_t launches = 0, h2d = 0, d2h = 0;
   CommitImpl impl = CommitImpl::kLdg;
@@ -139,6 +141,7 @@ extern "C" mlf_status mlf_init(const mlf_config *cfg, int64_t v0, mlf_ctx **out)
       CK(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, k.device));
       CK(cudaEventCreate(&c->ev_start));
       CK(cudaEventCreate(&c->ev_stop));
+      if (k.world > 1) CK(cudaEventCreateWithFlags(&c->ev_phase, cudaEventInterprocess | cudaEventDisableTiming));
     } catch (...) {
       delete c;
       throw;
@@ -151,6 +154,8 @@ extern "C" void mlf_destroy(mlf_ctx *c) {
   if (!c) return;
   if (c->ev_start) cudaEventDestroy(c->ev_start);
   if (c->ev_stop) cudaEventDestroy(c->ev_stop);
+  for (auto e : c->peer_events) cudaEventDestroy(e);
+  if (c->ev_phase) cudaEventDestroy(c->ev_phase);
   delete c;
 }
 
@@ -272,8 +277,12 @@ static void record_start(mlf_ctx *c) {
   }
 }
 
+static void reduce_local_groups(mlf_ctx *c, const mlf_plan_out *p);
+
 static void phase_stage(mlf_ctx *c, const mlf_plan_out *p) {
   CK(cudaSetDevice(c->cfg.device));
+  // two-phase multi-GPU batches: the device window starts with the batch on every rank
+  if (c->cfg.world > 1) record_start(c);
   const size_t bytes = (size_t)c->cfg.model_elems * c->elem_bytes;
   // committed host-resident updates homed on this rank move host -> device;
   // dropped ones never move ("dropped at the worker itself")
@@ -285,7 +294,11 @@ static void phase_stage(mlf_ctx *c, const mlf_plan_out *p) {
       c->h2d += (int64_t)bytes;
     }
   }
-  if (!tree_mode(c)) return;
+  if (tree_mode(c)) reduce_local_groups(c, p);
+  if (c->ev_phase) CK(cudaEventRecord(c->ev_phase, c->stream));
+}
+
+static void reduce_local_groups(mlf_ctx *c, const mlf_plan_out *p) {
   // tree_reduce of the groups aggregated on this rank
   for (int ci = 0; ci < p->n_server_commits; ++ci) {
     int first = p->commit_first[ci], cnt = p->commit_count[ci];
@@ -312,6 +325,8 @@ static void phase_stage(mlf_ctx *c, const mlf_plan_out *p) {
 
 static void phase_commit(mlf_ctx *c, const mlf_plan_out *p) {
   CK(cudaSetDevice(c->cfg.device));
+  // aggregates / staged updates of the other ranks are complete (phase events)
+  for (auto e : c->peer_events) CK(cudaStreamWaitEvent(c->stream, e, 0));
   const bool tree = tree_mode(c);
   const uint8_t dflag = c->cfg.update_dtype == MLF_BF16 ? kOpBf16 : 0;
   // operand table in commit order
@@ -404,6 +419,35 @@ extern "C" mlf_status mlf_execute_phase(mlf_ctx *c, const mlf_plan_out *p, int32
   });
   if (st == MLF_E_CUDA && c) c->sticky = true;
   return st;
+}
+
+extern "C" mlf_status mlf_phase_event_export(mlf_ctx *c, mlf_ipc_event *out) {
+  return guard([&] {
+    check_ctx(c);
+    if (!out) throw Fail{MLF_E_INVALID, "null output"};
+    if (!c->ev_phase) throw Fail{MLF_E_STATE, "phase events exist only when world > 1"};
+    cudaIpcEventHandle_t h;
+    CK(cudaIpcGetEventHandle(&h, c->ev_phase));
+    static_assert(sizeof(h) == 64, "ipc event handle size");
+    std::memcpy(out->handle, &h, 64);
+  });
+}
+
+extern "C" mlf_status mlf_phase_events_open(mlf_ctx *c, int32_t n, const mlf_ipc_event *peers) {
+  return guard([&] {
+    check_ctx(c);
+    if (n < 0 || (n > 0 && !peers)) throw Fail{MLF_E_INVALID, "peer events"};
+    CK(cudaSetDevice(c->cfg.device));
+    for (auto e : c->peer_events) cudaEventDestroy(e);
+    c->peer_events.clear();
+    for (int i = 0; i < n; ++i) {
+      cudaIpcEventHandle_t h;
+      std::memcpy(&h, peers[i].handle, 64);
+      cudaEvent_t e;
+      CK(cudaIpcOpenEventHandle(&e, h));
+      c->peer_events.push_back(e);
+    }
+  });
 }
 
 extern "C" mlf_status mlf_execute(mlf_ctx *c, const mlf_plan_out *p) {

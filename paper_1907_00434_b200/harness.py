@@ -22,7 +22,7 @@ class Workload:
 
     def __init__(self, cfg: dict, *, device: int = 0, rank: int = 0, world: int = 1, variant: int = 0,
                  peer_slots=None, backup_ptr=None, agg_slots: int = 0, agg_scratch=None, stream=None,
-                 alloc_slots: bool = True):
+                 slot_tensors: dict | None = None):
         self.cfg = cfg
         self.device, self.rank, self.world = device, rank, world
         self.variant = variant
@@ -37,10 +37,10 @@ class Workload:
         self.backup = torch.zeros(n, dtype=torch.float32, device=dev) if (cfg["replica"] and world == 1) else None
         # update slots of the workers homed here (full-length vectors)
         self.local_workers = [w for w in range(cfg["W"]) if cfg["home"][w] == rank]
-        self.slots = {}
-        if alloc_slots:
-            for w in self.local_workers:
-                self.slots[w] = torch.empty(self.S, dtype=tdt, device=dev)
+        if slot_tensors is not None:
+            self.slots = dict(slot_tensors)
+        else:
+            self.slots = {w: torch.empty(self.S, dtype=tdt, device=dev) for w in self.local_workers}
         slot_ptrs = []
         for w in range(cfg["W"]):
             if w in self.slots:

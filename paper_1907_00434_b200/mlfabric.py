@@ -23,7 +23,8 @@ MLF_PHASE_AGGREGATE, MLF_PHASE_COMMIT = 1, 2
 EXPORTS = (
     "mlf_plan", "mlf_init", "mlf_submit_update", "mlf_set_update_host", "mlf_batch_view", "mlf_version",
     "mlf_execute", "mlf_execute_phase", "mlf_sync", "mlf_pull_model", "mlf_stats", "mlf_destroy",
-    "mlf_last_error", "mlf_ipc_export", "mlf_ipc_open", "mlf_ipc_close", "mlf_synth_fill", "mlf_copy_kernel",
+    "mlf_last_error", "mlf_ipc_export", "mlf_ipc_open", "mlf_ipc_close", "mlf_phase_event_export",
+    "mlf_phase_events_open", "mlf_synth_fill", "mlf_copy_kernel",
 )
 
 
@@ -85,6 +86,10 @@ class MlfIpcHandle(C.Structure):
     _fields_ = [("handle", C.c_uint8 * 64), ("offset", C.c_int64)]
 
 
+class MlfIpcEvent(C.Structure):
+    _fields_ = [("handle", C.c_uint8 * 64)]
+
+
 _lib.mlf_last_error.restype = C.c_char_p
 _lib.mlf_plan.argtypes = [C.POINTER(MlfNet), C.POINTER(MlfBatch), C.POINTER(MlfPlanParams), C.POINTER(MlfPlanOut)]
 _lib.mlf_init.argtypes = [C.POINTER(MlfConfig), C.c_int64, C.POINTER(_p)]
@@ -102,6 +107,8 @@ _lib.mlf_destroy.restype = None
 _lib.mlf_ipc_export.argtypes = [C.c_int32, _p, C.POINTER(MlfIpcHandle)]
 _lib.mlf_ipc_open.argtypes = [C.c_int32, C.POINTER(MlfIpcHandle), C.POINTER(_p)]
 _lib.mlf_ipc_close.argtypes = [C.c_int32, _p, C.c_int64]
+_lib.mlf_phase_event_export.argtypes = [_p, C.POINTER(MlfIpcEvent)]
+_lib.mlf_phase_events_open.argtypes = [_p, C.c_int32, C.POINTER(MlfIpcEvent)]
 _lib.mlf_synth_fill.argtypes = [C.c_int32, _p, C.c_int64, C.c_int64, C.c_int32, C.c_uint64, C.c_int32,
                                 C.c_int64, C.c_int64, C.c_int32, _p]
 _lib.mlf_copy_kernel.argtypes = [C.c_int32, _p, _p, C.c_int64, _p]
@@ -308,6 +315,17 @@ class Context:
         d = dst if isinstance(dst, int) else dst.data_ptr()
         _check(_lib.mlf_pull_model(self._h, d, int(dst_is_host), C.byref(v)))
         return v.value
+
+    def phase_event(self) -> bytes:
+        e = MlfIpcEvent()
+        _check(_lib.mlf_phase_event_export(self._h, C.byref(e)))
+        return bytes(e.handle)
+
+    def open_phase_events(self, blobs):
+        arr = (MlfIpcEvent * max(len(blobs), 1))()
+        for i, b in enumerate(blobs):
+            C.memmove(arr[i].handle, b, 64)
+        _check(_lib.mlf_phase_events_open(self._h, len(blobs), arr))
 
     def stats(self):
         a, b, c = C.c_int64(), C.c_int64(), C.c_int64()

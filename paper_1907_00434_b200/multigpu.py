@@ -1,0 +1,341 @@
+"""Multi-GPU execution: one process per GPU, the model split into PS shards (App. B.2).
+
+PAPER.md App. B.2: the model is split across a set S of servers,
+every update has one component per server, all components share the update's
+version and deadline and are reserved together.  On one 8xB200 box the servers
+are the GPUs: rank j owns the contiguous shard j of w, and the plan (identical
+on every rank: mlf_plan is deterministic) is executed by every rank on its own
+slice.  The exchange step is the plan's tree edges:
+
+* fold mode (agg_slots = 0): each shard's fused_commit kernel reads its slice of
+  every committed update straight from the update's home GPU (NVLink peer loads
+  through IPC-mapped pointers), folds groups in registers and applies them in
+  commit order: a plan-driven reduce-scatter fused with the apply, one kernel.
+* tree mode: groups are first summed on their aggregator's GPU (tree_reduce over
+  peer members, fp32 aggregate in scratch), then every shard reads its slice of
+  the aggregate — the paper's member -> aggregator -> server path.
+The replica mirror of shard j is stored by rank j's commit kernel straight into
+rank (j+1) mod G's memory (NVLink remote stores).
+
+Host plumbing only: torch.distributed (gloo control group) exchanges IPC handles
+and provides barriers; every byte of the data path moves inside libmlfabric's
+kernels.
+"""
+from __future__ import annotations
+
+import json
+import os
+import time
+
+import torch
+import torch.distributed as dist
+
+from synthgen import configs as cfgs
+
+from . import mlfabric as m
+from .harness import Workload, committed_bytes
+
+
+def init_dist():
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    if not dist.is_initialized():
+        # NCCL when every rank has its own GPU; ranks sharing a device (tests) use gloo only
+        use_nccl = torch.cuda.is_available() and torch.cuda.device_count() >= world
+        dist.init_process_group(backend="nccl" if use_nccl else "gloo")
+    ctrl = dist.new_group(backend="gloo")
+    return rank, world, local, ctrl
+
+
+def agg_slots_needed(cfg: dict, world: int) -> int:
+    counts = [0] * world
+    for a in cfg["aggs"]:
+        counts[cfg["node_rank"][a]] += 1
+    return max(counts) if counts else 0
+
+
+class IpcMapper:
+    """Opens every distinct peer allocation once (cudaIpcOpenMemHandle)."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.opened = {}
+
+    def open(self, blob: bytes) -> int:
+        h = blob[:64]
+        off = int.from_bytes(blob[64:72], "little", signed=True)
+        if h not in self.opened:
+            self.opened[h] = m.ipc_open(self.device, h + bytes(8))
+        return self.opened[h] + off
+
+    def close(self):
+        for h, p in self.opened.items():
+            m.ipc_close(self.device, p, h + bytes(8))
+        self.opened = {}
+
+
+class ShardedWorkload:
+    """Rank `rank`'s part of a config sharded over `world` GPUs."""
+
+    def __init__(self, cfg: dict, rank: int, world: int, device: int, ctrl, mode: str = "fold", variant: int = 0):
+        assert cfg["G"] == world, "config shard count must equal the world size"
+        self.cfg, self.rank, self.world, self.ctrl, self.mode = cfg, rank, world, ctrl, mode
+        dev = torch.device("cuda", device)
+        S, W = cfg["S"], cfg["W"]
+        tdt = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
+        e = cfg["e"]
+        local = [w for w in range(W) if cfg["home"][w] == rank]
+        self.slots_all = torch.empty((max(len(local), 1), S), dtype=tdt, device=dev)
+        slot_tensors = {w: self.slots_all[i] for i, w in enumerate(local)}
+        prev = (rank - 1) % world
+        self.mirror = (torch.zeros(cfg["shards"][prev][1], dtype=torch.float32, device=dev)
+                       if cfg["replica"] else None)
+        self.n_slots = agg_slots_needed(cfg, world) if mode == "tree" else 0
+        self.scratch = (torch.empty((self.n_slots, S), dtype=torch.float32, device=dev) if self.n_slots else None)
+        torch.cuda.synchronize(dev)
+        mine = {"rank": rank, "workers": local,
+                "slots": m.ipc_export(device, self.slots_all.data_ptr()),
+                "mirror": m.ipc_export(device, self.mirror.data_ptr()) if self.mirror is not None else None,
+                "scratch": m.ipc_export(device, self.scratch.data_ptr()) if self.scratch is not None else None}
+        allinfo = [None] * world
+        dist.all_gather_object(allinfo, mine, group=ctrl)
+        allinfo.sort(key=lambda d: d["rank"])
+        self.mapper = IpcMapper(device)
+        peer_slots = [None] * W
+        for info in allinfo:
+            r = info["rank"]
+            base = self.slots_all.data_ptr() if r == rank else self.mapper.open(info["slots"])
+            for i, w in enumerate(info["workers"]):
+                peer_slots[w] = base + i * S * e
+        backup_ptr = None
+        if cfg["replica"]:
+            nxt = (rank + 1) % world
+            backup_ptr = self.mirror.data_ptr() if nxt == rank else self.mapper.open(allinfo[nxt]["mirror"])
+        scratch_tab = None
+        if self.n_slots:
+            scratch_tab = []
+            for info in allinfo:
+                base = self.scratch.data_ptr() if info["rank"] == rank else self.mapper.open(info["scratch"])
+                scratch_tab += [base + s * S * 4 for s in range(self.n_slots)]
+        self.wl = Workload(cfg, device=device, rank=rank, world=world, variant=variant, peer_slots=peer_slots,
+                           backup_ptr=backup_ptr, agg_slots=self.n_slots, agg_scratch=scratch_tab,
+                           slot_tensors=slot_tensors)
+        ev = self.wl.ctx.phase_event()
+        evs = [None] * world
+        dist.all_gather_object(evs, (rank, ev), group=ctrl)
+        self.wl.ctx.open_phase_events([b for (r, b) in sorted(evs) if r != rank])
+        self.two_phase = mode == "tree"
+        self.barrier()
+
+    def barrier(self):
+        dist.barrier(group=self.ctrl)
+
+    def fill(self, iteration: int):
+        self.wl.fill_updates(iteration)
+        torch.cuda.current_stream().synchronize()
+        self.barrier()
+
+    def step(self, iteration: int, flush=None):
+        """One batch on every rank.  Returns (plan dict, this rank's device ms)."""
+        wl = self.wl
+        draws = wl.submit_all(iteration)
+        pb = wl.plan(iteration)
+        pd = pb.to_dict(self.cfg["W"])
+        if flush is not None:
+            flush()
+        torch.cuda.current_stream().synchronize()
+        self.barrier()                          # every rank's slots are final
+        if self.two_phase:
+            wl.ctx.execute(pb, m.MLF_PHASE_AGGREGATE)
+            self.barrier()                      # every phase-1 record enqueued (overlaps GPU work)
+            wl.ctx.execute(pb, m.MLF_PHASE_COMMIT)
+        else:
+            wl.ctx.execute(pb)
+        ms = wl.ctx.sync()
+        wl.after_commit(pd, draws)
+        self.barrier()                          # nobody reads a slot any more
+        return pd, ms
+
+    def close(self):
+        self.wl.ctx.close()
+        self.barrier()
+        self.mapper.close()
+
+
+def max_over_ranks(x: float, ctrl) -> float:
+    t = torch.tensor([x], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=ctrl)
+    return float(t.item())
+
+
+def plan_traffic(cfg: dict, pd: dict, mode: str) -> dict:
+    """Algorithmic bytes per device of one executed plan.
+
+    Returns per-rank lists: hbm (bytes read+written in local HBM), nv_in, nv_out.
+    """
+    G, S, e = cfg["G"], cfg["S"], cfg["e"]
+    home, nr = cfg["home"], cfg["node_rank"]
+    sl = [n for (_, n) in cfg["shards"]]
+    hbm, nin, nout = [0] * G, [0] * G, [0] * G
+    order = pd["order"]
+    for ci, (f, k) in enumerate(zip(pd["commit_first"], pd["commit_count"])):
+        gid = pd["group"][order[f]]
+        if mode == "tree" and gid > 0:
+            a = nr[pd["group_node"][gid - 1]]
+            for p in range(f, f + k):
+                h = home[order[p]]
+                hbm[h] += S * e
+                if h != a:
+                    nout[h] += S * e
+                    nin[a] += S * e
+            hbm[a] += S * 4                       # aggregate written once
+            for j in range(G):
+                hbm[a] += sl[j] * 4               # each shard's slice read from the aggregator's HBM
+                if a != j:
+                    nout[a] += sl[j] * 4
+                    nin[j] += sl[j] * 4
+            continue
+        for p in range(f, f + k):
+            h = home[order[p]]
+            for j in range(G):
+                hbm[h] += sl[j] * e
+                if h != j:
+                    nout[h] += sl[j] * e
+                    nin[j] += sl[j] * e
+    for j in range(G):
+        hbm[j] += 2 * sl[j] * 4                   # w read + write
+        if pd["replica_boundary_commit"] >= 0:
+            t = (j + 1) % G
+            hbm[t] += sl[j] * 4
+            if t != j:
+                nout[j] += sl[j] * 4
+                nin[t] += sl[j] * 4
+    return {"hbm": hbm, "nv_in": nin, "nv_out": nout}
+
+
+def measure_nvlink(device: int, rank: int, world: int, ctrl, nbytes: int = 1 << 30) -> float:
+    """Per-GPU NVLink ingress (GB/s): every rank pulls nbytes from its right neighbour with
+    the library's copy kernel (SM peer loads), all at once; the min over ranks."""
+    dev = torch.device("cuda", device)
+    src = torch.ones(nbytes // 4, dtype=torch.float32, device=dev)
+    dst = torch.empty_like(src)
+    torch.cuda.synchronize(dev)
+    blobs = [None] * world
+    dist.all_gather_object(blobs, (rank, m.ipc_export(device, src.data_ptr())), group=ctrl)
+    blobs = dict(blobs)
+    mp = IpcMapper(device)
+    peer = mp.open(blobs[(rank + 1) % world])
+    best = 0.0
+    for _ in range(4):
+        dist.barrier(group=ctrl)
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        m.copy_kernel(device, dst.data_ptr(), peer, nbytes, torch.cuda.current_stream().cuda_stream)
+        s1.record()
+        s1.synchronize()
+        ms = max_over_ranks(s0.elapsed_time(s1), ctrl)
+        best = max(best, nbytes / (ms / 1e3) / 1e9)
+    dist.barrier(group=ctrl)
+    mp.close()
+    del src, dst
+    return best
+
+
+def run_bench_multi(a):
+    """bench.py at N > 1: config 3 (64 workers, VGG-19-sized updates) over N PS shards."""
+    from bench import Clocks, cpu_baseline_oracle, hbm_peak  # noqa: F401  (same process)
+
+    rank, world, local, ctrl = init_dist()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    cid = a.config or 3
+    os.environ["MLF_COMMIT_IMPL"] = a.kernel
+    peak_hbm, peak_src = hbm_peak()
+    b_nv = measure_nvlink(local, rank, world, ctrl)
+    flush_w = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush_r = torch.ones(64 << 20, dtype=torch.float32, device=dev)
+
+    def l2_flush():
+        flush_w.zero_()
+        flush_r.sum()
+
+    def run(mode, steps, warmup, clocks=False):
+        cfg = cfgs.config(cid, G=world, tau=a.tau, dtype=a.dtype)
+        sw = ShardedWorkload(cfg, rank, world, local, ctrl, mode=mode)
+        sw.fill(0)
+        ck = Clocks(local)
+        recs = []
+        kl0 = 0
+        for s in range(warmup + steps):
+            if s == warmup:
+                kl0 = sw.wl.ctx.stats()[0]
+                if clocks:
+                    ck.__enter__()
+            pd, ms = sw.step(s, flush=l2_flush)
+            ms_max = max_over_ranks(ms, ctrl)
+            if s >= warmup:
+                tr = plan_traffic(cfg, pd, mode)
+                t_roof = max(max(tr["hbm"][j] / (peak_hbm * 1e9), tr["nv_in"][j] / (b_nv * 1e9),
+                                 tr["nv_out"][j] / (b_nv * 1e9)) for j in range(world))
+                recs.append(dict(ms=ms_max, bytes=committed_bytes(cfg, pd), t_roof=t_roof, tr=tr,
+                                 commits=pd["n_commit"], groups=pd["n_groups"]))
+        if clocks:
+            ck.__exit__()
+        kl = sw.wl.ctx.stats()[0] - kl0
+        sw.close()
+        return cfg, recs, ck, kl
+
+    torch.cuda.synchronize()
+    dist.barrier(group=ctrl)
+    modes = ["fold", "tree"] if not a.no_variants else ["fold"]
+    results = {}
+    for i, mode in enumerate(modes):
+        results[mode] = run(mode, a.steps if i == 0 else max(3, a.steps // 2), a.warmup if i == 0 else 2,
+                            clocks=(i == 0))
+    torch.cuda.synchronize()
+    dist.barrier(group=ctrl)
+    if rank != 0:
+        return
+    cfg, recs, ck, kl = results[modes[0]]
+    T = sum(r["ms"] for r in recs) / 1e3
+    value = sum(r["bytes"] for r in recs) / T / 1e9
+    t_roof = sum(r["t_roof"] for r in recs)
+    tr0 = recs[0]["tr"]
+    jmax = max(range(world), key=lambda j: max(tr0["nv_in"][j], tr0["nv_out"][j]))
+    nv_bytes = sum(max(r["tr"]["nv_in"][jmax], r["tr"]["nv_out"][jmax]) for r in recs)
+    hbm_bytes = sum(max(r["tr"]["hbm"]) for r in recs)
+    nv_bound = nv_bytes / b_nv > hbm_bytes / peak_hbm
+    line = {
+        "metric": "aggregated update GB/s committed (device-timed, max over ranks)",
+        "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": round(T * 1e3 / len(recs), 4), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": a.dtype, "data": "synthetic",
+        "config": {"workload": f"config{cid}", "workers": cfg["W"], "update_elems": cfg["S"],
+                   "tau_max": cfg["tau"], "update_dtype": a.dtype, "shards": world, "mode": modes[0],
+                   "committed_per_step": round(sum(r["commits"] for r in recs) / len(recs), 2),
+                   "groups_per_step": round(sum(r["groups"] for r in recs) / len(recs), 2),
+                   "l2": "flushed before every step (256 MiB write + 256 MiB read); operands >> L2",
+                   "parallelism": f"ps-shards{world} (one process per GPU, NVLink peer loads)"},
+        "roofline": {"bound": "nvlink" if nv_bound else "hbm",
+                     "achieved": round((nv_bytes if nv_bound else hbm_bytes) / T / 1e9, 1),
+                     "peak": round(b_nv if nv_bound else peak_hbm, 1), "unit": "GB/s",
+                     "frac": round(t_roof / T, 4), "traffic": None,
+                     "peak_source": ("NVLink ingress measured in this run (copy kernel, peer loads)" if nv_bound
+                                     else peak_src),
+                     "plan_relative_t_roof_ms": round(t_roof * 1e3 / len(recs), 4),
+                     "kernel": f"fused_commit_{a.kernel}"},
+        "nvlink_measured_GBps": round(b_nv, 1),
+        "gpu_launches": int(kl),
+        "clocks": ck.summary(),
+    }
+    if len(modes) > 1:
+        cfg2, recs2, _, _ = results[modes[1]]
+        T2 = sum(r["ms"] for r in recs2) / 1e3
+        line["variants"] = {f"mode_{modes[1]}": {
+            "value": round(sum(r["bytes"] for r in recs2) / T2 / 1e9, 2), "unit": "GB/s",
+            "ms_per_step": round(T2 * 1e3 / len(recs2), 4),
+            "roofline_frac": round(sum(r["t_roof"] for r in recs2) / T2, 4)}}
+    line["e2e"] = {"value": None, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                   "note": "end-to-end host-buffer path is measured at N = 1"}
+    print(json.dumps(line), flush=True)

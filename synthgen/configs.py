@@ -24,11 +24,13 @@ def shard_bounds(S: int, G: int, align: int = 64):
     """Contiguous PS shards (App. B.2), boundaries multiples of `align` elements."""
     per = -(-S // G)
     per = -(-per // align) * align
-    out, b = [], 0
+    out = []
     for j in range(G):
-        e = min(S, b + per)
-        out.append((b, e - b))
-        b = e
+        b = j * per
+        if b >= S:
+            out.append((S - S % align, 0))       # empty trailing shard, aligned begin
+        else:
+            out.append((b, min(S, b + per) - b))
     return out
 
 

@@ -1,0 +1,97 @@
+"""Multi-rank parity check, run under torchrun (one process per rank).
+
+    torchrun --nproc-per-node N tests/multigpu_check.py [--cid 3] [--S 1000003] [--steps 2]
+
+Each rank owns PS shard `rank` (App. B.2); after every batch the shards are
+compared bitwise with the oracle at sampled indices (the oracle plans the same
+batch from the same inputs and applies it with numpy), and the replica mirror
+(stored by rank j into rank (j+1) mod N) is checked where the plan writes it.
+If there are fewer GPUs than ranks, ranks share devices (rank % device_count):
+the path has no kernel that waits on another kernel, so co-resident ranks are safe.
+Prints "MULTIGPU_OK <mode>" on rank 0 when every check passed.
+"""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import synthgen as sg  # noqa: E402
+from oracle.numerics import execute_plan  # noqa: E402
+from oracle.plan import Item, Params, make_net, plan as oracle_plan  # noqa: E402
+from paper_1907_00434_b200.multigpu import ShardedWorkload, init_dist  # noqa: E402
+from synthgen import configs  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cid", type=int, default=3)
+    ap.add_argument("--S", type=int, default=1_000_003)
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--dtype", default="f32")
+    ap.add_argument("--modes", default="fold,tree")
+    ap.add_argument("--kernel", default="ldg")
+    a = ap.parse_args()
+    os.environ["MLF_COMMIT_IMPL"] = a.kernel
+    rank, world, local, ctrl = init_dist()
+    device = local % torch.cuda.device_count()
+    torch.cuda.set_device(device)
+    dt = sg.DTYPE_BF16 if a.dtype == "bf16" else sg.DTYPE_F32
+    for mode in a.modes.split(","):
+        cfg = configs.config(a.cid, G=world, dtype=a.dtype, scale_S=a.S)
+        sw = ShardedWorkload(cfg, rank, world, device, ctrl, mode=mode)
+        b, n = cfg["shards"][rank]
+        rng = np.random.default_rng(rank)
+        idx = np.unique(np.concatenate([rng.integers(b, b + n, 5000), np.arange(b, min(b + 17, b + n)),
+                                        np.arange(max(b, b + n - 17), b + n)]))
+        w_ref = sg.w0_values(cfg["seed"], idx)
+        carried = []
+        v_init = v_prev = 0
+        for it in range(a.steps):
+            sw.fill(it)
+            pd, ms = sw.step(it)
+            # oracle: same planner inputs
+            up, down, site = configs.network(cfg, it)
+            draws = configs.batch_draws(cfg, it, v_init, v_prev)
+            batch = [Item(g, cfg["S"] * cfg["e"], d["version"], d["t_avail"], d["norm"])
+                     for g, d in enumerate(draws)]
+            prm = Params(servers=cfg["servers"], aggs=cfg["aggs"], replicas=cfg["replicas"], raggs=cfg["raggs"],
+                         v_init=v_init, tau_max=cfg["tau"], div_max=cfg["div_max"],
+                         carried=[Item(c["node"], c["size"], 0, 0, c["norm"]) for c in carried],
+                         shard_weights=[x for (_, x) in cfg["shards"]])
+            op = oracle_plan(make_net(cfg["n_nodes"], up, down, None, site), batch, prm)
+            assert op == pd, f"rank {rank}: plan mismatch"
+            w_ref, backup_ref, _ = execute_plan(
+                w_ref, op, lambda g: sg.update_values(cfg["seed"], g, it, idx, dt), cfg["lr"])
+            got = sw.wl.w.cpu().numpy()[idx - b]
+            assert np.array_equal(got.view(np.uint32), w_ref.view(np.uint32)), f"rank {rank} {mode}: w mismatch"
+            torch.cuda.synchronize()
+            dist.barrier(group=ctrl)
+            if op["replica_boundary_commit"] >= 0:
+                # rank (rank+1) % world holds our mirror: gather it through the control group
+                mirrors = [None] * world
+                dist.all_gather_object(mirrors, (rank, sw.mirror.cpu().numpy() if sw.mirror is not None else None),
+                                       group=ctrl)
+                mine = dict(mirrors)[(rank + 1) % world]
+                assert np.array_equal(mine[idx - b].view(np.uint32), backup_ref.view(np.uint32)), \
+                    f"rank {rank} {mode}: mirror mismatch"
+            if cfg["replica"]:
+                items = list(carried) + [dict(node=g, size=cfg["S"] * cfg["e"], norm=draws[g]["norm"])
+                                         for g in op["order"]]
+                carried = [items[i] for i in op["punted"]]
+            v_prev, v_init = v_init, v_init + op["n_commit"]
+        sw.close()
+        if rank == 0:
+            print(f"MULTIGPU_OK {mode} cid={a.cid} world={world} S={cfg['S']} commits={op['n_commit']} "
+                  f"groups={op['n_groups']} boundary={op['replica_boundary_commit']}", flush=True)
+    dist.barrier(group=ctrl)
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

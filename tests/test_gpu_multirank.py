@@ -1,0 +1,37 @@
+"""The sharded (N > 1) path through the C ABI: 2 ranks (one process each; sharing cuda:0 when
+the box has one GPU), IPC peer mappings, fold and tree modes, remote mirror stores —
+bitwise against the oracle at sampled indices (tests/multigpu_check.py)."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _run(nproc, *args, timeout=600):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", "--nnodes=1",
+           f"--nproc-per-node={nproc}", os.path.join(HERE, "multigpu_check.py"), *args]
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", OMP_NUM_THREADS="1")
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, env=env)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    return r.stdout
+
+
+@pytest.mark.parametrize("cid,extra", [(3, []), (4, ["--steps", "3"]), (5, ["--S", "300007"]),
+                                        (3, ["--dtype", "bf16", "--kernel", "bulk"])])
+def test_two_ranks_bitwise(cid, extra):
+    out = _run(2, "--cid", str(cid), *extra)
+    assert "MULTIGPU_OK fold" in out and "MULTIGPU_OK tree" in out
+
+
+def test_all_gpus_if_several():
+    n = torch.cuda.device_count()
+    if n < 4:
+        pytest.skip("needs >= 4 GPUs")
+    out = _run(4, "--cid", "5", "--S", "2000011")
+    assert "MULTIGPU_OK fold" in out and "MULTIGPU_OK tree" in out
