@@ -104,6 +104,15 @@ extern "C" mlf_status mlf_init(const mlf_config *cfg, int64_t v0, mlf_ctx **out)
     if (k.shard_elems > 0 && !k.model_shard) throw Fail{MLF_E_INVALID, "model shard"};
     if (k.agg_slots < 0 || (k.agg_slots > 0 && !k.agg_scratch)) throw Fail{MLF_E_INVALID, "aggregate scratch"};
     if (k.n_nodes < k.n_workers) throw Fail{MLF_E_INVALID, "n_nodes < n_workers"};
+    // the kernels move 128-bit vectors: every buffer must be 16-byte aligned
+    auto misaligned = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) != 0; };
+    if (misaligned(k.model_shard) || misaligned(k.backup_shard))
+      throw Fail{MLF_E_INVALID, "model/backup shard not 16-byte aligned"};
+    for (int w = 0; w < k.n_workers; ++w)
+      if (misaligned(k.update_slot[w])) throw Fail{MLF_E_INVALID, "update slot not 16-byte aligned"};
+    for (int i = 0; i < k.world * k.agg_slots; ++i)
+      if (!k.agg_scratch[i] || misaligned(k.agg_scratch[i]))
+        throw Fail{MLF_E_INVALID, "aggregate scratch null or not 16-byte aligned"};
     auto c = new mlf_ctx();
     c->cfg = k;
     c->version = v0;

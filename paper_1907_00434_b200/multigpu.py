@@ -86,13 +86,15 @@ class ShardedWorkload:
         tdt = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
         e = cfg["e"]
         local = [w for w in range(W) if cfg["home"][w] == rank]
-        self.slots_all = torch.empty((max(len(local), 1), S), dtype=tdt, device=dev)
-        slot_tensors = {w: self.slots_all[i] for i, w in enumerate(local)}
+        self.row = -(-S // 64) * 64               # 256-byte aligned rows (128-bit loads)
+        self.slots_all = torch.empty((max(len(local), 1), self.row), dtype=tdt, device=dev)
+        slot_tensors = {w: self.slots_all[i, :S] for i, w in enumerate(local)}
         prev = (rank - 1) % world
         self.mirror = (torch.zeros(cfg["shards"][prev][1], dtype=torch.float32, device=dev)
                        if cfg["replica"] else None)
         self.n_slots = agg_slots_needed(cfg, world) if mode == "tree" else 0
-        self.scratch = (torch.empty((self.n_slots, S), dtype=torch.float32, device=dev) if self.n_slots else None)
+        self.scratch = (torch.empty((self.n_slots, self.row), dtype=torch.float32, device=dev)
+                        if self.n_slots else None)
         torch.cuda.synchronize(dev)
         mine = {"rank": rank, "workers": local,
                 "slots": m.ipc_export(device, self.slots_all.data_ptr()),
@@ -107,7 +109,7 @@ class ShardedWorkload:
             r = info["rank"]
             base = self.slots_all.data_ptr() if r == rank else self.mapper.open(info["slots"])
             for i, w in enumerate(info["workers"]):
-                peer_slots[w] = base + i * S * e
+                peer_slots[w] = base + i * self.row * e
         backup_ptr = None
         if cfg["replica"]:
             nxt = (rank + 1) % world
@@ -117,7 +119,7 @@ class ShardedWorkload:
             scratch_tab = []
             for info in allinfo:
                 base = self.scratch.data_ptr() if info["rank"] == rank else self.mapper.open(info["scratch"])
-                scratch_tab += [base + s * S * 4 for s in range(self.n_slots)]
+                scratch_tab += [base + s * self.row * 4 for s in range(self.n_slots)]
         self.wl = Workload(cfg, device=device, rank=rank, world=world, variant=variant, peer_slots=peer_slots,
                            backup_ptr=backup_ptr, agg_slots=self.n_slots, agg_scratch=scratch_tab,
                            slot_tensors=slot_tensors)
