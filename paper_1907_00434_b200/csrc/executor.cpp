@@ -579,3 +579,11 @@ extern "C" mlf_status mlf_copy_kernel(int32_t device, void *dst, const void *src
     CK(launch_copy(dst, src, bytes, static_cast<cudaStream_t>(stream), sm));
   });
 }
+
+extern "C" mlf_status mlf_copy_engine(int32_t device, void *dst, const void *src, int64_t bytes, void *stream) {
+  return guard([&] {
+    if (bytes < 0 || (!dst && bytes) || (!src && bytes)) throw Fail{MLF_E_INVALID, "copy arguments"};
+    CK(cudaSetDevice(device));
+    CK(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream)));
+  });
+}

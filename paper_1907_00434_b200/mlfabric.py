@@ -24,7 +24,7 @@ EXPORTS = (
     "mlf_plan", "mlf_init", "mlf_submit_update", "mlf_set_update_host", "mlf_batch_view", "mlf_version",
     "mlf_execute", "mlf_execute_phase", "mlf_sync", "mlf_pull_model", "mlf_stats", "mlf_destroy",
     "mlf_last_error", "mlf_ipc_export", "mlf_ipc_open", "mlf_ipc_close", "mlf_phase_event_export",
-    "mlf_phase_events_open", "mlf_synth_fill", "mlf_copy_kernel",
+    "mlf_phase_events_open", "mlf_synth_fill", "mlf_copy_kernel", "mlf_copy_engine",
 )
 
 
@@ -112,6 +112,7 @@ _lib.mlf_phase_events_open.argtypes = [_p, C.c_int32, C.POINTER(MlfIpcEvent)]
 _lib.mlf_synth_fill.argtypes = [C.c_int32, _p, C.c_int64, C.c_int64, C.c_int32, C.c_uint64, C.c_int32,
                                 C.c_int64, C.c_int64, C.c_int32, _p]
 _lib.mlf_copy_kernel.argtypes = [C.c_int32, _p, _p, C.c_int64, _p]
+_lib.mlf_copy_engine.argtypes = [C.c_int32, _p, _p, C.c_int64, _p]
 
 
 def lib():
@@ -387,3 +388,7 @@ def synth_fill(device: int, dst_ptr: int, n: int, *, elem_offset: int = 0, dtype
 
 def copy_kernel(device: int, dst_ptr: int, src_ptr: int, nbytes: int, stream=None):
     _check(_lib.mlf_copy_kernel(device, dst_ptr, src_ptr, int(nbytes), stream))
+
+
+def copy_engine(device: int, dst_ptr: int, src_ptr: int, nbytes: int, stream=None):
+    _check(_lib.mlf_copy_engine(device, dst_ptr, src_ptr, int(nbytes), stream))
