@@ -53,7 +53,8 @@ def parse():
     ap.add_argument("--no-variants", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--kernel", default=os.environ.get("MLF_COMMIT_IMPL", "ldg"), choices=["ldg", "bulk"])
+    ap.add_argument("--kernel", default=os.environ.get("MLF_COMMIT_IMPL"), choices=["ldg", "bulk"],
+                    help="fused commit kernel (default: ldg on 1 GPU, bulk when operands cross NVLink)")
     return ap.parse_args()
 
 
@@ -364,7 +365,10 @@ def main():
         run_reference(a)
         return
     rank, world, local = dist_env()
-    if world > 1 or a.gpus > 1:
+    multi = world > 1 or a.gpus > 1
+    if a.kernel is None:
+        a.kernel = "bulk" if multi else "ldg"
+    if multi:
         from paper_1907_00434_b200.multigpu import run_bench_multi
         run_bench_multi(a)
         return

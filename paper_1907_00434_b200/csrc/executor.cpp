@@ -143,8 +143,12 @@ extern "C" mlf_status mlf_init(const mlf_config *cfg, int64_t v0, mlf_ctx **out)
     c->in_batch.assign(k.n_workers, 0);
     c->in_flight.assign(k.n_workers, 0);
     c->host_src.assign(k.n_workers, nullptr);
+    // default kernel: LDG streaming on one GPU (HBM-bound, measured best), TMA bulk copies when
+    // operands cross NVLink (8 KB peer transfers beat 16 B peer loads); MLF_COMMIT_IMPL overrides
+    c->impl = k.world > 1 ? CommitImpl::kBulk : CommitImpl::kLdg;
     const char *impl = getenv("MLF_COMMIT_IMPL");
     if (impl && std::string(impl) == "bulk") c->impl = CommitImpl::kBulk;
+    if (impl && std::string(impl) == "ldg") c->impl = CommitImpl::kLdg;
     try {
       CK(cudaSetDevice(k.device));
       CK(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, k.device));

@@ -251,6 +251,47 @@ def measure_nvlink(device: int, rank: int, world: int, ctrl, nbytes: int = 1 << 
     return out
 
 
+def e2e_multi(cfg: dict, rank: int, world: int, local: int, ctrl, steps: int) -> dict:
+    """The metric end to end through the public API on every rank: committed updates of the
+    workers homed on a rank move from pinned host memory (phase 1, H2D), the sharded commit
+    runs (phase 2), and every rank pulls its shard to pinned host memory (D2H).  Wall time
+    per batch, max over ranks.  One pinned source buffer per rank is registered for all of
+    its workers (host RAM bound; the bytes moved are the same)."""
+    import time as _t
+
+    sw = ShardedWorkload(cfg, rank, world, local, ctrl, mode="fold")
+    sw.fill(0)
+    host = sw.slots_all[0].cpu().pin_memory()
+    for w in sw.wl.slots:
+        sw.wl.ctx.set_update_host(w, host.data_ptr())
+    sw.two_phase = True                      # host staging: peers read after every rank's H2D
+    pulled = torch.empty(max(sw.wl.shard_elems, 1), dtype=torch.float32).pin_memory()
+    dst = pulled.data_ptr() - sw.wl.shard_begin * 4
+    tot_b, tot_s = 0, 0.0
+    st0 = None
+    for s in range(2 + steps):
+        if s == 2:
+            st0 = sw.wl.ctx.stats()
+        sw.barrier()
+        t0 = _t.perf_counter()
+        pd, _ = sw.step(s)
+        sw.wl.ctx.pull(dst, True)
+        dt = max_over_ranks(_t.perf_counter() - t0, ctrl)
+        if s >= 2:
+            tot_b += committed_bytes(cfg, pd)
+            tot_s += dt
+    st1 = sw.wl.ctx.stats()
+    h2d = torch.tensor([float(st1[1] - st0[1])], dtype=torch.float64)
+    d2h = torch.tensor([float(st1[2] - st0[2])], dtype=torch.float64)
+    dist.all_reduce(h2d, group=ctrl)
+    dist.all_reduce(d2h, group=ctrl)
+    sw.close()
+    return {"value": round(tot_b / tot_s / 1e9, 3), "unit": "GB/s",
+            "h2d_bytes_per_step": int(h2d.item() / steps), "d2h_bytes_per_step": int(d2h.item() / steps),
+            "includes": "submit + plan (host, every rank) + H2D of committed updates on their home GPU + "
+                        "sharded commit over NVLink + D2H pull of every shard; wall time, max over ranks"}
+
+
 def run_bench_multi(a):
     """bench.py at N > 1: config 3 (64 workers, VGG-19-sized updates) over N PS shards."""
     from bench import Clocks, cpu_baseline_oracle, hbm_peak  # noqa: F401  (same process)
@@ -305,6 +346,10 @@ def run_bench_multi(a):
     for i, mode in enumerate(modes):
         results[mode] = run(mode, a.steps if i == 0 else max(3, a.steps // 2), a.warmup if i == 0 else 2,
                             clocks=(i == 0))
+    e2e = None
+    if not a.no_e2e:
+        e2e = e2e_multi(cfgs.config(cid, G=world, tau=a.tau, dtype=a.dtype), rank, world, local, ctrl,
+                        max(3, a.steps // 4))
     torch.cuda.synchronize()
     dist.barrier(group=ctrl)
     if rank != 0:
@@ -348,6 +393,6 @@ def run_bench_multi(a):
             "value": round(sum(r["bytes"] for r in recs2) / T2 / 1e9, 2), "unit": "GB/s",
             "ms_per_step": round(T2 * 1e3 / len(recs2), 4),
             "roofline_frac": round(sum(r["t_roof"] for r in recs2) / T2, 4)}}
-    line["e2e"] = {"value": None, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
-                   "note": "end-to-end host-buffer path is measured at N = 1"}
+    if e2e is not None:
+        line["e2e"] = e2e
     print(json.dumps(line), flush=True)
