@@ -1,0 +1,14 @@
+#!/bin/bash
+# Multi-GPU evidence on one box: parity check, then bench at N = 2, 4, 8 (config 3) and config 5 at N = 8.
+OUT=${OUT:-gpurun_out}
+NG=$(nvidia-smi -L | wc -l)
+timeout 300 python -m torch.distributed.run --standalone --nproc-per-node $NG tests/multigpu_check.py --cid 5 --S 4000037 > $OUT/check_n$NG.log 2>&1; echo rc=$? >> $OUT/check_n$NG.log
+for N in 2 4 8; do
+  [ $N -le $NG ] || continue
+  timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 2953$N \
+     bench.py --gpus $N --steps 10 --warmup 3 > $OUT/bench_n$N.log 2>&1; echo rc=$? >> $OUT/bench_n$N.log
+done
+if [ $NG -ge 8 ]; then
+  timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 8 --master-addr 127.0.0.1 --master-port 29599 \
+     bench.py --gpus 8 --config 5 --steps 6 --warmup 2 --no-e2e > $OUT/bench_n8_cfg5.log 2>&1; echo rc=$? >> $OUT/bench_n8_cfg5.log
+fi
