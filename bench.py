@@ -138,7 +138,8 @@ def run_reference(a):
         draws = configs.batch_draws(cfg, it, v_init, v_prev)
         ops = {g: sg.update_values(cfg["seed"], g, it, idx, dt) for g in range(cfg["W"])}
         t0 = time.perf_counter()
-        batch = [Item(g, cfg["S"] * cfg["e"], d["version"], d["t_avail"], d["norm"]) for g, d in enumerate(draws)]
+        batch = [Item(cfg["worker_node"][g], cfg["S"] * cfg["e"], d["version"], d["t_avail"], d["norm"])
+                 for g, d in enumerate(draws)]
         weights = [n for (_, n) in cfg["shards"]] if cfg["G"] > 1 else None
         p = oracle_plan(make_net(cfg["n_nodes"], up, down, None, site), batch,
                         Params(servers=cfg["servers"], aggs=cfg["aggs"], v_init=v_init, tau_max=cfg["tau"],
@@ -184,7 +185,8 @@ def cpu_baseline_oracle(cfg, dt, budget_s=15.0):
         draws = configs.batch_draws(cfg, it, v_init, v_prev)
         ops = {g: sg.update_values(cfg["seed"], g, it, idx, dt) for g in range(cfg["W"])}
         t0 = time.perf_counter()
-        batch = [Item(g, cfg["S"] * cfg["e"], d["version"], d["t_avail"], d["norm"]) for g, d in enumerate(draws)]
+        batch = [Item(cfg["worker_node"][g], cfg["S"] * cfg["e"], d["version"], d["t_avail"], d["norm"])
+                 for g, d in enumerate(draws)]
         p = oracle_plan(make_net(cfg["n_nodes"], up, down, None, site), batch,
                         Params(servers=cfg["servers"], aggs=cfg["aggs"], v_init=v_init, tau_max=cfg["tau"]))
         w, _, _ = execute_plan(w, p, lambda g: ops[g], cfg["lr"])

@@ -30,8 +30,11 @@
  *   - All device memory is allocated by the caller (PyTorch) and borrowed for
  *     the lifetime of the context.  Host arrays passed in are borrowed only for
  *     the duration of the call.
- *   - Planner node ids: the caller numbers the network's nodes; by convention
- *     virtual worker w of a context is node w (mlf_batch_view reports node = w).
+ *   - Planner node ids: the caller numbers the network's nodes; a context maps
+ *     worker w to node worker_node[w] (default w) in mlf_batch_view.  On one
+ *     B200 box the nodes are the GPUs: the virtual workers multiplexed on a GPU
+ *     share its NVLink egress, exactly as the paper's co-located workers share a
+ *     host NIC.
  *
  * Readings of silent or ambiguous passages (R1-R20) are listed in DESIGN.md §3.
  */
@@ -163,8 +166,10 @@ typedef struct {
   void *const *update_slot;    /* [n_workers] full-length update vectors (S elements), each a
                                   device pointer valid on `device` (local or mapped peer) */
   const int32_t *worker_rank;  /* [n_workers] home rank of each worker, or NULL (all local) */
-  int32_t n_nodes;             /* planner nodes known to the executor (>= n_workers) */
+  int32_t n_nodes;             /* planner nodes known to the executor */
   const int32_t *node_rank;    /* [n_nodes] rank hosting each node (aggregators), or NULL (all 0) */
+  const int32_t *worker_node;  /* [n_workers] planner node of each worker (the machine/GPU whose NIC
+                                  its pushes use), or NULL: worker w is node w */
   int32_t agg_slots;           /* fp32 aggregate buffers per rank for cross-GPU groups (0 = fold groups
                                   inside the commit kernel, no materialised aggregates) */
   float *const *agg_scratch;   /* [world*agg_slots] S-element fp32 buffers valid on `device` */
@@ -192,7 +197,7 @@ mlf_status mlf_submit_update(mlf_ctx *ctx, int32_t worker, int64_t version,
 mlf_status mlf_set_update_host(mlf_ctx *ctx, int32_t worker, const void *host_ptr);
 
 /* Borrow the current batch as planner input (arrays valid until the next
- * submit/execute).  bytes = model_elems * sizeof(dtype), node = worker. */
+ * submit/execute).  bytes = model_elems * sizeof(dtype), node = worker_node[worker]. */
 mlf_status mlf_batch_view(mlf_ctx *ctx, mlf_batch *out);
 
 /* Current model version v_init. */

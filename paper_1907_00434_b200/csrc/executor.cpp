@@ -64,7 +64,7 @@ mlf_status guard(F &&f) {
 struct mlf_ctx {
   mlf_config cfg{};
   std::vector<void *> slot;
-  std::vector<int32_t> worker_rank, node_rank;
+  std::vector<int32_t> worker_rank, node_rank, worker_node;
   std::vector<float *> agg_scratch;
   int sm_count = 148;
   int64_t version = 0;
@@ -103,7 +103,11 @@ extern "C" mlf_status mlf_init(const mlf_config *cfg, int64_t v0, mlf_ctx **out)
     if (k.update_dtype != MLF_F32 && k.update_dtype != MLF_BF16) throw Fail{MLF_E_INVALID, "update dtype"};
     if (k.shard_elems > 0 && !k.model_shard) throw Fail{MLF_E_INVALID, "model shard"};
     if (k.agg_slots < 0 || (k.agg_slots > 0 && !k.agg_scratch)) throw Fail{MLF_E_INVALID, "aggregate scratch"};
-    if (k.n_nodes < k.n_workers) throw Fail{MLF_E_INVALID, "n_nodes < n_workers"};
+    if (k.n_nodes < 1) throw Fail{MLF_E_INVALID, "n_nodes < 1"};
+    for (int w = 0; w < k.n_workers; ++w) {
+      int nd = k.worker_node ? k.worker_node[w] : w;
+      if (nd < 0 || nd >= k.n_nodes) throw Fail{MLF_E_INVALID, "worker_node out of range"};
+    }
     // the kernels move 128-bit vectors: every buffer must be 16-byte aligned
     auto misaligned = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) != 0; };
     if (misaligned(k.model_shard) || misaligned(k.backup_shard))
@@ -130,6 +134,7 @@ extern "C" mlf_status mlf_init(const mlf_config *cfg, int64_t v0, mlf_ctx **out)
         throw Fail{MLF_E_INVALID, "worker_rank out of range"};
       }
       c->worker_rank.push_back(r);
+      c->worker_node.push_back(k.worker_node ? k.worker_node[w] : w);
     }
     for (int i = 0; i < k.n_nodes; ++i) {
       int r = k.node_rank ? k.node_rank[i] : 0;
@@ -197,7 +202,7 @@ extern "C" mlf_status mlf_submit_update(mlf_ctx *c, int32_t worker, int64_t vers
     c->in_batch[worker] = 1;
     if (index_in_batch) *index_in_batch = (int32_t)c->b_worker.size();
     c->b_worker.push_back(worker);
-    c->b_node.push_back(worker);
+    c->b_node.push_back(c->worker_node[worker]);
     c->b_bytes.push_back(c->cfg.model_elems * (int64_t)c->elem_bytes);
     c->b_version.push_back(version);
     c->b_tavail.push_back(t_avail_ns);

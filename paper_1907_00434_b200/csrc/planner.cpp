@@ -10,19 +10,27 @@
 // Compiled with -ffp-contract=off so the only floating point (the divergence
 // bound) is evaluated exactly in the documented order.
 //
-// Performance: planning is O(#U^2 * G) transfer evaluations.
-// Candidate evaluations never copy the network: a transfer's tentative
-// reservation lives in a small overlay of the <= 3G links it touches.  The
-// #U+1 DetAgg cases are independent ("can be parallelized") and run
-// on a thread pool, reduced in case order so the result equals the sequential
-// argmin with ties to the smallest n (R14).
+// Performance (planning is O(#U^2 * G) transfer evaluations):
+//  * a candidate's tentative reservation is never materialised: evaluations read
+//    the residual as base profile minus a short list of pending reservation
+//    segments (the candidate's earlier components, the look-ahead's g*), with
+//    monotone per-link cursors instead of repeated binary searches;
+//  * the ShrtUp/ShrtDline candidate scans and the #U+1 DetAgg cases ("can be
+//    parallelized") run on a thread pool; results are reduced in
+//    index order, so the plan equals the sequential one bit for bit (ties ->
+//    lowest index, R6/R14);
+//  * DetAgg(n) shares its n-update direct prefix with DetAgg(n-1): each worker
+//    thread extends one prefix state incrementally instead of re-sending it.
 #include "planner.h"
 
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <condition_variable>
 #include <cstring>
+#include <functional>
 #include <limits>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -43,12 +51,91 @@ struct PlanFail {
   std::string msg;
 };
 
+// ---------------------------------------------------------------- thread pool
+// Persistent workers; run(n, f) calls f(i) for i in [0, n) and returns when all
+// are done.  Concurrent callers (mlf_plan is reentrant) fall back to serial.
+class Pool {
+ public:
+  static Pool &get() {
+    static Pool p;
+    return p;
+  }
+  int threads() const { return (int)th_.size() + 1; }
+  void run(int n, const std::function<void(int)> &f, int min_parallel) {
+    if (n < min_parallel || th_.empty() || !busy_.try_lock()) {
+      for (int i = 0; i < n; ++i) f(i);
+      return;
+    }
+    {
+      std::lock_guard<std::mutex> g(m_);
+      job_ = &f;
+      n_ = n;
+      next_.store(0);
+      pending_ = (int)th_.size();
+      ++gen_;
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> g(m_);
+    done_.wait(g, [&] { return pending_ == 0; });
+    job_ = nullptr;
+    busy_.unlock();
+  }
+
+ private:
+  Pool() {
+    unsigned hw = std::thread::hardware_concurrency();
+    int t = (int)std::min<unsigned>(hw ? hw : 1, 32) - 1;
+    for (int i = 0; i < t; ++i) th_.emplace_back([this] { loop(); });
+  }
+  ~Pool() {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto &t : th_) t.join();
+  }
+  void work() {
+    for (;;) {
+      int i = next_.fetch_add(1);
+      if (i >= n_) return;
+      (*job_)(i);
+    }
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> g(m_);
+        cv_.wait(g, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+      }
+      work();
+      {
+        std::lock_guard<std::mutex> g(m_);
+        if (--pending_ == 0) done_.notify_one();
+      }
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex m_, busy_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int)> *job_ = nullptr;
+  int n_ = 0, pending_ = 0;
+  std::atomic<int> next_{0};
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+// ---------------------------------------------------------------- network
 struct Seg {
   i64 t, r;
 };
 using Profile = std::vector<Seg>;
 
-// ---------------------------------------------------------------- network
 struct NetDef {
   int n = 0;
   const int64_t *up = nullptr, *down = nullptr, *bw = nullptr;
@@ -58,7 +145,7 @@ struct NetDef {
 // link keys: up(i) = i, down(j) = n + j, pair(i, j) = 2n + i*n + j
 struct Net {
   const NetDef *def = nullptr;
-  std::vector<Profile> ud;                         // 2n up/down profiles
+  std::vector<Profile> ud;                         // 2n up/down residual profiles
   std::unordered_map<i64, Profile> pair;           // pair links touched so far
 
   explicit Net(const NetDef *d) : def(d), ud(2 * d->n) {
@@ -115,56 +202,27 @@ static bool path_dead(const NetDef &d, int src, int dst) {
   return false;
 }
 
-// A view = base network + overlay of modified profiles (copy-on-write).
-struct View {
-  Net *base;
-  std::vector<std::pair<i64, Profile>> ov;
-  explicit View(Net *b) : base(b) {}
-  const Profile &prof(i64 key) const {
-    for (auto &kv : ov)
-      if (kv.first == key) return kv.second;
-    const Profile *p = base->get(key);
-    if (p) return *p;
-    // untouched pair link: constant capacity
-    static thread_local Profile tmp;
-    tmp.assign(1, Seg{0, std::max<i64>(base->capacity(key), 0)});
-    return tmp;
-  }
-  Profile &mut(i64 key) {
-    for (auto &kv : ov)
-      if (kv.first == key) return kv.second;
-    ov.emplace_back(key, prof(key));
-    return ov.back().second;
-  }
-  void commit() {
-    for (auto &kv : ov) base->mut(kv.first) = std::move(kv.second);
-    ov.clear();
-  }
-};
-
-static inline i64 rate_at(const Profile &p, i64 t) {
-  // last segment with start <= t (profiles start at 0, t >= 0)
-  auto it = std::upper_bound(p.begin(), p.end(), t, [](i64 v, const Seg &s) { return v < s.t; });
-  return (it == p.begin()) ? p.front().r : std::prev(it)->r;
-}
-static inline i64 next_bp(const Profile &p, i64 t) {
-  auto it = std::upper_bound(p.begin(), p.end(), t, [](i64 v, const Seg &s) { return v < s.t; });
-  return it == p.end() ? T_INF : it->t;
-}
-
 struct TSeg {
-  i64 a, b, r;
+  i64 a, b, r;        // rate r used on [a, b)
 };
+struct Res {
+  i64 key;            // link
+  TSeg s;
+};
+using Pending = std::vector<Res>;   // reservations evaluated but not applied to a Net
+
 struct Transfer {
   i64 t_st = 0, t_en = 0;
   Path path;
   std::vector<TSeg> segs;
 };
 
-// O1: water-fill `size` bytes from t_avail along the path residual (Fig. 5(b)).
-// Returns false if the path residual is zero forever after t_avail.
-template <class V>
-static bool transfer(const V &v, const NetDef &d, i64 size, int src, int dst, i64 t_avail, Transfer &out) {
+// O1: water-fill `size` bytes from t_avail along the path residual (Fig. 5(b)),
+// on `net` minus the pending reservations of L0 and L1.  Returns false if the
+// path residual is zero forever after t_avail.
+static bool transfer(const Net &net, const Pending *L0, const Pending *L1, i64 size, int src, int dst, i64 t_avail,
+                     Transfer &out) {
+  const NetDef &d = *net.def;
   out.segs.clear();
   out.path = path_of(d, src, dst);
   if (size == 0 || out.path.nk == 0) {
@@ -172,17 +230,61 @@ static bool transfer(const V &v, const NetDef &d, i64 size, int src, int dst, i6
     out.t_st = out.t_en = t_avail;
     return true;
   }
-  const Profile *pr[3];
-  for (int k = 0; k < out.path.nk; ++k) pr[k] = &v.prof(out.path.key[k]);
+  struct Lk {
+    const Seg *p;
+    int n, idx;
+    Seg own;
+    int s0, s1;       // subs range in `subs`
+  };
+  thread_local std::vector<TSeg> subs;
+  subs.clear();
+  Lk lk[3];
+  const int nk = out.path.nk;
+  for (int k = 0; k < nk; ++k) {
+    const i64 key = out.path.key[k];
+    const Profile *pr = net.get(key);
+    if (pr) {
+      lk[k].p = pr->data();
+      lk[k].n = (int)pr->size();
+    } else {
+      lk[k].own = Seg{0, std::max<i64>(net.capacity(key), 0)};
+      lk[k].p = &lk[k].own;
+      lk[k].n = 1;
+    }
+    // last segment with start <= t_avail
+    const Seg *b = lk[k].p, *e = lk[k].p + lk[k].n;
+    const Seg *it = std::upper_bound(b, e, t_avail, [](i64 v, const Seg &s) { return v < s.t; });
+    lk[k].idx = it == b ? 0 : (int)(it - b) - 1;
+    lk[k].s0 = (int)subs.size();
+    for (const Pending *L : {L0, L1})
+      if (L)
+        for (const Res &r : *L)
+          if (r.key == key && r.s.b > t_avail) subs.push_back(r.s);
+    lk[k].s1 = (int)subs.size();
+  }
   i128 need = (i128)size * NS_PER_S;
   i64 cur = t_avail;
   bool started = false;
   for (;;) {
     i64 r = T_INF, nb = T_INF;
-    for (int k = 0; k < out.path.nk; ++k) {
-      r = std::min(r, rate_at(*pr[k], cur));
-      nb = std::min(nb, next_bp(*pr[k], cur));
+    for (int k = 0; k < nk; ++k) {
+      Lk &L = lk[k];
+      while (L.idx + 1 < L.n && L.p[L.idx + 1].t <= cur) ++L.idx;
+      i64 rk = L.p[L.idx].r;
+      i64 nbk = L.idx + 1 < L.n ? L.p[L.idx + 1].t : T_INF;
+      for (int s = L.s0; s < L.s1; ++s) {
+        const TSeg &q = subs[s];
+        if (q.a <= cur && cur < q.b) {
+          rk -= q.r;
+          nbk = std::min(nbk, q.b);
+        } else if (q.a > cur) {
+          nbk = std::min(nbk, q.a);
+        }
+      }
+      r = std::min(r, rk);
+      nb = std::min(nb, nbk);
     }
+    if (r < 0) throw PlanFail{MLF_E_INVALID, "internal: negative residual"};
     if (r > 0) {
       if (!started) {
         out.t_st = cur;
@@ -204,7 +306,12 @@ static bool transfer(const V &v, const NetDef &d, i64 size, int src, int dst, i6
   }
 }
 
-// O2: NetUp — subtract the transfer's rate profile on every link of its path.
+static void add_pending(Pending &P, const Transfer &tr) {
+  for (int k = 0; k < tr.path.nk; ++k)
+    for (auto &s : tr.segs) P.push_back({tr.path.key[k], s});
+}
+
+// O2: NetUp — subtract reservations from the residual profiles.
 static void split_at(Profile &p, i64 t) {
   auto it = std::lower_bound(p.begin(), p.end(), t, [](const Seg &s, i64 v) { return s.t < v; });
   if (it != p.end() && it->t == t) return;
@@ -214,18 +321,25 @@ static void split_at(Profile &p, i64 t) {
 static void subtract(Profile &p, i64 a, i64 b, i64 r) {
   split_at(p, a);
   split_at(p, b);
-  for (auto &s : p)
-    if (s.t >= a && s.t < b) {
-      s.r -= r;
-      if (s.r < 0) throw PlanFail{MLF_E_INVALID, "internal: residual went negative"};
-    }
-}
-template <class V>
-static void reserve(V &v, const Transfer &tr) {
-  for (int k = 0; k < tr.path.nk; ++k) {
-    Profile &p = v.mut(tr.path.key[k]);
-    for (auto &s : tr.segs) subtract(p, s.a, s.b, s.r);
+  auto lo = std::lower_bound(p.begin(), p.end(), a, [](const Seg &s, i64 v) { return s.t < v; });
+  auto it = lo;
+  for (; it != p.end() && it->t < b; ++it) {
+    it->r -= r;
+    if (it->r < 0) throw PlanFail{MLF_E_INVALID, "internal: residual went negative"};
   }
+  // keep the profile canonical (no two adjacent segments with equal rates) around the edit:
+  // a fully reserved stretch collapses into one zero segment, so later t_en walks skip it in
+  // one step.  The residual function is unchanged, hence so is every t_en.
+  size_t i0 = (size_t)(lo - p.begin());
+  i0 = i0 > 0 ? i0 - 1 : 0;
+  size_t i1 = std::min(p.size(), (size_t)(it - p.begin()) + 1);
+  size_t w = i0 + 1;
+  for (size_t i = i0 + 1; i < i1; ++i)
+    if (p[i].r != p[w - 1].r) p[w++] = p[i];
+  if (w < i1) p.erase(p.begin() + w, p.begin() + i1);
+}
+static void apply_pending(Net &net, const Pending &P) {
+  for (const Res &r : P) subtract(net.mut(r.key), r.s.a, r.s.b, r.s.r);
 }
 
 // App. B.2: component sizes proportional to the shard weights.
@@ -251,19 +365,30 @@ struct Ctx {
 };
 
 // Multi-component transfer: components reserved sequentially in destination
-// order (R11) into view v; t_en = max, t_st = min.  False if unschedulable.
-static bool send(View &v, const Ctx &c, const std::vector<int> &dsts, int src, i64 size, i64 t_avail, Send &out) {
-  std::vector<i64> comp;
+// order (R11) into `local` (pending on top of net - L0); t_en = max, t_st = min.
+static bool send(const Net &net, const Pending *L0, const Ctx &c, const std::vector<int> &dsts, int src, i64 size,
+                 i64 t_avail, Send &out, Pending &local) {
+  thread_local std::vector<i64> comp;
+  thread_local Transfer tr;
   component_bytes(size, c.weights, c.wsum, comp);
-  Transfer tr;
+  local.clear();
   out.t_st = T_INF;
   out.t_en = 0;
   for (size_t j = 0; j < dsts.size(); ++j) {
-    if (!transfer(v, c.d, comp[j], src, dsts[j], t_avail, tr)) return false;
-    reserve(v, tr);
+    if (!transfer(net, L0, &local, comp[j], src, dsts[j], t_avail, tr)) return false;
+    add_pending(local, tr);
     out.t_st = std::min(out.t_st, tr.t_st);
     out.t_en = std::max(out.t_en, tr.t_en);
   }
+  return true;
+}
+
+// send + NetUp on `net`
+static bool send_apply(Net &net, const Ctx &c, const std::vector<int> &dsts, int src, i64 size, i64 t_avail,
+                       Send &out) {
+  thread_local Pending P;
+  if (!send(net, nullptr, c, dsts, src, size, t_avail, out, P)) return false;
+  apply_pending(net, P);
   return true;
 }
 
@@ -279,6 +404,8 @@ struct OrderRes {
   std::vector<uint8_t> reason;
 };
 
+static constexpr int kMinParallelEvals = 24;
+
 static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 tau, i64 v_init) {
   const int n = (int)batch.size();
   std::vector<i64> dl(n);
@@ -289,31 +416,41 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
   res.reason.assign(n, 0);
   Net nw(&c.d);
   i64 p = 1;
+  const int G = (int)c.servers.size();
+  std::vector<i64> ten(n);
+  std::vector<uint8_t> ok(n);
+  std::vector<int> pool;
 
-  // ShrtDline(pos, cands, NW): due set argmin if any, else ShrtUp (R4, R6).
-  auto pick = [&](i64 pos, const std::vector<int> &cands, View &base_view, int &g_out, Send &s_out,
-                  View *view_out) {
+  // ShrtDline(pos, cands, NW + L0): the due set's argmin if any, else ShrtUp (R4, R6).
+  auto pick = [&](i64 pos, const std::vector<int> &cands, const Pending *L0) -> int {
     bool any_due = false;
     for (int g : cands)
       if (dl[g] == pos) {
         any_due = true;
         break;
       }
-    g_out = -1;
-    for (int g : cands) {
-      if (any_due && dl[g] != pos) continue;
-      View v = base_view;                          // copies only the overlay
-      Send s;
-      if (!send(v, c, c.servers, batch[g].node, batch[g].size, batch[g].t_avail, s))
-        throw PlanFail{MLF_E_UNSCHEDULABLE, "update path to a server is down"};
-      if (g_out < 0 || s.t_en < s_out.t_en) {
-        g_out = g;
-        s_out = s;
-        if (view_out) *view_out = std::move(v);
-      }
+    pool.clear();
+    for (int g : cands)
+      if (!any_due || dl[g] == pos) pool.push_back(g);
+    Pool::get().run(
+        (int)pool.size(),
+        [&](int i) {
+          thread_local Pending local;
+          const int g = pool[i];
+          Send s;
+          ok[g] = send(nw, L0, c, c.servers, batch[g].node, batch[g].size, batch[g].t_avail, s, local);
+          ten[g] = s.t_en;
+        },
+        std::max(1, kMinParallelEvals / std::max(1, G)));
+    int best = -1;
+    for (int g : pool) {
+      if (!ok[g]) throw PlanFail{MLF_E_UNSCHEDULABLE, "update path to a server is down"};
+      if (best < 0 || ten[g] < ten[best]) best = g;
     }
+    return best;
   };
 
+  Pending star;
   for (;;) {
     std::vector<int> keep;
     for (int g : unproc) {
@@ -324,20 +461,17 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
     }
     unproc.swap(keep);
     if (unproc.empty()) break;
-    View base(&nw);
-    View star(&nw);
-    int g_star;
+    const int g_star = pick(p, unproc, nullptr);
+    const i64 t_star = ten[g_star];
     Send s_star;
-    pick(p, unproc, base, g_star, s_star, &star);
+    send(nw, nullptr, c, c.servers, batch[g_star].node, batch[g_star].size, batch[g_star].t_avail, s_star, star);
     std::vector<int> cands;
     for (int g : unproc)
       if (g != g_star && dl[g] >= p + 1) cands.push_back(g);
     bool drop = false;
     if (!cands.empty()) {
-      int g_next;
-      Send s_next;
-      pick(p + 1, cands, star, g_next, s_next, nullptr);   // on NetUp(NW, g*)
-      if (s_star.t_en > s_next.t_en) drop = true;          // Alg. 2 line 10
+      const int g_next = pick(p + 1, cands, &star);    // on NetUp(NW, g*)
+      if (t_star > ten[g_next]) drop = true;           // Alg. 2 line 10
     }
     unproc.erase(std::find(unproc.begin(), unproc.end(), g_star));
     if (drop) {
@@ -345,7 +479,7 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
       continue;
     }
     res.order.push_back(g_star);
-    star.commit();
+    apply_pending(nw, star);
     ++p;
   }
   return res;
@@ -363,31 +497,18 @@ struct AggCase {
   std::vector<CommitRec> commits;
 };
 
-// Alg. 3 DetAgg(n) on a copy of `net0` (R10-R12).  If net_out is given, the
-// final network is stored there.
-static AggCase det_agg(int n, const std::vector<Item> &items, const Net &net0, const Ctx &c,
-                       const std::vector<int> &dsts, const std::vector<int> &aggs, Net *net_out) {
-  AggCase cs;
-  cs.n = n;
-  Net nw = net0;
-  i64 t_max = 0;
+// Alg. 3 DetAgg(n), continued from the state after its n direct sends (R10-R12):
+// `nw` holds that network, t_max/commits the direct part.
+static void det_agg_tail(AggCase &cs, Net &nw, i64 t_max, const std::vector<Item> &items, const Ctx &c,
+                         const std::vector<int> &dsts, const std::vector<int> &aggs) {
+  const int n = cs.n;
   bool have = n > 0;
   const int k = (int)aggs.size();
-  for (int i = 0; i < n; ++i) {                               // lines 3-7
-    View v(&nw);
-    Send s;
-    if (!send(v, c, dsts, items[i].node, items[i].size, items[i].t_avail, s)) return cs;
-    v.commit();
-    t_max = std::max(t_max, s.t_en);
-    cs.commits.push_back({i, 1, 0, s});
-  }
   int aid = 1, i = n, gfirst = n, gcount = 0;
   i64 gsize = 0, garr = 0;
   auto flush = [&]() -> bool {                                // lines 11-12
-    View v(&nw);
     Send s;
-    if (!send(v, c, dsts, aggs[aid - 1], gsize, garr, s)) return false;
-    v.commit();
+    if (!send_apply(nw, c, dsts, aggs[aid - 1], gsize, garr, s)) return false;
     t_max = std::max(t_max, s.t_en);
     have = true;
     cs.commits.push_back({gfirst, gcount, aid, s});
@@ -398,36 +519,60 @@ static AggCase det_agg(int n, const std::vector<Item> &items, const Net &net0, c
     garr = 0;
     return true;
   };
-  Transfer tr;
-  View direct(&nw);
+  thread_local Transfer tr;
+  thread_local Pending P;
   while (i < (int)items.size()) {
-    if (aid > k) return cs;
-    if (!transfer(direct, c.d, items[i].size, items[i].node, aggs[aid - 1], items[i].t_avail, tr)) return cs;
+    if (aid > k) return;
+    if (!transfer(nw, nullptr, nullptr, items[i].size, items[i].node, aggs[aid - 1], items[i].t_avail, tr)) return;
     if (have && tr.t_en > t_max) {                            // line 10
-      if (gcount == 0) return cs;
-      if (!flush()) return cs;
+      if (gcount == 0) return;
+      if (!flush()) return;
       continue;
     }
-    reserve(direct, tr);                                      // lines 16-18
-    direct.commit();
+    P.clear();                                                // lines 16-18
+    add_pending(P, tr);
+    apply_pending(nw, P);
     if (gcount == 0) gfirst = i;
     ++gcount;
     gsize = std::max(gsize, items[i].size);
     garr = std::max(garr, tr.t_en);
     ++i;
   }
-  if (gcount > 0 && !flush()) return cs;
+  if (gcount > 0 && !flush()) return;
   cs.feasible = true;
   cs.total = t_max;
-  if (net_out) *net_out = std::move(nw);
-  return cs;
 }
 
-static int n_threads_for(int cases) {
-  unsigned hw = std::thread::hardware_concurrency();
-  int t = (int)std::min<unsigned>(hw ? hw : 1, 16);
-  if (cases < 16) t = 1;
-  return std::max(1, std::min(t, cases));
+// The n-update direct prefix (Alg. 3 lines 3-7) applied to `nw`.
+struct Prefix {
+  Net nw;
+  i64 t_max = 0;
+  std::vector<CommitRec> commits;
+  bool ok = true;
+  explicit Prefix(const Net &n0) : nw(n0) {}
+  void extend(const std::vector<Item> &items, int i, const Ctx &c, const std::vector<int> &dsts) {
+    if (!ok) return;
+    Send s;
+    if (!send_apply(nw, c, dsts, items[i].node, items[i].size, items[i].t_avail, s)) {
+      ok = false;
+      return;
+    }
+    t_max = std::max(t_max, s.t_en);
+    commits.push_back({i, 1, 0, s});
+  }
+};
+
+static AggCase det_agg(int n, const std::vector<Item> &items, const Net &net0, const Ctx &c,
+                       const std::vector<int> &dsts, const std::vector<int> &aggs, Net *net_out) {
+  Prefix pre(net0);
+  for (int i = 0; i < n; ++i) pre.extend(items, i, c, dsts);
+  AggCase cs;
+  cs.n = n;
+  if (!pre.ok) return cs;
+  cs.commits = pre.commits;
+  det_agg_tail(cs, pre.nw, pre.t_max, items, c, dsts, aggs);
+  if (cs.feasible && net_out) *net_out = std::move(pre.nw);
+  return cs;
 }
 
 // Alg. 3 lines 21-24: all |U|+1 cases, argmin total, ties -> smallest n (R14).
@@ -435,30 +580,35 @@ static AggCase plan_aggregation(const std::vector<Item> &items, const Net &net0,
                                 const std::vector<int> &dsts, const std::vector<int> &aggs, Net *net_out) {
   const int N = (int)items.size();
   std::vector<i64> totals(N + 1, -1);
-  const int nt = n_threads_for(N + 1);
-  std::atomic<int> next{0};
-  std::vector<PlanFail> errs;
+  // contiguous ranges of n per task; each task extends one prefix state incrementally
+  const int tasks = std::max(1, std::min(N + 1, 4 * Pool::get().threads()));
   std::atomic<bool> failed{false};
   PlanFail first_err{MLF_OK, ""};
-  auto worker = [&]() {
-    for (;;) {
-      int n = next.fetch_add(1);
-      if (n > N || failed.load()) return;
-      try {
-        AggCase cs = det_agg(n, items, net0, c, dsts, aggs, nullptr);
-        totals[n] = cs.feasible ? cs.total : -1;
-      } catch (const PlanFail &e) {
-        if (!failed.exchange(true)) first_err = e;
-      }
-    }
-  };
-  if (nt == 1) {
-    worker();
-  } else {
-    std::vector<std::thread> th;
-    for (int t = 0; t < nt; ++t) th.emplace_back(worker);
-    for (auto &t : th) t.join();
-  }
+  std::mutex err_m;
+  Pool::get().run(
+      tasks,
+      [&](int t) {
+        try {
+          const int n0 = (int)((int64_t)(N + 1) * t / tasks), n1 = (int)((int64_t)(N + 1) * (t + 1) / tasks);
+          if (n0 >= n1) return;
+          Prefix pre(net0);
+          for (int i = 0; i < n0; ++i) pre.extend(items, i, c, dsts);
+          for (int n = n0; n < n1; ++n) {
+            if (!pre.ok) break;
+            AggCase cs;
+            cs.n = n;
+            cs.commits = pre.commits;
+            Net nw = pre.nw;
+            det_agg_tail(cs, nw, pre.t_max, items, c, dsts, aggs);
+            totals[n] = cs.feasible ? cs.total : -1;
+            if (n < N) pre.extend(items, n, c, dsts);
+          }
+        } catch (const PlanFail &e) {
+          std::lock_guard<std::mutex> g(err_m);
+          if (!failed.exchange(true)) first_err = e;
+        }
+      },
+      2);
   if (failed.load()) throw first_err;
   int best = -1;
   for (int n = 0; n <= N; ++n)

@@ -53,7 +53,7 @@ class Workload:
                              model_elems=self.S, shard_begin=b, rank=rank, world=world, dtype=self.dt,
                              backup_shard=bptr, worker_rank=cfg["home"], node_rank=cfg["node_rank"],
                              n_nodes=cfg["n_nodes"], agg_slots=agg_slots, agg_scratch=agg_scratch,
-                             stream=self.stream.cuda_stream, v0=0)
+                             stream=self.stream.cuda_stream, v0=0, worker_node=cfg["worker_node"])
         self.v_init, self.v_prev = 0, 0
         self.iteration = 0
         self.carried = []
@@ -97,7 +97,7 @@ class Workload:
         self.v_prev = self.v_init
         self.v_init += plan_dict["n_commit"]
         if self.cfg["replica"]:
-            items = list(self.carried) + [dict(node=g, size=self.S * self.cfg["e"],
+            items = list(self.carried) + [dict(node=self.cfg["worker_node"][g], size=self.S * self.cfg["e"],
                                                norm=draws[g]["norm"]) for g in plan_dict["order"]]
             self.carried = [items[i] for i in plan_dict["punted"]]
         self.iteration += 1

@@ -79,7 +79,8 @@ class MlfConfig(C.Structure):
                 ("n_workers", C.c_int32), ("update_dtype", C.c_int32), ("lr", C.c_float),
                 ("model_shard", _p), ("backup_shard", _p), ("update_slot", C.POINTER(_p)),
                 ("worker_rank", _i32p), ("n_nodes", C.c_int32), ("node_rank", _i32p),
-                ("agg_slots", C.c_int32), ("agg_scratch", C.POINTER(_p)), ("stream", _p)]
+                ("worker_node", _i32p), ("agg_slots", C.c_int32), ("agg_scratch", C.POINTER(_p)),
+                ("stream", _p)]
 
 
 class MlfIpcHandle(C.Structure):
@@ -247,7 +248,7 @@ class Context:
     def __init__(self, *, device: int, model_shard, update_slots, lr: float, model_elems: int,
                  shard_begin: int = 0, rank: int = 0, world: int = 1, dtype: int = MLF_F32,
                  backup_shard=None, worker_rank=None, node_rank=None, n_nodes=None, agg_slots: int = 0,
-                 agg_scratch=None, stream=None, v0: int = 0):
+                 agg_scratch=None, stream=None, v0: int = 0, worker_node=None):
         """update_slots: list of int device pointers (or torch tensors); model_shard/backup_shard:
         torch tensors or int pointers; stream: int cudaStream_t (None -> default stream)."""
         def ptr(x):
@@ -259,13 +260,14 @@ class Context:
         self._wr = _arr(worker_rank if worker_rank is not None else [0] * self.n_workers, np.int32)
         nn = n_nodes if n_nodes is not None else (len(node_rank) if node_rank is not None else self.n_workers)
         self._nr = _arr(node_rank if node_rank is not None else [0] * nn, np.int32)
+        self._wn = _arr(worker_node, np.int32) if worker_node is not None else None
         scr = [ptr(s) for s in (agg_scratch or [])]
         self._scr = (_p * max(len(scr), 1))(*scr)
         shard_elems = model_shard.numel() if hasattr(model_shard, "numel") else int(model_elems)
         self.cfg = MlfConfig(device, rank, world, int(model_elems), int(shard_begin), int(shard_elems),
                              self.n_workers, dtype, float(lr), ptr(model_shard), ptr(backup_shard), self._slots,
-                             _ptr(self._wr, C.c_int32), int(nn), _ptr(self._nr, C.c_int32), int(agg_slots),
-                             self._scr, stream)
+                             _ptr(self._wr, C.c_int32), int(nn), _ptr(self._nr, C.c_int32),
+                             _ptr(self._wn, C.c_int32), int(agg_slots), self._scr, stream)
         self._h = _p()
         _check(_lib.mlf_init(C.byref(self.cfg), int(v0), C.byref(self._h)))
         self._bufs = None

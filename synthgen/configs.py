@@ -76,14 +76,17 @@ def config(cid: int, *, G: int | None = None, tau: int | None = None, dtype: str
         d["tau"] = 4 if tau is None else tau
         d["replan_rates"] = True
     else:
-        # box model: one site per GPU, NIC up/down = NVLink per direction, same site free
-        n = W + 2 * G
-        d["servers"] = list(range(W, W + G))
-        d["site"] = d["home"] + list(range(G)) + [(j + 1) % G for j in range(G)]
+        # box model: planner node g = GPU g.  Its NIC up/down = NVLink egress/ingress per
+        # direction, shared by every virtual worker multiplexed on it (as co-located workers
+        # share a host NIC); shard j's server is node j; the core
+        # (NVSwitch) is congestion-free; same node = zero-time transfer.
+        n = G
+        d["worker_node"] = list(d["home"])
+        d["servers"] = list(range(G))
+        d["site"] = None
         d["nic_up"] = [B_NV_BPS] * n
         d["nic_down"] = [B_NV_BPS] * n
-        firsts = [min(w for w in range(W) if d["home"][w] == g) for g in range(G)]
-        d["aggs"] = shuffle(seed, firsts, salt=3)
+        d["aggs"] = shuffle(seed, list(range(G)), salt=3)      # one aggregator per GPU
         d["tau"] = W if tau is None else tau
         if cid == 4:
             d["preset_net"] = "N2"
@@ -91,12 +94,12 @@ def config(cid: int, *, G: int | None = None, tau: int | None = None, dtype: str
             d["replan_rates"] = True
         if cid == 5:
             d["replica"] = True
-            d["replicas"] = list(range(W + G, W + 2 * G))
+            d["replicas"] = [(j + 1) % G for j in range(G)]   # backup of shard j lives on GPU j+1
             d["raggs"] = []
             d["div_max"] = 0.0
     d["n_nodes"] = n
-    d["node_rank"] = (d["home"] + list(range(G)) + [(j + 1) % G for j in range(G)])[:n] if cid >= 3 \
-        else [0] * n
+    d["node_rank"] = list(range(G)) if cid >= 3 else [0] * n
+    d.setdefault("worker_node", list(range(W)))
     d.setdefault("replicas", [])
     d.setdefault("raggs", [])
     return d

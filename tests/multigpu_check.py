@@ -58,7 +58,7 @@ def main():
             # oracle: same planner inputs
             up, down, site = configs.network(cfg, it)
             draws = configs.batch_draws(cfg, it, v_init, v_prev)
-            batch = [Item(g, cfg["S"] * cfg["e"], d["version"], d["t_avail"], d["norm"])
+            batch = [Item(cfg["worker_node"][g], cfg["S"] * cfg["e"], d["version"], d["t_avail"], d["norm"])
                      for g, d in enumerate(draws)]
             prm = Params(servers=cfg["servers"], aggs=cfg["aggs"], replicas=cfg["replicas"], raggs=cfg["raggs"],
                          v_init=v_init, tau_max=cfg["tau"], div_max=cfg["div_max"],
@@ -81,7 +81,8 @@ def main():
                 assert np.array_equal(mine[idx - b].view(np.uint32), backup_ref.view(np.uint32)), \
                     f"rank {rank} {mode}: mirror mismatch"
             if cfg["replica"]:
-                items = list(carried) + [dict(node=g, size=cfg["S"] * cfg["e"], norm=draws[g]["norm"])
+                items = list(carried) + [dict(node=cfg["worker_node"][g], size=cfg["S"] * cfg["e"],
+                                              norm=draws[g]["norm"])
                                          for g in op["order"]]
                 carried = [items[i] for i in op["punted"]]
             v_prev, v_init = v_init, v_init + op["n_commit"]

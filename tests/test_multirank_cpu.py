@@ -31,7 +31,7 @@ def _worker(rank, world, port, cid, q):
     for it in range(3):
         up, down, site = configs.network(cfg, it)
         draws = configs.batch_draws(cfg, it, v_init, v_prev)
-        batch = [dict(node=g, size=cfg["S"] * cfg["e"], **d) for g, d in enumerate(draws)]
+        batch = [dict(node=cfg["worker_node"][g], size=cfg["S"] * cfg["e"], **d) for g, d in enumerate(draws)]
         p = m.plan(cfg["n_nodes"], up, down, batch, cfg["servers"], site=site, aggs=cfg["aggs"],
                    replicas=cfg["replicas"], raggs=cfg["raggs"], v_init=v_init, tau_max=cfg["tau"],
                    div_max=cfg["div_max"], shard_weights=[n for (_, n) in cfg["shards"]])
