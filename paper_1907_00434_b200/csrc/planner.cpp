@@ -234,10 +234,14 @@ static bool transfer(const Net &net, const Pending *L0, const Pending *L1, i64 s
     const Seg *p;
     int n, idx;
     Seg own;
-    int s0, s1;       // subs range in `subs`
+    int e0, e1;       // pending-reservation events of this link, sorted by time: [e0, e1) in `ev`
+    i64 used;         // pending rate active at the cursor
   };
-  thread_local std::vector<TSeg> subs;
-  subs.clear();
+  struct Ev {
+    i64 t, d;         // at time t the pending rate changes by d
+  };
+  thread_local std::vector<Ev> ev;
+  ev.clear();
   Lk lk[3];
   const int nk = out.path.nk;
   for (int k = 0; k < nk; ++k) {
@@ -255,12 +259,25 @@ static bool transfer(const Net &net, const Pending *L0, const Pending *L1, i64 s
     const Seg *b = lk[k].p, *e = lk[k].p + lk[k].n;
     const Seg *it = std::upper_bound(b, e, t_avail, [](i64 v, const Seg &s) { return v < s.t; });
     lk[k].idx = it == b ? 0 : (int)(it - b) - 1;
-    lk[k].s0 = (int)subs.size();
+    lk[k].e0 = (int)ev.size();
+    lk[k].used = 0;
     for (const Pending *L : {L0, L1})
       if (L)
         for (const Res &r : *L)
-          if (r.key == key && r.s.b > t_avail) subs.push_back(r.s);
-    lk[k].s1 = (int)subs.size();
+          if (r.key == key && r.s.b > t_avail) {
+            if (r.s.a <= t_avail)
+              lk[k].used += r.s.r;
+            else
+              ev.push_back({r.s.a, r.s.r});
+            ev.push_back({r.s.b, -r.s.r});
+          }
+    lk[k].e1 = (int)ev.size();
+    for (int i = lk[k].e0 + 1; i < lk[k].e1; ++i) {      // insertion sort: a few dozen events at most
+      Ev x = ev[i];
+      int j = i - 1;
+      for (; j >= lk[k].e0 && ev[j].t > x.t; --j) ev[j + 1] = ev[j];
+      ev[j + 1] = x;
+    }
   }
   i128 need = (i128)size * NS_PER_S;
   i64 cur = t_avail;
@@ -270,17 +287,10 @@ static bool transfer(const Net &net, const Pending *L0, const Pending *L1, i64 s
     for (int k = 0; k < nk; ++k) {
       Lk &L = lk[k];
       while (L.idx + 1 < L.n && L.p[L.idx + 1].t <= cur) ++L.idx;
-      i64 rk = L.p[L.idx].r;
+      while (L.e0 < L.e1 && ev[L.e0].t <= cur) L.used += ev[L.e0++].d;
+      const i64 rk = L.p[L.idx].r - L.used;
       i64 nbk = L.idx + 1 < L.n ? L.p[L.idx + 1].t : T_INF;
-      for (int s = L.s0; s < L.s1; ++s) {
-        const TSeg &q = subs[s];
-        if (q.a <= cur && cur < q.b) {
-          rk -= q.r;
-          nbk = std::min(nbk, q.b);
-        } else if (q.a > cur) {
-          nbk = std::min(nbk, q.a);
-        }
-      }
+      if (L.e0 < L.e1) nbk = std::min(nbk, ev[L.e0].t);
       r = std::min(r, rk);
       nb = std::min(nb, nbk);
     }
@@ -404,7 +414,7 @@ struct OrderRes {
   std::vector<uint8_t> reason;
 };
 
-static constexpr int kMinParallelEvals = 24;
+static constexpr int kMinParallelEvals = 128;   // component transfers per scan worth a pool dispatch
 
 static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 tau, i64 v_init) {
   const int n = (int)batch.size();
@@ -419,7 +429,7 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
   const int G = (int)c.servers.size();
   std::vector<i64> ten(n);
   std::vector<uint8_t> ok(n);
-  std::vector<int> pool;
+  std::vector<int> pool, uniq, rep;
 
   // ShrtDline(pos, cands, NW + L0): the due set's argmin if any, else ShrtUp (R4, R6).
   auto pick = [&](i64 pos, const std::vector<int> &cands, const Pending *L0) -> int {
@@ -432,11 +442,26 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
     pool.clear();
     for (int g : cands)
       if (!any_due || dl[g] == pos) pool.push_back(g);
+    // t_en is a pure function of (network, node, size, t_avail): evaluate each distinct
+    // triple once (virtual workers on one GPU usually share all three)
+    uniq.clear();
+    rep.assign(n, -1);
+    for (int g : pool) {
+      int u = -1;
+      for (int q : uniq)
+        if (batch[q].node == batch[g].node && batch[q].size == batch[g].size &&
+            batch[q].t_avail == batch[g].t_avail) {
+          u = q;
+          break;
+        }
+      if (u < 0) uniq.push_back(g);
+      rep[g] = u < 0 ? g : u;
+    }
     Pool::get().run(
-        (int)pool.size(),
+        (int)uniq.size(),
         [&](int i) {
           thread_local Pending local;
-          const int g = pool[i];
+          const int g = uniq[i];
           Send s;
           ok[g] = send(nw, L0, c, c.servers, batch[g].node, batch[g].size, batch[g].t_avail, s, local);
           ten[g] = s.t_en;
@@ -444,6 +469,8 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
         std::max(1, kMinParallelEvals / std::max(1, G)));
     int best = -1;
     for (int g : pool) {
+      ok[g] = ok[rep[g]];
+      ten[g] = ten[rep[g]];
       if (!ok[g]) throw PlanFail{MLF_E_UNSCHEDULABLE, "update path to a server is down"};
       if (best < 0 || ten[g] < ten[best]) best = g;
     }
@@ -579,9 +606,25 @@ static AggCase det_agg(int n, const std::vector<Item> &items, const Net &net0, c
 static AggCase plan_aggregation(const std::vector<Item> &items, const Net &net0, const Ctx &c,
                                 const std::vector<int> &dsts, const std::vector<int> &aggs, Net *net_out) {
   const int N = (int)items.size();
+  // no aggregators: every case n < |U| meets aid = 1 > k at its first tail item (R12), so
+  // only the all-direct case is feasible
+  if (aggs.empty()) return det_agg(N, items, net0, c, dsts, aggs, net_out);
   std::vector<i64> totals(N + 1, -1);
-  // contiguous ranges of n per task; each task extends one prefix state incrementally
-  const int tasks = std::max(1, std::min(N + 1, 4 * Pool::get().threads()));
+  // contiguous ranges of n per task; the prefix states at the range starts are built in
+  // one sequential pass, then every task extends its own copy incrementally
+  // (small batches: one task, no dispatch overhead)
+  const int tasks = (N + 1) * (int)dsts.size() < 256 ? 1 : std::max(1, std::min(N + 1, 2 * Pool::get().threads()));
+  std::vector<Prefix> starts;
+  starts.reserve(tasks);
+  {
+    Prefix pre(net0);
+    int done = 0;
+    for (int t = 0; t < tasks; ++t) {
+      const int n0 = (int)((int64_t)(N + 1) * t / tasks);
+      for (; done < n0; ++done) pre.extend(items, done, c, dsts);
+      starts.push_back(pre);
+    }
+  }
   std::atomic<bool> failed{false};
   PlanFail first_err{MLF_OK, ""};
   std::mutex err_m;
@@ -591,8 +634,7 @@ static AggCase plan_aggregation(const std::vector<Item> &items, const Net &net0,
         try {
           const int n0 = (int)((int64_t)(N + 1) * t / tasks), n1 = (int)((int64_t)(N + 1) * (t + 1) / tasks);
           if (n0 >= n1) return;
-          Prefix pre(net0);
-          for (int i = 0; i < n0; ++i) pre.extend(items, i, c, dsts);
+          Prefix &pre = starts[t];
           for (int n = n0; n < n1; ++n) {
             if (!pre.ok) break;
             AggCase cs;

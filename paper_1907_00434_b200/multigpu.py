@@ -145,7 +145,9 @@ class ShardedWorkload:
         """One batch on every rank.  Returns (plan dict, this rank's device ms)."""
         wl = self.wl
         draws = wl.submit_all(iteration)
+        t0 = time.perf_counter()
         pb = wl.plan(iteration)
+        self.last_plan_ms = (time.perf_counter() - t0) * 1e3
         pd = pb.to_dict(self.cfg["W"])
         if flush is not None:
             flush()
@@ -332,7 +334,7 @@ def run_bench_multi(a):
                 t_roof = max(max(tr["hbm"][j] / (peak_hbm * 1e9), tr["nv_in"][j] / (b_nv * 1e9),
                                  tr["nv_out"][j] / (b_nv * 1e9)) for j in range(world))
                 recs.append(dict(ms=ms_max, bytes=committed_bytes(cfg, pd), t_roof=t_roof, tr=tr,
-                                 commits=pd["n_commit"], groups=pd["n_groups"]))
+                                 commits=pd["n_commit"], groups=pd["n_groups"], plan_ms=sw.last_plan_ms))
         if clocks:
             ck.__exit__()
         kl = sw.wl.ctx.stats()[0] - kl0
@@ -383,6 +385,7 @@ def run_bench_multi(a):
                      "plan_relative_t_roof_ms": round(t_roof * 1e3 / len(recs), 4),
                      "kernel": f"fused_commit_{a.kernel}"},
         "nvlink_measured_GBps": nv_meas,
+        "planner_ms": round(sum(r["plan_ms"] for r in recs) / len(recs), 3),
         "gpu_launches": int(kl),
         "clocks": ck.summary(),
     }

@@ -2,7 +2,7 @@
 # Multi-GPU evidence on one box: parity check, then bench at N = 2, 4, 8 (config 3) and config 5 at N = 8.
 OUT=${OUT:-gpurun_out}
 NG=$(nvidia-smi -L | wc -l)
-timeout 300 python -m torch.distributed.run --standalone --nproc-per-node $NG tests/multigpu_check.py --cid 5 --S 4000037 > $OUT/check_n$NG.log 2>&1; echo rc=$? >> $OUT/check_n$NG.log
+timeout 300 python -m torch.distributed.run --standalone --nproc-per-node $NG tests/multigpu_check.py --cid 3 --S 4000037 > $OUT/check_n$NG.log 2>&1; echo rc=$? >> $OUT/check_n$NG.log
 for N in 2 4 8; do
   [ $N -le $NG ] || continue
   timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 2953$N \
