@@ -17,20 +17,19 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.h"
 
 namespace mlf {
 namespace bulk {
 
-constexpr int kTile = 2048;                     // elements per tile
-constexpr int kStageBytes = kTile * 4;          // an fp32 tile (bf16 tiles use half a stage)
-constexpr int kStages = 24;                     // 192 KB ring
 constexpr int kConsumerWarps = 8;
 constexpr int kConsumers = kConsumerWarps * 32;
 constexpr int kThreads = kConsumers + 32;       // + 1 producer warp
-constexpr int kChunks = kTile / 4 / kConsumers; // float4 chunks per consumer thread per tile (2)
-constexpr size_t kSmem = (size_t)kStages * kStageBytes + 2 * kStages * sizeof(uint64_t);
+constexpr size_t smem_bytes(int tile, int stages) {
+  return (size_t)stages * tile * 4 + 2 * stages * sizeof(uint64_t);
+}
 
 __device__ __forceinline__ uint32_t smem_addr(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -72,7 +71,12 @@ __device__ __forceinline__ float4 widen_bf16x4(uint2 u) {
                      __uint_as_float(u.y & 0xffff0000u));
 }
 
+// kTile elements per tile (one fp32 tile per stage; bf16 tiles use half), kStages-deep ring
+template <int kTile, int kStages>
 __global__ void __launch_bounds__(kThreads, 1) fused_commit_bulk(const __grid_constant__ CommitArgs a) {
+  constexpr int kStageBytes = kTile * 4;
+  constexpr int kChunks = kTile / 4 / kConsumers;   // float4 chunks per consumer thread per tile
+  static_assert(kChunks >= 1 && kTile % (4 * kConsumers) == 0, "tile must be a multiple of 4 * consumers");
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)kStages * kStageBytes);
   uint64_t *empty = full + kStages;
@@ -204,18 +208,33 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_bulk(const __grid_co
 
 }  // namespace bulk
 
-cudaError_t launch_commit_bulk(const CommitArgs &a, cudaStream_t s, int sm_count) {
+template <int kTile, int kStages>
+static cudaError_t launch_tile(const CommitArgs &a, cudaStream_t s, int sm_count) {
+  constexpr size_t smem = bulk::smem_bytes(kTile, kStages);
   static bool init = false;
   if (!init) {
-    cudaError_t e = cudaFuncSetAttribute(bulk::fused_commit_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)bulk::kSmem);
+    cudaError_t e = cudaFuncSetAttribute(bulk::fused_commit_bulk<kTile, kStages>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     init = true;
   }
-  const int64_t n_tiles = ((a.n & ~int64_t(7)) + bulk::kTile - 1) / bulk::kTile;
+  const int64_t n_tiles = ((a.n & ~int64_t(7)) + kTile - 1) / kTile;
   int grid = (int)(n_tiles < sm_count ? (n_tiles > 0 ? n_tiles : 1) : sm_count);
-  bulk::fused_commit_bulk<<<grid, bulk::kThreads, bulk::kSmem, s>>>(a);
+  bulk::fused_commit_bulk<kTile, kStages><<<grid, bulk::kThreads, smem, s>>>(a);
   return cudaGetLastError();
+}
+
+// Tile size (elements) per bulk copy: MLF_BULK_TILE in {2048, 4096, 8192}, default 2048;
+// the ring is always 192 KB.
+cudaError_t launch_commit_bulk(const CommitArgs &a, cudaStream_t s, int sm_count) {
+  static int tile = 0;
+  if (tile == 0) {
+    const char *e = getenv("MLF_BULK_TILE");
+    tile = e ? atoi(e) : 2048;
+  }
+  if (tile == 8192) return launch_tile<8192, 6>(a, s, sm_count);
+  if (tile == 4096) return launch_tile<4096, 12>(a, s, sm_count);
+  return launch_tile<2048, 24>(a, s, sm_count);
 }
 
 }  // namespace mlf
