@@ -224,17 +224,19 @@ static cudaError_t launch_tile(const CommitArgs &a, cudaStream_t s, int sm_count
   return cudaGetLastError();
 }
 
-// Tile size (elements) per bulk copy: MLF_BULK_TILE in {2048, 4096, 8192}, default 2048;
-// the ring is always 192 KB.
+// Tile size (elements) per bulk copy: MLF_BULK_TILE in {2048, 4096, 8192}; the ring is
+// always 192 KB.  Default 4096 (16 KB per copy): measured best on one B200 (99.7% of the
+// HBM copy roofline at config 2, tau 4, vs 93.5% at 2048 and 8192); NVLink-bound runs
+// are insensitive to the tile size.
 cudaError_t launch_commit_bulk(const CommitArgs &a, cudaStream_t s, int sm_count) {
   static int tile = 0;
   if (tile == 0) {
     const char *e = getenv("MLF_BULK_TILE");
-    tile = e ? atoi(e) : 2048;
+    tile = e ? atoi(e) : 4096;
   }
   if (tile == 8192) return launch_tile<8192, 6>(a, s, sm_count);
-  if (tile == 4096) return launch_tile<4096, 12>(a, s, sm_count);
-  return launch_tile<2048, 24>(a, s, sm_count);
+  if (tile == 2048) return launch_tile<2048, 24>(a, s, sm_count);
+  return launch_tile<4096, 12>(a, s, sm_count);
 }
 
 }  // namespace mlf
