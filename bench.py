@@ -369,7 +369,7 @@ def main():
     rank, world, local = dist_env()
     multi = world > 1 or a.gpus > 1
     if a.kernel is None:
-        a.kernel = "bulk" if multi else "ldg"
+        a.kernel = "bulk"
     if multi:
         from paper_1907_00434_b200.multigpu import run_bench_multi
         run_bench_multi(a)
