@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--kernel", default=os.environ.get("MLF_COMMIT_IMPL"), choices=["ldg", "bulk"],
-                    help="fused commit kernel (default: ldg on 1 GPU, bulk when operands cross NVLink)")
+                    help="fused commit kernel (default bulk: TMA bulk copies; ldg: 128-bit load streaming)")
     return ap.parse_args()
 
 
