@@ -174,6 +174,17 @@ typedef struct {
                                   inside the commit kernel, no materialised aggregates) */
   float *const *agg_scratch;   /* [world*agg_slots] S-element fp32 buffers valid on `device` */
   void *stream;                /* cudaStream_t (borrowed) */
+  /* Momentum (Eq. 2: w <- w + u + gamma (w_t - w_{t-1}), u = -lr * g).  gamma = 0: the
+   * hot path above.  gamma in (0,1): the server keeps the history h = w_t - w_{t-1}
+   * (history_shard, fp32, shard_elems) and a commit of m updates u_1..u_m applies the
+   * aggregate form of m sequential Eq. 2 steps ("consistent to the case with no
+   * aggregation"): w += (sum_{j=1..m} g^j) h + sum_i (sum_{j=0..m-i} g^j) u_i,
+   * h = g^m h + sum_i g^(m-i) u_i, two weighted sums in one pass (the aggregators'
+   * "weighted sum").  backup_history receives h at the mirror boundary.
+   * Requires fold mode (agg_slots = 0) and the bulk kernel. */
+  float gamma;
+  float *history_shard;
+  float *backup_history;
 } mlf_config;
 
 typedef struct mlf_ctx mlf_ctx;

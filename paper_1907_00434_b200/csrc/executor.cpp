@@ -103,6 +103,15 @@ extern "C" mlf_status mlf_init(const mlf_config *cfg, int64_t v0, mlf_ctx **out)
     if (k.update_dtype != MLF_F32 && k.update_dtype != MLF_BF16) throw Fail{MLF_E_INVALID, "update dtype"};
     if (k.shard_elems > 0 && !k.model_shard) throw Fail{MLF_E_INVALID, "model shard"};
     if (k.agg_slots < 0 || (k.agg_slots > 0 && !k.agg_scratch)) throw Fail{MLF_E_INVALID, "aggregate scratch"};
+    if (!(k.gamma >= 0.f && k.gamma < 1.f)) throw Fail{MLF_E_INVALID, "gamma must be in [0, 1)"};
+    if (k.gamma != 0.f) {
+      if (k.shard_elems > 0 && !k.history_shard) throw Fail{MLF_E_INVALID, "momentum needs history_shard"};
+      if (k.backup_shard && !k.backup_history) throw Fail{MLF_E_INVALID, "momentum mirror needs backup_history"};
+      if (k.world > 1 && k.agg_slots > 0)
+        throw Fail{MLF_E_INVALID, "momentum is executed in fold mode (agg_slots = 0)"};
+      if ((reinterpret_cast<uintptr_t>(k.history_shard) & 15) || (reinterpret_cast<uintptr_t>(k.backup_history) & 15))
+        throw Fail{MLF_E_INVALID, "history buffers not 16-byte aligned"};
+    }
     if (k.n_nodes < 1) throw Fail{MLF_E_INVALID, "n_nodes < 1"};
     for (int w = 0; w < k.n_workers; ++w) {
       int nd = k.worker_node ? k.worker_node[w] : w;
@@ -342,6 +351,69 @@ static void reduce_local_groups(mlf_ctx *c, const mlf_plan_out *p) {
   }
 }
 
+struct CommitOp {
+  const void *ptr;
+  uint8_t flag;
+  int commit;      // 1-based server commit index
+};
+
+// Momentum commits (NEXT-1, Eq. 2 with gamma > 0): the aggregate form's weights per member
+// and per commit, from float64 powers summed left to right (oracle/momentum.py coefficients).
+static void launch_momentum(mlf_ctx *c, const mlf_plan_out *p, const std::vector<CommitOp> &ops, int boundary) {
+  const double g = c->cfg.gamma;
+  size_t i0 = 0;
+  bool first_launch = true;
+  while (i0 < ops.size() || (first_launch && c->cfg.shard_elems > 0 && boundary == 0)) {
+    size_t i1 = std::min(ops.size(), i0 + (size_t)kMaxOpsM);
+    if (i1 < ops.size())
+      while (i1 > i0 && !(ops[i1 - 1].flag & kOpLast)) --i1;
+    if (i1 == i0 && i0 < ops.size()) throw Fail{MLF_E_CAPACITY, "a single commit has more than kMaxOpsM members"};
+    MomentumArgs a;
+    a.w = c->cfg.model_shard;
+    a.h = c->cfg.history_shard;
+    a.backup = c->cfg.backup_shard;
+    a.backup_h = c->cfg.backup_history;
+    a.n = c->cfg.shard_elems;
+    a.src_off = c->cfg.shard_begin;
+    a.lr = c->cfg.lr;
+    a.n_ops = (int32_t)(i1 - i0);
+    a.backup_after = (first_launch && boundary == 0) ? -1 : -2;
+    size_t q = i0;
+    while (q < i1) {
+      const int ci = ops[q].commit;
+      size_t e = q;
+      while (e < i1 && ops[e].commit == ci) ++e;
+      const int m = (int)(e - q);
+      std::vector<double> pw(m + 1);
+      pw[0] = 1.0;
+      for (int j = 1; j <= m; ++j) pw[j] = pw[j - 1] * g;
+      double sh = 0.0;
+      for (int j = 1; j <= m; ++j) sh += pw[j];
+      for (int i = 1; i <= m; ++i) {
+        double ca = 0.0;
+        for (int j = 0; j <= m - i; ++j) ca += pw[j];
+        const size_t o = q + i - 1 - i0;
+        a.op[o] = ops[q + i - 1].ptr;
+        a.flag[o] = ops[q + i - 1].flag;
+        a.cA[o] = (float)ca;
+        a.cB[o] = (float)pw[m - i];
+        a.sh[o] = (float)sh;
+        a.gm[o] = (float)pw[m];
+      }
+      if (boundary > 0 && ci == boundary) a.backup_after = (int32_t)(e - 1 - i0);
+      q = e;
+    }
+    if (a.n > 0) {
+      record_start(c);
+      CK(launch_commit_momentum(a, c->stream, c->sm_count));
+      ++c->launches;
+    }
+    first_launch = false;
+    i0 = i1;
+    if (ops.empty()) break;
+  }
+}
+
 static void phase_commit(mlf_ctx *c, const mlf_plan_out *p) {
   CK(cudaSetDevice(c->cfg.device));
   // aggregates / staged updates of the other ranks are complete (phase events)
@@ -349,12 +421,7 @@ static void phase_commit(mlf_ctx *c, const mlf_plan_out *p) {
   const bool tree = tree_mode(c);
   const uint8_t dflag = c->cfg.update_dtype == MLF_BF16 ? kOpBf16 : 0;
   // operand table in commit order
-  struct Op {
-    const void *ptr;
-    uint8_t flag;
-    int commit;
-  };
-  std::vector<Op> ops;
+  std::vector<CommitOp> ops;
   for (int ci = 0; ci < p->n_server_commits; ++ci) {
     int first = p->commit_first[ci], cnt = p->commit_count[ci];
     int gid = p->group[p->order[first]];
@@ -372,6 +439,9 @@ static void phase_commit(mlf_ctx *c, const mlf_plan_out *p) {
     }
   }
   const int boundary = c->cfg.backup_shard ? p->replica_boundary_commit : -1;
+  if (c->cfg.gamma != 0.f) {
+    launch_momentum(c, p, ops, boundary);
+  } else {
   // launches, split at commit boundaries when the list exceeds kMaxOps
   size_t i0 = 0;
   bool first_launch = true;
@@ -402,6 +472,7 @@ static void phase_commit(mlf_ctx *c, const mlf_plan_out *p) {
     first_launch = false;
     i0 = i1;
     if (ops.empty()) break;
+  }
   }
   record_start(c);
   CK(cudaEventRecord(c->ev_stop, c->stream));

@@ -38,7 +38,26 @@ struct ReduceArgs {
   uint8_t flag[kMaxOps];
 };
 
+// Momentum commit (Eq. 2 with gamma > 0, aggregate form): per operand the weights of the two
+// weighted sums, per commit (stored at its last operand) the history weights.
+constexpr int kMaxOpsM = 512;
+struct MomentumArgs {
+  float *w, *h;              // [n] shard slice and its history, read once, written once
+  float *backup, *backup_h;  // mirror targets or nullptr
+  int64_t n, src_off;
+  float lr;
+  int32_t n_ops, backup_after;
+  const void *op[kMaxOpsM];
+  uint8_t flag[kMaxOpsM];
+  float cA[kMaxOpsM];        // sum_{j=0..m-i} g^j   (w's weight of member i)
+  float cB[kMaxOpsM];        // g^(m-i)              (h's weight of member i)
+  float sh[kMaxOpsM];        // sum_{j=1..m} g^j     (at the commit's last operand)
+  float gm[kMaxOpsM];        // g^m                  (at the commit's last operand)
+};
+
 enum class CommitImpl : int { kLdg = 0, kBulk = 1 };
+
+cudaError_t launch_commit_momentum(const MomentumArgs &a, cudaStream_t s, int sm_count);
 
 cudaError_t launch_commit(const CommitArgs &a, cudaStream_t s, int sm_count, CommitImpl impl);
 cudaError_t launch_commit_bulk(const CommitArgs &a, cudaStream_t s, int sm_count);

@@ -22,7 +22,7 @@ class Workload:
 
     def __init__(self, cfg: dict, *, device: int = 0, rank: int = 0, world: int = 1, variant: int = 0,
                  peer_slots=None, backup_ptr=None, agg_slots: int = 0, agg_scratch=None, stream=None,
-                 slot_tensors: dict | None = None):
+                 slot_tensors: dict | None = None, backup_h_ptr=None):
         self.cfg = cfg
         self.device, self.rank, self.world = device, rank, world
         self.variant = variant
@@ -35,6 +35,11 @@ class Workload:
         self.stream = stream or torch.cuda.current_stream(dev)
         self.w = torch.empty(n, dtype=torch.float32, device=dev)
         self.backup = torch.zeros(n, dtype=torch.float32, device=dev) if (cfg["replica"] and world == 1) else None
+        # momentum (NEXT-1): the server-side history h = w_t - w_{t-1}, zero at start
+        self.gamma = cfg.get("gamma", 0.0)
+        self.h = torch.zeros(n, dtype=torch.float32, device=dev) if self.gamma else None
+        self.backup_h = (torch.zeros(n, dtype=torch.float32, device=dev)
+                         if (self.gamma and cfg["replica"] and world == 1) else None)
         # update slots of the workers homed here (full-length vectors)
         self.local_workers = [w for w in range(cfg["W"]) if cfg["home"][w] == rank]
         if slot_tensors is not None:
@@ -53,7 +58,9 @@ class Workload:
                              model_elems=self.S, shard_begin=b, rank=rank, world=world, dtype=self.dt,
                              backup_shard=bptr, worker_rank=cfg["home"], node_rank=cfg["node_rank"],
                              n_nodes=cfg["n_nodes"], agg_slots=agg_slots, agg_scratch=agg_scratch,
-                             stream=self.stream.cuda_stream, v0=0, worker_node=cfg["worker_node"])
+                             stream=self.stream.cuda_stream, v0=0, worker_node=cfg["worker_node"],
+                             gamma=self.gamma, history=self.h,
+                             backup_history=(backup_h_ptr if backup_h_ptr is not None else self.backup_h))
         self.v_init, self.v_prev = 0, 0
         self.iteration = 0
         self.carried = []
@@ -77,8 +84,9 @@ class Workload:
         net, k1 = m.make_net(c["n_nodes"], up, down, None, site)
         weights = [n for (_, n) in c["shards"]] if c["G"] > 1 else None
         prm, k2 = m.make_params(c["servers"], aggs=c["aggs"], replicas=c["replicas"], raggs=c["raggs"],
-                                v_init=self.v_init, tau_max=c["tau"], div_max=c["div_max"], gamma=0.0,
-                                hist_norm=0.0, carried=self.carried, shard_weights=weights)
+                                v_init=self.v_init, tau_max=c["tau"], div_max=c["div_max"],
+                                gamma=c.get("gamma", 0.0), hist_norm=0.0, carried=self.carried,
+                                shard_weights=weights)
         return net, prm, (k1, k2)
 
     def submit_all(self, iteration: int):

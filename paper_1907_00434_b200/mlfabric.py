@@ -80,7 +80,7 @@ class MlfConfig(C.Structure):
                 ("model_shard", _p), ("backup_shard", _p), ("update_slot", C.POINTER(_p)),
                 ("worker_rank", _i32p), ("n_nodes", C.c_int32), ("node_rank", _i32p),
                 ("worker_node", _i32p), ("agg_slots", C.c_int32), ("agg_scratch", C.POINTER(_p)),
-                ("stream", _p)]
+                ("stream", _p), ("gamma", C.c_float), ("history_shard", _p), ("backup_history", _p)]
 
 
 class MlfIpcHandle(C.Structure):
@@ -248,7 +248,8 @@ class Context:
     def __init__(self, *, device: int, model_shard, update_slots, lr: float, model_elems: int,
                  shard_begin: int = 0, rank: int = 0, world: int = 1, dtype: int = MLF_F32,
                  backup_shard=None, worker_rank=None, node_rank=None, n_nodes=None, agg_slots: int = 0,
-                 agg_scratch=None, stream=None, v0: int = 0, worker_node=None):
+                 agg_scratch=None, stream=None, v0: int = 0, worker_node=None, gamma: float = 0.0,
+                 history=None, backup_history=None):
         """update_slots: list of int device pointers (or torch tensors); model_shard/backup_shard:
         torch tensors or int pointers; stream: int cudaStream_t (None -> default stream)."""
         def ptr(x):
@@ -267,7 +268,8 @@ class Context:
         self.cfg = MlfConfig(device, rank, world, int(model_elems), int(shard_begin), int(shard_elems),
                              self.n_workers, dtype, float(lr), ptr(model_shard), ptr(backup_shard), self._slots,
                              _ptr(self._wr, C.c_int32), int(nn), _ptr(self._nr, C.c_int32),
-                             _ptr(self._wn, C.c_int32), int(agg_slots), self._scr, stream)
+                             _ptr(self._wn, C.c_int32), int(agg_slots), self._scr, stream, float(gamma),
+                             ptr(history), ptr(backup_history))
         self._h = _p()
         _check(_lib.mlf_init(C.byref(self.cfg), int(v0), C.byref(self._h)))
         self._bufs = None

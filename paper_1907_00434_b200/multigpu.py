@@ -95,6 +95,8 @@ class ShardedWorkload:
         prev = (rank - 1) % world
         self.mirror = (torch.zeros(cfg["shards"][prev][1], dtype=torch.float32, device=dev)
                        if cfg["replica"] else None)
+        self.mirror_h = (torch.zeros(cfg["shards"][prev][1], dtype=torch.float32, device=dev)
+                         if (cfg["replica"] and cfg.get("gamma", 0.0)) else None)
         self.n_slots = agg_slots_needed(cfg, world) if mode == "tree" else 0
         self.scratch = (torch.empty((self.n_slots, self.row), dtype=torch.float32, device=dev)
                         if self.n_slots else None)
@@ -102,6 +104,8 @@ class ShardedWorkload:
         mine = {"rank": rank, "workers": local,
                 "slots": m.ipc_export(device, self.slots_all.data_ptr()),
                 "mirror": m.ipc_export(device, self.mirror.data_ptr()) if self.mirror is not None else None,
+                "mirror_h": (m.ipc_export(device, self.mirror_h.data_ptr())
+                             if self.mirror_h is not None else None),
                 "scratch": m.ipc_export(device, self.scratch.data_ptr()) if self.scratch is not None else None}
         allinfo = [None] * world
         dist.all_gather_object(allinfo, mine, group=ctrl)
@@ -113,10 +117,13 @@ class ShardedWorkload:
             base = self.slots_all.data_ptr() if r == rank else self.mapper.open(info["slots"])
             for i, w in enumerate(info["workers"]):
                 peer_slots[w] = base + i * self.row * e
-        backup_ptr = None
+        backup_ptr = backup_h_ptr = None
         if cfg["replica"]:
             nxt = (rank + 1) % world
             backup_ptr = self.mirror.data_ptr() if nxt == rank else self.mapper.open(allinfo[nxt]["mirror"])
+            if self.mirror_h is not None:
+                backup_h_ptr = (self.mirror_h.data_ptr() if nxt == rank
+                                else self.mapper.open(allinfo[nxt]["mirror_h"]))
         scratch_tab = None
         if self.n_slots:
             scratch_tab = []
@@ -125,7 +132,7 @@ class ShardedWorkload:
                 scratch_tab += [base + s * self.row * 4 for s in range(self.n_slots)]
         self.wl = Workload(cfg, device=device, rank=rank, world=world, variant=variant, peer_slots=peer_slots,
                            backup_ptr=backup_ptr, agg_slots=self.n_slots, agg_scratch=scratch_tab,
-                           slot_tensors=slot_tensors)
+                           slot_tensors=slot_tensors, backup_h_ptr=backup_h_ptr)
         ev = self.wl.ctx.phase_event()
         evs = [None] * world
         dist.all_gather_object(evs, (rank, ev), group=ctrl)

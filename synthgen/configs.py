@@ -35,7 +35,7 @@ def shard_bounds(S: int, G: int, align: int = 64):
 
 
 def config(cid: int, *, G: int | None = None, tau: int | None = None, dtype: str = "f32",
-           seed: int = SEED_ROOT, scale_S: int | None = None) -> dict:
+           seed: int = SEED_ROOT, scale_S: int | None = None, gamma: float = 0.0) -> dict:
     """Static part of config `cid` (1..5)."""
     if cid == 1:
         W, S, G = 4, 1 << 20, 1
@@ -52,7 +52,7 @@ def config(cid: int, *, G: int | None = None, tau: int | None = None, dtype: str
     if scale_S is not None:
         S = scale_S
     d = dict(cid=cid, W=W, S=S, G=G, dtype=dtype, seed=seed, lr=0.01, div_max=math.inf, replica=False,
-             preset_net=None, preset_c=None, replan_rates=False)
+             preset_net=None, preset_c=None, replan_rates=False, gamma=gamma)
     d["e"] = 2 if dtype == "bf16" else 4
     d["home"] = [w * G // W for w in range(W)]            # block placement of virtual workers
     d["shards"] = shard_bounds(S, G)

@@ -22,7 +22,8 @@ import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
 import synthgen as sg  # noqa: E402
-from oracle.numerics import execute_plan  # noqa: E402
+from oracle.momentum import weighted_f32  # noqa: E402
+from oracle.numerics import commits_from_plan, execute_plan  # noqa: E402
 from oracle.plan import Item, Params, make_net, plan as oracle_plan  # noqa: E402
 from paper_1907_00434_b200.multigpu import ShardedWorkload, init_dist  # noqa: E402
 from synthgen import configs  # noqa: E402
@@ -35,7 +36,8 @@ def main():
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--dtype", default="f32")
     ap.add_argument("--modes", default="fold,tree")
-    ap.add_argument("--kernel", default="ldg")
+    ap.add_argument("--kernel", default="bulk")
+    ap.add_argument("--gamma", type=float, default=0.0)
     a = ap.parse_args()
     os.environ["MLF_COMMIT_IMPL"] = a.kernel
     rank, world, local, ctrl = init_dist()
@@ -43,13 +45,16 @@ def main():
     torch.cuda.set_device(device)
     dt = sg.DTYPE_BF16 if a.dtype == "bf16" else sg.DTYPE_F32
     for mode in a.modes.split(","):
-        cfg = configs.config(a.cid, G=world, dtype=a.dtype, scale_S=a.S)
+        if a.gamma and mode != "fold":
+            continue                             # momentum runs in fold mode only
+        cfg = configs.config(a.cid, G=world, dtype=a.dtype, scale_S=a.S, gamma=a.gamma)
         sw = ShardedWorkload(cfg, rank, world, device, ctrl, mode=mode)
         b, n = cfg["shards"][rank]
         rng = np.random.default_rng(rank)
         idx = np.unique(np.concatenate([rng.integers(b, b + n, 5000), np.arange(b, min(b + 17, b + n)),
                                         np.arange(max(b, b + n - 17), b + n)]))
         w_ref = sg.w0_values(cfg["seed"], idx)
+        h_ref = np.zeros(len(idx), np.float32)
         carried = []
         v_init = v_prev = 0
         for it in range(a.steps):
@@ -61,13 +66,20 @@ def main():
             batch = [Item(cfg["worker_node"][g], cfg["S"] * cfg["e"], d["version"], d["t_avail"], d["norm"])
                      for g, d in enumerate(draws)]
             prm = Params(servers=cfg["servers"], aggs=cfg["aggs"], replicas=cfg["replicas"], raggs=cfg["raggs"],
-                         v_init=v_init, tau_max=cfg["tau"], div_max=cfg["div_max"],
+                         v_init=v_init, tau_max=cfg["tau"], div_max=cfg["div_max"], gamma=cfg["gamma"],
                          carried=[Item(c["node"], c["size"], 0, 0, c["norm"]) for c in carried],
                          shard_weights=[x for (_, x) in cfg["shards"]])
             op = oracle_plan(make_net(cfg["n_nodes"], up, down, None, site), batch, prm)
             assert op == pd, f"rank {rank}: plan mismatch"
-            w_ref, backup_ref, _ = execute_plan(
-                w_ref, op, lambda g: sg.update_values(cfg["seed"], g, it, idx, dt), cfg["lr"])
+            operand = lambda g: sg.update_values(cfg["seed"], g, it, idx, dt)  # noqa: E731
+            if a.gamma:
+                w_ref, h_ref, bk = weighted_f32(w_ref, h_ref, commits_from_plan(op, operand), cfg["lr"],
+                                                a.gamma, op["replica_boundary_commit"])
+                backup_ref = bk[0] if bk is not None else None
+                got_h = sw.wl.h.cpu().numpy()[idx - b]
+                assert np.array_equal(got_h.view(np.uint32), h_ref.view(np.uint32)), f"rank {rank}: h mismatch"
+            else:
+                w_ref, backup_ref, _ = execute_plan(w_ref, op, operand, cfg["lr"])
             got = sw.wl.w.cpu().numpy()[idx - b]
             assert np.array_equal(got.view(np.uint32), w_ref.view(np.uint32)), f"rank {rank} {mode}: w mismatch"
             torch.cuda.synchronize()

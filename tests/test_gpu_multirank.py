@@ -29,6 +29,11 @@ def test_two_ranks_bitwise(cid, extra):
     assert "MULTIGPU_OK fold" in out and "MULTIGPU_OK tree" in out
 
 
+def test_two_ranks_momentum_with_mirror():
+    out = _run(2, "--cid", "5", "--S", "300007", "--gamma", "0.9", "--modes", "fold")
+    assert "MULTIGPU_OK fold" in out
+
+
 def test_all_gpus_if_several():
     n = torch.cuda.device_count()
     if n < 4:
