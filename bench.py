@@ -220,9 +220,9 @@ def run_single(a):
         flush_w.zero_()
         flush_r.sum()
 
-    def measure(tau, dtype, steps, warmup, kernel, clocks=False):
+    def measure(tau, dtype, steps, warmup, kernel, clocks=False, gamma=0.0):
         os.environ["MLF_COMMIT_IMPL"] = kernel
-        cfg = configs.config(cid, tau=tau, dtype=dtype)
+        cfg = configs.config(cid, tau=tau, dtype=dtype, gamma=gamma)
         wl = Workload(cfg, device=0)
         wl.fill_updates(0)
         torch.cuda.synchronize()
@@ -246,9 +246,10 @@ def run_single(a):
             wl.after_commit(pd, draws)
             if timed:
                 n_ops = sum(pd["commit_count"])
-                alg = n_ops * wl.shard_elems * cfg["e"] + 2 * wl.shard_elems * 4
+                hist = 2 if gamma else 1                  # momentum adds the history stream
+                alg = n_ops * wl.shard_elems * cfg["e"] + 2 * hist * wl.shard_elems * 4
                 if pd["replica_boundary_commit"] >= 0:
-                    alg += wl.shard_elems * 4
+                    alg += hist * wl.shard_elems * 4
                 recs.append(dict(ms=ms, bytes=committed_bytes(cfg, pd), alg=alg, plan_ms=plan_ms,
                                  commits=pd["n_commit"], groups=pd["n_groups"]))
         if clocks:
@@ -306,6 +307,11 @@ def run_single(a):
             for k in (a.kernel, other):
                 _, r3, T3, _, _ = measure(32, a.dtype, nv, 3, k)
                 var[f"tau32_{k}"] = summarize(r3, T3)
+            # NEXT-1: momentum gamma = 0.9 (Eq. 2 with history), bulk kernel
+            _, r4, T4, _, _ = measure(a.tau, a.dtype, nv, 3, "bulk", gamma=0.9)
+            var["momentum0.9_bulk"] = summarize(r4, T4)
+            _, r5, T5, _, _ = measure(32, a.dtype, nv, 3, "bulk", gamma=0.9)
+            var["momentum0.9_tau32_bulk"] = summarize(r5, T5)
         line["variants"] = var
         os.environ["MLF_COMMIT_IMPL"] = a.kernel
     # e2e through the public API with host buffers
