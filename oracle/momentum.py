@@ -15,8 +15,10 @@ Paper passages:
 Two oracles:
 * sequential_f64 — the plain definition: Eq. 2 per update, in float64.
 * weighted_f32 — the aggregate form in fp32 with a pinned evaluation order (what the
-  commit kernel computes): coefficients from float64 powers pw[j] = pw[j-1]*g summed
-  left to right, rounded once to fp32; per member u_i = -(lr*g_i); A = left fold of
+  commit kernel computes): gamma taken as its fp32 value (reading R21: the model, its
+  history and the momentum parameter are fp32); coefficients from float64 powers
+  pw[j] = pw[j-1]*g summed left to right, rounded once to fp32; per member
+  u_i = -(lr*g_i); A = left fold of
   (cA_i*u_i), B = left fold of (cB_i*u_i); t = s_h*h + A; w' = w + t;
   h' = g_m*h + B; every product / sum rounded to fp32, never fused.
 
@@ -67,6 +69,7 @@ def sequential_f64(w, h, commits: list, lr: float, gamma: float, boundary: int =
 def weighted_f32(w, h, commits: list, lr: float, gamma: float, boundary: int = -1):
     """The aggregate (weighted-sum) form in fp32, pinned order.  Returns (w, h, backup)."""
     f = np.float32
+    gamma = float(np.float32(gamma))      # R21: gamma is an fp32 parameter (the model's dtype)
     w = np.asarray(w, dtype=np.float32).copy()
     h = np.asarray(h, dtype=np.float32).copy()
     lr32 = f(lr)
