@@ -117,6 +117,11 @@ typedef struct {
   const int32_t *carried_node;
   const int64_t *carried_bytes;
   const double *carried_norm;
+  /* 0 = mirror (R16: the frozen prefix is rounded up to a server-commit boundary and the
+   * replica receives w there); 1 = replica trees (NEXT-2: the replica applies
+   * the frozen replica commits — its own Alg. 3 grouping — and exactly the frozen prefix
+   * is frozen, the rest punted) */
+  int32_t replica_mode;
 } mlf_plan_params;
 
 /* Plan outputs.  All arrays are caller-allocated; `capacity` is their length
@@ -141,6 +146,13 @@ typedef struct {
   int32_t *punted;           /* [n_punted] indices into carried ++ order, carried to the next batch */
   uint8_t delayed_last;      /* 1 if the last server commit was delayed to meet Div_max (§5.3) */
   int64_t t_total_ns;        /* model time of the last server commit */
+  /* the frozen replica commits of the tentative replica plan (Alg. 3 toward the replica on
+   * the network after the server plan): runs over carried ++ order */
+  int32_t n_replica_commits;
+  int32_t *replica_commit_first;   /* [n_replica_commits] (capacity n + n_carried) */
+  int32_t *replica_commit_count;
+  int32_t *replica_commit_group;   /* 0 direct to the replica, i >= 1 via replica_agg[i-1] */
+  int64_t replica_bytes;           /* bytes those commits deliver to the replica nodes */
 } mlf_plan_out;
 
 /* Alg. 2 -> Alg. 3 -> §5.3 on one batch.  Pure; may run concurrently. */

@@ -39,6 +39,7 @@ class Params:
     hist_norm: float = 0.0
     carried: list = field(default_factory=list)        # Items (node, size, norm), in order
     shard_weights: list | None = None                  # None = equal weights
+    replica_mode: int = 0                              # 0 mirror (R16), 1 replica trees (NEXT-2)
 
 
 def validate(net: Net, batch: list, prm: Params) -> list:
@@ -55,6 +56,8 @@ def validate(net: Net, batch: list, prm: Params) -> list:
         raise PlanError(E_INVALID, "no server")
     if prm.replicas and len(prm.replicas) != len(prm.servers):
         raise PlanError(E_INVALID, "replica count must equal server count")
+    if prm.replica_mode not in (0, 1):
+        raise PlanError(E_INVALID, "replica_mode")
     if prm.tau_max < 0 or not (prm.div_max >= 0) or not (0.0 <= prm.gamma < 1.0):
         raise PlanError(E_INVALID, "tau_max / div_max / gamma")
     if not (prm.hist_norm >= 0 and math.isfinite(prm.hist_norm)):
@@ -108,11 +111,19 @@ def plan(net: Net, batch: list, prm: Params) -> dict:
         "commit_count": commit_count, "commit_t_ns": list(times),
         "replica_frozen": 0, "replica_boundary_commit": -1, "n_punted": 0, "punted": [],
         "delayed_last": 0, "t_total_ns": times[-1] if times else 0,
+        "n_replica_commits": 0, "replica_commit_first": [], "replica_commit_count": [],
+        "replica_commit_group": [], "replica_bytes": 0,
     }
     # 3. replication (§5.3) on the network after the server plan's reservations
     if prm.replicas:
         rres = plan_replication(case.commits, times, prm.carried, ordered_items, case.net,
-                                prm.replicas, w, prm.raggs, prm.div_max, prm.gamma, prm.hist_norm)
+                                prm.replicas, w, prm.raggs, prm.div_max, prm.gamma, prm.hist_norm,
+                                mode="trees" if prm.replica_mode == 1 else "mirror")
+        out["n_replica_commits"] = len(rres.commits)
+        out["replica_commit_first"] = [c[0] for c in rres.commits]
+        out["replica_commit_count"] = [c[1] for c in rres.commits]
+        out["replica_commit_group"] = [c[2] for c in rres.commits]
+        out["replica_bytes"] = rres.replica_bytes
         out["replica_frozen"] = rres.frozen
         out["replica_boundary_commit"] = rres.boundary
         out["punted"] = rres.punted

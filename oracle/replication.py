@@ -75,13 +75,20 @@ class ReplicaResult:
     plan_frozen: int = 0            # frozen prefix before rounding up to a boundary
     bound: float = 0.0              # divergence bound at T_last for the plan's frozen prefix
     replica_case: object = None
+    commits: list = field(default_factory=list)  # frozen replica commits: (first, count, group)
+    replica_bytes: int = 0          # bytes the frozen replica commits deliver to the replica
 
 
 def plan_replication(server_commits: list, server_times: list, carried: list, ordered: list,
                      net_after, replicas, weights, raggs, div_max: float, gamma: float,
-                     hist_norm: float) -> ReplicaResult:
+                     hist_norm: float, mode: str = "mirror") -> ReplicaResult:
     """§5.3 on the tentative server plan.  `server_commits` are aggregation.Commit
-    objects over positions of `ordered`; `server_times` their chained commit times."""
+    objects over positions of `ordered`; `server_times` their chained commit times.
+
+    mode "mirror" (R16): the frozen prefix is rounded up to a server-commit boundary and
+    realised as a mirror store of w.  mode "trees" (NEXT-2): the replica
+    applies the frozen replica commits themselves — its own Alg. 3 grouping — and exactly
+    the plan's frozen prefix is frozen; the rest is punted."""
     items = list(carried) + list(ordered)
     n_c = len(carried)
     rcase = plan_aggregation(items, net_after, replicas, weights, raggs)
@@ -96,6 +103,7 @@ def plan_replication(server_commits: list, server_times: list, carried: list, or
     while n_pre < len(rtimes) and rtimes[n_pre] <= t_last:
         n_pre += 1
     frozen = ends[n_pre - 1] if n_pre else 0
+    n_fc = n_pre                                    # frozen replica commits
     norms = [it.norm for it in items]
     bound = divergence_bound(norms[frozen:], gamma, hist_norm)
     delayed = False
@@ -107,6 +115,7 @@ def plan_replication(server_commits: list, server_times: list, carried: list, or
                 break
         assert a_e is not None, "the full prefix has bound 0 <= div_max"
         frozen = ends[a_e]
+        n_fc = a_e + 1
         bound = divergence_bound(norms[frozen:], gamma, hist_norm)
         if server_commits:
             delayed = True
@@ -115,6 +124,15 @@ def plan_replication(server_commits: list, server_times: list, carried: list, or
             new_end = last.t_en + shift
             prev = server_times[-2] if len(server_times) > 1 else 0
             t_last = max(prev, new_end)
+
+    rcommits, rbytes, pos = [], 0, 0
+    for c in rcase.commits[:n_fc]:
+        rcommits.append((pos, len(c.members), c.group))
+        rbytes += max(items[p].size for p in c.members)    # a direct item, or one aggregate
+        pos += len(c.members)
+    if mode == "trees":
+        punted = list(range(frozen, len(items)))
+        return ReplicaResult(frozen, -1, punted, delayed, t_last, frozen, bound, rcase, rcommits, rbytes)
 
     # R16 mirror boundary
     f_o = max(0, frozen - n_c)
@@ -131,4 +149,4 @@ def plan_replication(server_commits: list, server_times: list, carried: list, or
                 break
         covered = n_c + acc
     punted = list(range(covered, len(items)))
-    return ReplicaResult(covered, boundary, punted, delayed, t_last, frozen, bound, rcase)
+    return ReplicaResult(covered, boundary, punted, delayed, t_last, frozen, bound, rcase, rcommits, rbytes)

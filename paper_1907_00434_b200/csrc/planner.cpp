@@ -732,6 +732,7 @@ static mlf_status plan_impl(const mlf_net *net, const mlf_batch *batch, const ml
     if (!node_ok(prm->replica_agg[i])) throw PlanFail{MLF_E_INVALID, "replica aggregator out of range"};
     c.raggs.push_back(prm->replica_agg[i]);
   }
+  if (prm->replica_mode != 0 && prm->replica_mode != 1) throw PlanFail{MLF_E_INVALID, "replica_mode"};
   if (prm->tau_max < 0 || !(prm->div_max >= 0) || !(prm->gamma >= 0.0 && prm->gamma < 1.0))
     throw PlanFail{MLF_E_INVALID, "tau_max / div_max / gamma"};
   if (!(prm->hist_norm >= 0 && std::isfinite(prm->hist_norm))) throw PlanFail{MLF_E_INVALID, "hist_norm"};
@@ -759,7 +760,9 @@ static mlf_status plan_impl(const mlf_net *net, const mlf_batch *batch, const ml
   if (out->capacity < n + prm->n_carried ||
       (n > 0 && (!out->order || !out->drop_reason || !out->group || !out->commit_first || !out->commit_count ||
                  !out->commit_t_ns)) ||
-      ((n + prm->n_carried) > 0 && !out->punted) || (n > 0 && prm->k > 0 && !out->group_node))
+      ((n + prm->n_carried) > 0 && !out->punted) || (n > 0 && prm->k > 0 && !out->group_node) ||
+      (prm->n_replicas > 0 && (n + prm->n_carried) > 0 &&
+       (!out->replica_commit_first || !out->replica_commit_count || !out->replica_commit_group)))
     throw PlanFail{MLF_E_CAPACITY, "output arrays too small or missing"};
   // unschedulable pre-check (R9)
   std::vector<i64> comp;
@@ -812,6 +815,8 @@ static mlf_status plan_impl(const mlf_net *net, const mlf_batch *batch, const ml
   out->replica_frozen = 0;
   out->replica_boundary_commit = -1;
   out->n_punted = 0;
+  out->n_replica_commits = 0;
+  out->replica_bytes = 0;
   out->delayed_last = 0;
   out->t_total_ns = times.empty() ? 0 : times.back();
 
@@ -832,6 +837,7 @@ static mlf_status plan_impl(const mlf_net *net, const mlf_batch *batch, const ml
     size_t n_pre = 0;
     while (n_pre < rtimes.size() && rtimes[n_pre] <= t_last) ++n_pre;
     int frozen = n_pre ? ends[n_pre - 1] : 0;
+    size_t n_fc = n_pre;                                     // frozen replica commits
     std::vector<double> norms;
     for (auto &it : ritems) norms.push_back(it.norm);
     const int R = (int)ritems.size();
@@ -847,6 +853,7 @@ static mlf_status plan_impl(const mlf_net *net, const mlf_batch *batch, const ml
       }
       if (a_e < 0) throw PlanFail{MLF_E_INVALID, "internal: no replica commit meets Div_max"};
       frozen = ends[a_e];
+      n_fc = (size_t)a_e + 1;
       if (!cs.commits.empty()) {
         delayed = true;
         const Send &last = cs.commits.back().send;
@@ -856,9 +863,25 @@ static mlf_status plan_impl(const mlf_net *net, const mlf_batch *batch, const ml
         t_last = std::max(prev, new_end);
       }
     }
-    // R16 mirror boundary
+    // the frozen replica commits and the bytes they deliver (a direct item or one aggregate)
+    int64_t rbytes = 0;
+    for (size_t ci = 0; ci < n_fc; ++ci) {
+      const CommitRec &x = rc.commits[ci];
+      out->replica_commit_first[ci] = x.first;
+      out->replica_commit_count[ci] = x.count;
+      out->replica_commit_group[ci] = x.group;
+      i64 mx = 0;
+      for (int q = x.first; q < x.first + x.count; ++q) mx = std::max(mx, ritems[q].size);
+      rbytes += mx;
+    }
+    out->n_replica_commits = (int)n_fc;
+    out->replica_bytes = rbytes;
+    // R16 mirror boundary (mode 0); replica trees (mode 1): exactly the frozen prefix
     int f_o = std::max(0, frozen - n_c), boundary, covered;
-    if (frozen == 0) {
+    if (prm->replica_mode == 1) {
+      boundary = -1;
+      covered = frozen;
+    } else if (frozen == 0) {
       boundary = -1;
       covered = 0;
     } else if (f_o == 0) {

@@ -61,7 +61,7 @@ class MlfPlanParams(C.Structure):
                 ("v_init", C.c_int64), ("tau_max", C.c_int32),
                 ("div_max", C.c_double), ("gamma", C.c_double), ("hist_norm", C.c_double),
                 ("n_carried", C.c_int32), ("carried_node", _i32p), ("carried_bytes", _i64p),
-                ("carried_norm", _f64p)]
+                ("carried_norm", _f64p), ("replica_mode", C.c_int32)]
 
 
 class MlfPlanOut(C.Structure):
@@ -70,7 +70,9 @@ class MlfPlanOut(C.Structure):
                 ("n_server_commits", C.c_int32), ("commit_first", _i32p), ("commit_count", _i32p),
                 ("commit_t_ns", _i64p), ("replica_frozen", C.c_int32), ("replica_boundary_commit", C.c_int32),
                 ("n_punted", C.c_int32), ("punted", _i32p), ("delayed_last", C.c_uint8),
-                ("t_total_ns", C.c_int64)]
+                ("t_total_ns", C.c_int64), ("n_replica_commits", C.c_int32),
+                ("replica_commit_first", _i32p), ("replica_commit_count", _i32p),
+                ("replica_commit_group", _i32p), ("replica_bytes", C.c_int64)]
 
 
 class MlfConfig(C.Structure):
@@ -137,7 +139,8 @@ def _ptr(a: np.ndarray | None, ct):
 
 # ----------------------------------------------------------------- planning
 def plan(n_nodes, nic_up, nic_down, batch, servers, *, bw=None, site=None, aggs=(), replicas=(), raggs=(),
-         v_init=0, tau_max=1, div_max=math.inf, gamma=0.0, hist_norm=0.0, carried=(), shard_weights=None) -> dict:
+         v_init=0, tau_max=1, div_max=math.inf, gamma=0.0, hist_norm=0.0, carried=(), shard_weights=None,
+         replica_mode=0) -> dict:
     """mlf_plan.  `batch` = list of dicts (node, size, version, t_avail, norm) or a dict of arrays;
     `carried` = list of dicts (node, size, norm).  Returns the plan as a dict of Python lists."""
     keep = []
@@ -170,7 +173,7 @@ def plan(n_nodes, nic_up, nic_down, batch, servers, *, bw=None, site=None, aggs=
     prm = MlfPlanParams(len(sv), _ptr(sv, C.c_int32), _ptr(sw, C.c_int64), len(ag), _ptr(ag, C.c_int32),
                         len(rp), _ptr(rp, C.c_int32), len(ra), _ptr(ra, C.c_int32), int(v_init), int(tau_max),
                         float(div_max), float(gamma), float(hist_norm), len(cn), _ptr(cn, C.c_int32),
-                        _ptr(cb, C.c_int64), _ptr(cm, C.c_double))
+                        _ptr(cb, C.c_int64), _ptr(cm, C.c_double), int(replica_mode))
     return plan_raw(net, b, prm, n + len(cn), keep)
 
 
@@ -188,6 +191,9 @@ class PlanBuffers:
         self.ccount = np.zeros(cap, np.int32)
         self.ct = np.zeros(cap, np.int64)
         self.punted = np.zeros(cap, np.int32)
+        self.rfirst = np.zeros(cap, np.int32)
+        self.rcount = np.zeros(cap, np.int32)
+        self.rgroup = np.zeros(cap, np.int32)
         self.out = MlfPlanOut()
         o = self.out
         o.capacity = cap
@@ -195,6 +201,8 @@ class PlanBuffers:
         o.group_node = _ptr(self.group_node, C.c_int32)
         o.commit_first, o.commit_count = _ptr(self.cfirst, C.c_int32), _ptr(self.ccount, C.c_int32)
         o.commit_t_ns, o.punted = _ptr(self.ct, C.c_int64), _ptr(self.punted, C.c_int32)
+        o.replica_commit_first, o.replica_commit_count = _ptr(self.rfirst, C.c_int32), _ptr(self.rcount, C.c_int32)
+        o.replica_commit_group = _ptr(self.rgroup, C.c_int32)
 
     def to_dict(self, n: int) -> dict:
         o = self.out
@@ -208,6 +216,11 @@ class PlanBuffers:
             "replica_frozen": o.replica_frozen, "replica_boundary_commit": o.replica_boundary_commit,
             "n_punted": o.n_punted, "punted": self.punted[:o.n_punted].tolist(),
             "delayed_last": int(o.delayed_last), "t_total_ns": o.t_total_ns,
+            "n_replica_commits": o.n_replica_commits,
+            "replica_commit_first": self.rfirst[:o.n_replica_commits].tolist(),
+            "replica_commit_count": self.rcount[:o.n_replica_commits].tolist(),
+            "replica_commit_group": self.rgroup[:o.n_replica_commits].tolist(),
+            "replica_bytes": o.replica_bytes,
         }
 
 
@@ -238,6 +251,12 @@ def plan_from_dict(d: dict) -> MlfPlanOut:
     o.n_punted = d.get("n_punted", 0)
     o.delayed_last = d.get("delayed_last", 0)
     o.t_total_ns = d.get("t_total_ns", 0)
+    rf = d.get("replica_commit_first", [])
+    o.n_replica_commits = len(rf)
+    b.rfirst[:len(rf)] = rf
+    b.rcount[:len(rf)] = d.get("replica_commit_count", [])
+    b.rgroup[:len(rf)] = d.get("replica_commit_group", [0] * len(rf))
+    o.replica_bytes = d.get("replica_bytes", 0)
     return b
 
 
@@ -349,7 +368,7 @@ def make_net(n_nodes, nic_up, nic_down, bw=None, site=None):
 
 
 def make_params(servers, *, aggs=(), replicas=(), raggs=(), v_init=0, tau_max=1, div_max=math.inf, gamma=0.0,
-                hist_norm=0.0, carried=(), shard_weights=None):
+                hist_norm=0.0, carried=(), shard_weights=None, replica_mode=0):
     """(MlfPlanParams, keep-alive arrays)."""
     sv, ag = _arr(servers, np.int32), _arr(list(aggs), np.int32)
     rp, ra = _arr(list(replicas), np.int32), _arr(list(raggs), np.int32)
@@ -360,7 +379,7 @@ def make_params(servers, *, aggs=(), replicas=(), raggs=(), v_init=0, tau_max=1,
     prm = MlfPlanParams(len(sv), _ptr(sv, C.c_int32), _ptr(sw, C.c_int64), len(ag), _ptr(ag, C.c_int32),
                         len(rp), _ptr(rp, C.c_int32), len(ra), _ptr(ra, C.c_int32), int(v_init), int(tau_max),
                         float(div_max), float(gamma), float(hist_norm), len(cn), _ptr(cn, C.c_int32),
-                        _ptr(cb, C.c_int64), _ptr(cm, C.c_double))
+                        _ptr(cb, C.c_int64), _ptr(cm, C.c_double), int(replica_mode))
     return prm, (sv, ag, rp, ra, sw, cn, cb, cm)
 
 

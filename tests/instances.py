@@ -32,6 +32,7 @@ class Instance:
     hist_norm: float
     carried: list = field(default_factory=list)    # dicts: node, size, norm
     shard_weights: list | None = None
+    replica_mode: int = 0
 
 
 def random_instance(seed: int, idx: int, max_n: int = 8, max_servers: int = 2,
@@ -107,7 +108,7 @@ def random_instance(seed: int, idx: int, max_n: int = 8, max_servers: int = 2,
     if G > 1 and ri(0, 1):
         weights = [ri(1, 9) for _ in range(G)]
     return Instance(n_nodes, nic_up, nic_down, bw, site, batch, servers, aggs, replicas, raggs,
-                    v_init, tau, div_max, gamma, hist, carried, weights)
+                    v_init, tau, div_max, gamma, hist, carried, weights, replica_mode=ri(0, 1))
 
 
 def to_oracle(inst: Instance):
@@ -118,5 +119,6 @@ def to_oracle(inst: Instance):
     carried = [Item(c["node"], c["size"], 0, 0, c["norm"]) for c in inst.carried]
     prm = Params(servers=inst.servers, aggs=inst.aggs, replicas=inst.replicas, raggs=inst.raggs,
                  v_init=inst.v_init, tau_max=inst.tau_max, div_max=inst.div_max, gamma=inst.gamma,
-                 hist_norm=inst.hist_norm, carried=carried, shard_weights=inst.shard_weights)
+                 hist_norm=inst.hist_norm, carried=carried, shard_weights=inst.shard_weights,
+                 replica_mode=inst.replica_mode)
     return net, batch, prm

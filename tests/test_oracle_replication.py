@@ -75,8 +75,27 @@ def _replica_instances(n, seed):
     return out
 
 
+def test_replica_trees_mode_freezes_exactly_the_replica_commits():
+    for inst in _replica_instances(150, 777):
+        inst.replica_mode = 1
+        net, batch, prm = to_oracle(inst)
+        p = plan(net, batch, prm)
+        total = len(inst.carried) + p["n_commit"]
+        assert p["replica_boundary_commit"] == -1
+        assert p["replica_frozen"] == sum(p["replica_commit_count"])
+        assert p["replica_commit_first"] == [sum(p["replica_commit_count"][:i])
+                                             for i in range(p["n_replica_commits"])]
+        assert p["punted"] == list(range(p["replica_frozen"], total))
+        # the same plan in mirror mode freezes a superset (rounded up to a server commit)
+        inst.replica_mode = 0
+        pm = plan(*to_oracle(inst))
+        assert pm["replica_frozen"] >= p["replica_frozen"]
+        assert pm["order"] == p["order"] and pm["replica_bytes"] == p["replica_bytes"]
+
+
 def test_divmax_limits_and_mirror_consistency():
     for inst in _replica_instances(150, 4242):
+        inst.replica_mode = 0
         # Div_max = inf: the bound never binds, so no server delay
         inst.div_max = math.inf
         net, batch, prm = to_oracle(inst)
