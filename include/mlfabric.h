@@ -197,6 +197,17 @@ typedef struct {
   float gamma;
   float *history_shard;
   float *backup_history;
+  /* Replica trees (NEXT-2; plans with replica_mode = 1): backup_shard is the
+   * replica's model shard and mlf_execute applies the plan's frozen replica commits to it
+   * (its own grouping, O(U) order).  Updates punted to the next batch are retained: the
+   * rank that hosts a punted update copies it into a free slot of its retention pool
+   * (slot chosen deterministically, identically on every rank) and the next batch reads it
+   * from there as a carried item; the caller must pass the previous plan's punted items, in
+   * order, as the next plan's carried items.  retain_slot = [world * n_retain] full-length
+   * update buffers (update dtype), local or mapped peer pointers. */
+  int32_t replica_mode;
+  int32_t n_retain;
+  void *const *retain_slot;
 } mlf_config;
 
 typedef struct mlf_ctx mlf_ctx;

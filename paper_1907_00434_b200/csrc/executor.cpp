@@ -80,6 +80,11 @@ struct mlf_ctx {
   cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
   cudaEvent_t ev_phase = nullptr;                 // interprocess "phase 1 done" (world > 1)
   std::vector<cudaEvent_t> peer_events;           // opened peers' phase events
+  // replica trees (NEXT-2): retention pool and the carried items' slots, in carried order
+  std::vector<void *> retain;                     // [world * n_retain]
+  std::vector<std::vector<uint8_t>> used;         // [world][n_retain]
+  std::vector<std::pair<int, int>> carried;       // (rank, slot)
+  int64_t retained_bytes = 0;
   bool started = false, pending = false, sticky = false, phase1_done = false;
   int64_t launches = 0, h2d = 0, d2h = 0;
   CommitImpl impl = CommitImpl::kLdg;
@@ -104,6 +109,15 @@ extern "C" mlf_status mlf_init(const mlf_config *cfg, int64_t v0, mlf_ctx **out)
     if (k.shard_elems > 0 && !k.model_shard) throw Fail{MLF_E_INVALID, "model shard"};
     if (k.agg_slots < 0 || (k.agg_slots > 0 && !k.agg_scratch)) throw Fail{MLF_E_INVALID, "aggregate scratch"};
     if (!(k.gamma >= 0.f && k.gamma < 1.f)) throw Fail{MLF_E_INVALID, "gamma must be in [0, 1)"};
+    if (k.replica_mode != 0 && k.replica_mode != 1) throw Fail{MLF_E_INVALID, "replica_mode"};
+    if (k.replica_mode == 1) {
+      if (k.shard_elems > 0 && !k.backup_shard) throw Fail{MLF_E_INVALID, "replica trees need the replica shard"};
+      if (k.gamma != 0.f) throw Fail{MLF_E_INVALID, "replica trees are implemented for gamma = 0"};
+      if (k.n_retain < 0 || (k.n_retain > 0 && !k.retain_slot)) throw Fail{MLF_E_INVALID, "retention pool"};
+      for (int i = 0; i < k.world * k.n_retain; ++i)
+        if (!k.retain_slot[i] || (reinterpret_cast<uintptr_t>(k.retain_slot[i]) & 15))
+          throw Fail{MLF_E_INVALID, "retention slot null or not 16-byte aligned"};
+    }
     if (k.gamma != 0.f) {
       if (k.shard_elems > 0 && !k.history_shard) throw Fail{MLF_E_INVALID, "momentum needs history_shard"};
       if (k.backup_shard && !k.backup_history) throw Fail{MLF_E_INVALID, "momentum mirror needs backup_history"};
@@ -154,6 +168,10 @@ extern "C" mlf_status mlf_init(const mlf_config *cfg, int64_t v0, mlf_ctx **out)
       c->node_rank.push_back(r);
     }
     for (int i = 0; i < k.world * k.agg_slots; ++i) c->agg_scratch.push_back(k.agg_scratch[i]);
+    if (k.replica_mode == 1) {
+      for (int i = 0; i < k.world * k.n_retain; ++i) c->retain.push_back(k.retain_slot[i]);
+      c->used.assign(k.world, std::vector<uint8_t>(k.n_retain, 0));
+    }
     c->in_batch.assign(k.n_workers, 0);
     c->in_flight.assign(k.n_workers, 0);
     c->host_src.assign(k.n_workers, nullptr);
@@ -283,6 +301,21 @@ static void validate_plan(const mlf_ctx *c, const mlf_plan_out *p) {
     throw Fail{MLF_E_INVALID, "replica boundary out of range"};
   if (p->replica_boundary_commit >= 0 && !c->cfg.backup_shard)
     throw Fail{MLF_E_INVALID, "plan writes the replica but the context has no backup shard"};
+  if (c->cfg.replica_mode == 1) {
+    // the plan must be a replica-trees plan over this context's carried items
+    const int n_c = p->replica_frozen + p->n_punted - p->n_commit;
+    if (p->replica_boundary_commit != -1 || n_c != (int)c->carried.size())
+      throw Fail{MLF_E_INVALID, "plan is not a replica-trees plan over the carried items"};
+    if (p->n_replica_commits < 0 || (p->n_replica_commits > 0 && (!p->replica_commit_first || !p->replica_commit_count)))
+      throw Fail{MLF_E_INVALID, "replica commits"};
+    int rpos = 0;
+    for (int ci = 0; ci < p->n_replica_commits; ++ci) {
+      if (p->replica_commit_first[ci] != rpos || p->replica_commit_count[ci] < 1)
+        throw Fail{MLF_E_INVALID, "replica commit runs not contiguous"};
+      rpos += p->replica_commit_count[ci];
+    }
+    if (rpos != p->replica_frozen) throw Fail{MLF_E_INVALID, "replica commits do not cover the frozen prefix"};
+  }
 }
 
 static bool tree_mode(const mlf_ctx *c) { return c->cfg.world > 1 && c->cfg.agg_slots > 0; }
@@ -414,6 +447,88 @@ static void launch_momentum(mlf_ctx *c, const mlf_plan_out *p, const std::vector
   }
 }
 
+// The fused commit pass of `ops` (commit order) over w (this rank's slice, src_off =
+// shard_begin), launches split at commit boundaries when the list exceeds kMaxOps.
+static void launch_ops(mlf_ctx *c, float *w, float *backup, const std::vector<CommitOp> &ops, int boundary) {
+  size_t i0 = 0;
+  bool first_launch = true;
+  while (i0 < ops.size() || (first_launch && c->cfg.shard_elems > 0 && (boundary == 0))) {
+    size_t i1 = std::min(ops.size(), i0 + (size_t)kMaxOps);
+    if (i1 < ops.size())
+      while (i1 > i0 && !(ops[i1 - 1].flag & kOpLast)) --i1;
+    if (i1 == i0 && i0 < ops.size()) throw Fail{MLF_E_CAPACITY, "a single commit has more than kMaxOps members"};
+    CommitArgs a;
+    a.w = w;
+    a.backup = backup;
+    a.n = c->cfg.shard_elems;
+    a.src_off = c->cfg.shard_begin;
+    a.lr = c->cfg.lr;
+    a.n_ops = (int32_t)(i1 - i0);
+    a.backup_after = -2;
+    if (first_launch && boundary == 0) a.backup_after = -1;
+    for (size_t q = i0; q < i1; ++q) {
+      a.op[q - i0] = ops[q].ptr;
+      a.flag[q - i0] = ops[q].flag;
+      if (boundary > 0 && ops[q].commit == boundary && (ops[q].flag & kOpLast)) a.backup_after = (int32_t)(q - i0);
+    }
+    if (a.n > 0) {
+      record_start(c);   // as late as possible: the window brackets device work only
+      CK(launch_commit(a, c->stream, c->sm_count, c->impl));
+      ++c->launches;
+    }
+    first_launch = false;
+    i0 = i1;
+    if (ops.empty()) break;
+  }
+}
+
+// Replica trees (NEXT-2): apply the frozen replica commits (the replica's own Alg. 3
+// grouping over carried ++ order) to the replica shard, then retain the punted updates.
+static void replicate_trees(mlf_ctx *c, const mlf_plan_out *p) {
+  const int n_c = (int)c->carried.size();
+  const uint8_t dflag = c->cfg.update_dtype == MLF_BF16 ? kOpBf16 : 0;
+  auto item_ptr = [&](int i) -> void * {
+    if (i < n_c) return c->retain[(size_t)c->carried[i].first * c->cfg.n_retain + c->carried[i].second];
+    return c->slot[c->b_worker[p->order[i - n_c]]];
+  };
+  std::vector<CommitOp> rops;
+  for (int ci = 0; ci < p->n_replica_commits; ++ci) {
+    const int f = p->replica_commit_first[ci], k = p->replica_commit_count[ci];
+    for (int q = 0; q < k; ++q) {
+      uint8_t fl = dflag;
+      if (q == 0) fl |= kOpFirst;
+      if (q == k - 1) fl |= kOpLast;
+      rops.push_back({item_ptr(f + q), fl, ci + 1});
+    }
+  }
+  if (!rops.empty()) launch_ops(c, c->cfg.backup_shard, nullptr, rops, -1);
+  // retention: punted items stay readable for the next batch (the worker "retains" its
+  // update until the replica has it)
+  const size_t bytes = (size_t)c->cfg.model_elems * c->elem_bytes;
+  std::vector<std::pair<int, int>> next;
+  for (int i = 0; i < p->replica_frozen && i < n_c; ++i) c->used[c->carried[i].first][c->carried[i].second] = 0;
+  for (int i = p->replica_frozen; i < n_c + p->n_commit; ++i) {
+    if (i < n_c) {
+      next.push_back(c->carried[i]);
+      continue;
+    }
+    const int w = c->b_worker[p->order[i - n_c]];
+    const int r = c->worker_rank[w];
+    int s = 0;
+    while (s < c->cfg.n_retain && c->used[r][s]) ++s;
+    if (s == c->cfg.n_retain) throw Fail{MLF_E_CAPACITY, "retention pool exhausted (punted updates)"};
+    c->used[r][s] = 1;
+    next.push_back({r, s});
+    if (r == c->cfg.rank) {
+      record_start(c);
+      CK(cudaMemcpyAsync(c->retain[(size_t)r * c->cfg.n_retain + s], c->slot[w], bytes, cudaMemcpyDeviceToDevice,
+                         c->stream));
+      c->retained_bytes += (int64_t)bytes;
+    }
+  }
+  c->carried.swap(next);
+}
+
 static void phase_commit(mlf_ctx *c, const mlf_plan_out *p) {
   CK(cudaSetDevice(c->cfg.device));
   // aggregates / staged updates of the other ranks are complete (phase events)
@@ -438,42 +553,13 @@ static void phase_commit(mlf_ctx *c, const mlf_plan_out *p) {
       ops.push_back({c->slot[c->b_worker[p->order[first + q]]], f, ci + 1});
     }
   }
-  const int boundary = c->cfg.backup_shard ? p->replica_boundary_commit : -1;
-  if (c->cfg.gamma != 0.f) {
+  const bool trees = c->cfg.replica_mode == 1;
+  const int boundary = (c->cfg.backup_shard && !trees) ? p->replica_boundary_commit : -1;
+  if (c->cfg.gamma != 0.f)
     launch_momentum(c, p, ops, boundary);
-  } else {
-  // launches, split at commit boundaries when the list exceeds kMaxOps
-  size_t i0 = 0;
-  bool first_launch = true;
-  while (i0 < ops.size() || (first_launch && c->cfg.shard_elems > 0 && (boundary == 0))) {
-    size_t i1 = std::min(ops.size(), i0 + (size_t)kMaxOps);
-    if (i1 < ops.size())
-      while (i1 > i0 && !(ops[i1 - 1].flag & kOpLast)) --i1;
-    if (i1 == i0 && i0 < ops.size()) throw Fail{MLF_E_CAPACITY, "a single commit has more than kMaxOps members"};
-    CommitArgs a;
-    a.w = c->cfg.model_shard;
-    a.backup = c->cfg.backup_shard;
-    a.n = c->cfg.shard_elems;
-    a.src_off = c->cfg.shard_begin;
-    a.lr = c->cfg.lr;
-    a.n_ops = (int32_t)(i1 - i0);
-    a.backup_after = -2;
-    if (first_launch && boundary == 0) a.backup_after = -1;
-    for (size_t q = i0; q < i1; ++q) {
-      a.op[q - i0] = ops[q].ptr;
-      a.flag[q - i0] = ops[q].flag;
-      if (boundary > 0 && ops[q].commit == boundary && (ops[q].flag & kOpLast)) a.backup_after = (int32_t)(q - i0);
-    }
-    if (a.n > 0) {
-      record_start(c);   // as late as possible: the window brackets device work only
-      CK(launch_commit(a, c->stream, c->sm_count, c->impl));
-      ++c->launches;
-    }
-    first_launch = false;
-    i0 = i1;
-    if (ops.empty()) break;
-  }
-  }
+  else
+    launch_ops(c, c->cfg.model_shard, trees ? nullptr : c->cfg.backup_shard, ops, boundary);
+  if (trees) replicate_trees(c, p);
   record_start(c);
   CK(cudaEventRecord(c->ev_stop, c->stream));
   c->started = false;

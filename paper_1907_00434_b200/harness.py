@@ -22,7 +22,7 @@ class Workload:
 
     def __init__(self, cfg: dict, *, device: int = 0, rank: int = 0, world: int = 1, variant: int = 0,
                  peer_slots=None, backup_ptr=None, agg_slots: int = 0, agg_scratch=None, stream=None,
-                 slot_tensors: dict | None = None, backup_h_ptr=None):
+                 slot_tensors: dict | None = None, backup_h_ptr=None, retain_table=None):
         self.cfg = cfg
         self.device, self.rank, self.world = device, rank, world
         self.variant = variant
@@ -53,14 +53,26 @@ class Workload:
             else:
                 slot_ptrs.append(peer_slots[w])
         bptr = backup_ptr if backup_ptr is not None else (self.backup.data_ptr() if self.backup is not None else None)
+        # replica trees (NEXT-2): the backup is the replica's own model (starts equal to w0) and
+        # punted updates are retained in a pool until the replica has them
+        self.replica_mode = cfg.get("replica_mode", 0) if cfg["replica"] else 0
+        self.retain = None
+        if self.replica_mode == 1 and retain_table is None:
+            n_ret = cfg.get("n_retain", cfg["W"])
+            self.retain = torch.empty((n_ret, -(-self.S // 64) * 64), dtype=tdt, device=dev)
+            retain_table = [self.retain[i].data_ptr() for i in range(n_ret)]
         self.fill_w0()
+        if self.replica_mode == 1 and self.backup is not None:
+            m.synth_fill(device, self.backup.data_ptr(), n, elem_offset=b, dtype=m.MLF_F32, seed=cfg["seed"],
+                         kind=KIND_W0, variant=variant, stream=self.stream.cuda_stream)
         self.ctx = m.Context(device=device, model_shard=self.w, update_slots=slot_ptrs, lr=cfg["lr"],
                              model_elems=self.S, shard_begin=b, rank=rank, world=world, dtype=self.dt,
                              backup_shard=bptr, worker_rank=cfg["home"], node_rank=cfg["node_rank"],
                              n_nodes=cfg["n_nodes"], agg_slots=agg_slots, agg_scratch=agg_scratch,
                              stream=self.stream.cuda_stream, v0=0, worker_node=cfg["worker_node"],
                              gamma=self.gamma, history=self.h,
-                             backup_history=(backup_h_ptr if backup_h_ptr is not None else self.backup_h))
+                             backup_history=(backup_h_ptr if backup_h_ptr is not None else self.backup_h),
+                             replica_mode=self.replica_mode, retain_slots=retain_table)
         self.v_init, self.v_prev = 0, 0
         self.iteration = 0
         self.carried = []
@@ -86,7 +98,7 @@ class Workload:
         prm, k2 = m.make_params(c["servers"], aggs=c["aggs"], replicas=c["replicas"], raggs=c["raggs"],
                                 v_init=self.v_init, tau_max=c["tau"], div_max=c["div_max"],
                                 gamma=c.get("gamma", 0.0), hist_norm=0.0, carried=self.carried,
-                                shard_weights=weights)
+                                shard_weights=weights, replica_mode=self.replica_mode)
         return net, prm, (k1, k2)
 
     def submit_all(self, iteration: int):

@@ -82,7 +82,8 @@ class MlfConfig(C.Structure):
                 ("model_shard", _p), ("backup_shard", _p), ("update_slot", C.POINTER(_p)),
                 ("worker_rank", _i32p), ("n_nodes", C.c_int32), ("node_rank", _i32p),
                 ("worker_node", _i32p), ("agg_slots", C.c_int32), ("agg_scratch", C.POINTER(_p)),
-                ("stream", _p), ("gamma", C.c_float), ("history_shard", _p), ("backup_history", _p)]
+                ("stream", _p), ("gamma", C.c_float), ("history_shard", _p), ("backup_history", _p),
+                ("replica_mode", C.c_int32), ("n_retain", C.c_int32), ("retain_slot", C.POINTER(_p))]
 
 
 class MlfIpcHandle(C.Structure):
@@ -268,7 +269,7 @@ class Context:
                  shard_begin: int = 0, rank: int = 0, world: int = 1, dtype: int = MLF_F32,
                  backup_shard=None, worker_rank=None, node_rank=None, n_nodes=None, agg_slots: int = 0,
                  agg_scratch=None, stream=None, v0: int = 0, worker_node=None, gamma: float = 0.0,
-                 history=None, backup_history=None):
+                 history=None, backup_history=None, replica_mode: int = 0, retain_slots=None):
         """update_slots: list of int device pointers (or torch tensors); model_shard/backup_shard:
         torch tensors or int pointers; stream: int cudaStream_t (None -> default stream)."""
         def ptr(x):
@@ -288,7 +289,12 @@ class Context:
                              self.n_workers, dtype, float(lr), ptr(model_shard), ptr(backup_shard), self._slots,
                              _ptr(self._wr, C.c_int32), int(nn), _ptr(self._nr, C.c_int32),
                              _ptr(self._wn, C.c_int32), int(agg_slots), self._scr, stream, float(gamma),
-                             ptr(history), ptr(backup_history))
+                             ptr(history), ptr(backup_history), int(replica_mode), 0, None)
+        ret = [ptr(s) for s in (retain_slots or [])]
+        self._ret = (_p * max(len(ret), 1))(*ret)
+        if ret:
+            self.cfg.n_retain = len(ret) // int(world)
+            self.cfg.retain_slot = self._ret
         self._h = _p()
         _check(_lib.mlf_init(C.byref(self.cfg), int(v0), C.byref(self._h)))
         self._bufs = None

@@ -35,7 +35,19 @@ def shard_bounds(S: int, G: int, align: int = 64):
 
 
 def config(cid: int, *, G: int | None = None, tau: int | None = None, dtype: str = "f32",
-           seed: int = SEED_ROOT, scale_S: int | None = None, gamma: float = 0.0) -> dict:
+           seed: int = SEED_ROOT, scale_S: int | None = None, gamma: float = 0.0,
+           replica_mode: int = 0, div_max: float | None = None, with_replica: bool = False) -> dict:
+    """replica_mode 0 = mirror (R16), 1 = replica trees (NEXT-2).  with_replica adds a replica
+    to config 2 (a replica server with a 10 Gb/s ingress and 4 replica aggregators)."""
+    d = _config(cid, G=G, tau=tau, dtype=dtype, seed=seed, scale_S=scale_S, gamma=gamma,
+                with_replica=with_replica)
+    d["replica_mode"] = replica_mode
+    if div_max is not None:
+        d["div_max"] = div_max
+    return d
+
+
+def _config(cid: int, *, G, tau, dtype, seed, scale_S, gamma, with_replica) -> dict:
     """Static part of config `cid` (1..5)."""
     if cid == 1:
         W, S, G = 4, 1 << 20, 1
@@ -72,9 +84,18 @@ def config(cid: int, *, G: int | None = None, tau: int | None = None, dtype: str
         d["preset_net"] = "N1"
         d["server_rate"] = 10 * GBPS
         d["site"] = None
-        d["aggs"] = shuffle(seed, list(range(W)), salt=2)[:4]
+        perm = shuffle(seed, list(range(W)), salt=2)
+        d["aggs"] = perm[:4]
         d["tau"] = 4 if tau is None else tau
         d["replan_rates"] = True
+        if with_replica:
+            # a replica server on its own 10 Gb/s machine with k' = 4 replica
+            # aggregators earmarked among the workers
+            n = W + 2
+            d["replica"] = True
+            d["replicas"] = [W + 1]
+            d["raggs"] = perm[4:8]
+            d["replica_rate"] = 10 * GBPS
     else:
         # box model: planner node g = GPU g.  Its NIC up/down = NVLink egress/ingress per
         # direction, shared by every virtual worker multiplexed on it (as co-located workers
@@ -111,6 +132,8 @@ def network(cfg: dict, iteration: int):
         W = cfg["W"]
         ups = draw_rates(cfg["seed"], W, cfg["preset_net"], epoch=iteration, salt=1)
         downs = draw_rates(cfg["seed"], W, cfg["preset_net"], epoch=iteration, salt=2)
+        if cfg.get("replica_rate"):
+            return ups + [0, 0], downs + [cfg["server_rate"], cfg["replica_rate"]], None
         return ups + [0], downs + [cfg["server_rate"]], None
     if cfg["cid"] == 4:
         # N2: every NIC's NVLink share drawn from the rate set scaled to B_nv
