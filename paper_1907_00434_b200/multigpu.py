@@ -97,6 +97,15 @@ class ShardedWorkload:
                        if cfg["replica"] else None)
         self.mirror_h = (torch.zeros(cfg["shards"][prev][1], dtype=torch.float32, device=dev)
                          if (cfg["replica"] and cfg.get("gamma", 0.0)) else None)
+        self.replica_mode = cfg.get("replica_mode", 0) if cfg["replica"] else 0
+        self.retain = None
+        if self.replica_mode == 1:
+            # the replica of shard `prev` lives here and starts equal to w0 of that shard
+            pb, pn = cfg["shards"][prev]
+            m.synth_fill(device, self.mirror.data_ptr(), pn, elem_offset=pb, dtype=m.MLF_F32, seed=cfg["seed"],
+                         kind=2, stream=torch.cuda.current_stream(dev).cuda_stream)
+            self.n_retain = cfg.get("n_retain", max(len(local), 1) * 2)
+            self.retain = torch.empty((self.n_retain, -(-S // 64) * 64), dtype=tdt, device=dev)
         self.n_slots = agg_slots_needed(cfg, world) if mode == "tree" else 0
         self.scratch = (torch.empty((self.n_slots, self.row), dtype=torch.float32, device=dev)
                         if self.n_slots else None)
@@ -106,7 +115,8 @@ class ShardedWorkload:
                 "mirror": m.ipc_export(device, self.mirror.data_ptr()) if self.mirror is not None else None,
                 "mirror_h": (m.ipc_export(device, self.mirror_h.data_ptr())
                              if self.mirror_h is not None else None),
-                "scratch": m.ipc_export(device, self.scratch.data_ptr()) if self.scratch is not None else None}
+                "scratch": m.ipc_export(device, self.scratch.data_ptr()) if self.scratch is not None else None,
+                "retain": m.ipc_export(device, self.retain.data_ptr()) if self.retain is not None else None}
         allinfo = [None] * world
         dist.all_gather_object(allinfo, mine, group=ctrl)
         allinfo.sort(key=lambda d: d["rank"])
@@ -130,9 +140,16 @@ class ShardedWorkload:
             for info in allinfo:
                 base = self.scratch.data_ptr() if info["rank"] == rank else self.mapper.open(info["scratch"])
                 scratch_tab += [base + s * self.row * 4 for s in range(self.n_slots)]
+        retain_tab = None
+        if self.retain is not None:
+            retain_tab = []
+            rowb = self.retain.shape[1] * self.retain.element_size()
+            for info in allinfo:
+                base = self.retain.data_ptr() if info["rank"] == rank else self.mapper.open(info["retain"])
+                retain_tab += [base + s * rowb for s in range(self.n_retain)]
         self.wl = Workload(cfg, device=device, rank=rank, world=world, variant=variant, peer_slots=peer_slots,
                            backup_ptr=backup_ptr, agg_slots=self.n_slots, agg_scratch=scratch_tab,
-                           slot_tensors=slot_tensors, backup_h_ptr=backup_h_ptr)
+                           slot_tensors=slot_tensors, backup_h_ptr=backup_h_ptr, retain_table=retain_tab)
         ev = self.wl.ctx.phase_event()
         evs = [None] * world
         dist.all_gather_object(evs, (rank, ev), group=ctrl)

@@ -36,18 +36,20 @@ def shard_bounds(S: int, G: int, align: int = 64):
 
 def config(cid: int, *, G: int | None = None, tau: int | None = None, dtype: str = "f32",
            seed: int = SEED_ROOT, scale_S: int | None = None, gamma: float = 0.0,
-           replica_mode: int = 0, div_max: float | None = None, with_replica: bool = False) -> dict:
+           replica_mode: int = 0, div_max: float | None = None, with_replica: bool = False,
+           workers: int | None = None) -> dict:
     """replica_mode 0 = mirror (R16), 1 = replica trees (NEXT-2).  with_replica adds a replica
-    to config 2 (a replica server with a 10 Gb/s ingress and 4 replica aggregators)."""
+    to config 2 (a replica server with a 10 Gb/s ingress and 4 replica aggregators).
+    `workers` shrinks the worker count of configs 3-5 (tests whose oracle plans must be fast)."""
     d = _config(cid, G=G, tau=tau, dtype=dtype, seed=seed, scale_S=scale_S, gamma=gamma,
-                with_replica=with_replica)
+                with_replica=with_replica, workers=workers)
     d["replica_mode"] = replica_mode
     if div_max is not None:
         d["div_max"] = div_max
     return d
 
 
-def _config(cid: int, *, G, tau, dtype, seed, scale_S, gamma, with_replica) -> dict:
+def _config(cid: int, *, G, tau, dtype, seed, scale_S, gamma, with_replica, workers) -> dict:
     """Static part of config `cid` (1..5)."""
     if cid == 1:
         W, S, G = 4, 1 << 20, 1
@@ -63,6 +65,8 @@ def _config(cid: int, *, G, tau, dtype, seed, scale_S, gamma, with_replica) -> d
         raise ValueError(cid)
     if scale_S is not None:
         S = scale_S
+    if workers is not None and cid >= 3:
+        W = workers
     d = dict(cid=cid, W=W, S=S, G=G, dtype=dtype, seed=seed, lr=0.01, div_max=math.inf, replica=False,
              preset_net=None, preset_c=None, replan_rates=False, gamma=gamma)
     d["e"] = 2 if dtype == "bf16" else 4

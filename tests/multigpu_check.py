@@ -23,7 +23,7 @@ import torch.distributed as dist  # noqa: E402
 
 import synthgen as sg  # noqa: E402
 from oracle.momentum import weighted_f32  # noqa: E402
-from oracle.numerics import commits_from_plan, execute_plan  # noqa: E402
+from oracle.numerics import commit_batch, commits_from_plan, execute_plan  # noqa: E402
 from oracle.plan import Item, Params, make_net, plan as oracle_plan  # noqa: E402
 from paper_1907_00434_b200.multigpu import ShardedWorkload, init_dist  # noqa: E402
 from synthgen import configs  # noqa: E402
@@ -38,6 +38,9 @@ def main():
     ap.add_argument("--modes", default="fold,tree")
     ap.add_argument("--kernel", default="bulk")
     ap.add_argument("--gamma", type=float, default=0.0)
+    ap.add_argument("--replica-mode", type=int, default=0)
+    ap.add_argument("--div-max", type=float, default=None)
+    ap.add_argument("--workers", type=int, default=None)
     a = ap.parse_args()
     os.environ["MLF_COMMIT_IMPL"] = a.kernel
     rank, world, local, ctrl = init_dist()
@@ -47,7 +50,8 @@ def main():
     for mode in a.modes.split(","):
         if a.gamma and mode != "fold":
             continue                             # momentum runs in fold mode only
-        cfg = configs.config(a.cid, G=world, dtype=a.dtype, scale_S=a.S, gamma=a.gamma)
+        cfg = configs.config(a.cid, G=world, dtype=a.dtype, scale_S=a.S, gamma=a.gamma,
+                             replica_mode=a.replica_mode, div_max=a.div_max, workers=a.workers)
         sw = ShardedWorkload(cfg, rank, world, device, ctrl, mode=mode)
         b, n = cfg["shards"][rank]
         rng = np.random.default_rng(rank)
@@ -55,6 +59,9 @@ def main():
                                         np.arange(max(b, b + n - 17), b + n)]))
         w_ref = sg.w0_values(cfg["seed"], idx)
         h_ref = np.zeros(len(idx), np.float32)
+        r_ref = w_ref.copy()                     # replica model of this shard (replica trees)
+        carried_ids = []                         # (worker, iteration) of the carried items
+        n_punted_total = 0
         carried = []
         v_init = v_prev = 0
         for it in range(a.steps):
@@ -68,7 +75,7 @@ def main():
             prm = Params(servers=cfg["servers"], aggs=cfg["aggs"], replicas=cfg["replicas"], raggs=cfg["raggs"],
                          v_init=v_init, tau_max=cfg["tau"], div_max=cfg["div_max"], gamma=cfg["gamma"],
                          carried=[Item(c["node"], c["size"], 0, 0, c["norm"]) for c in carried],
-                         shard_weights=[x for (_, x) in cfg["shards"]])
+                         shard_weights=[x for (_, x) in cfg["shards"]], replica_mode=cfg["replica_mode"])
             op = oracle_plan(make_net(cfg["n_nodes"], up, down, None, site), batch, prm)
             assert op == pd, f"rank {rank}: plan mismatch"
             operand = lambda g: sg.update_values(cfg["seed"], g, it, idx, dt)  # noqa: E731
@@ -84,7 +91,16 @@ def main():
             assert np.array_equal(got.view(np.uint32), w_ref.view(np.uint32)), f"rank {rank} {mode}: w mismatch"
             torch.cuda.synchronize()
             dist.barrier(group=ctrl)
-            if op["replica_boundary_commit"] >= 0:
+            if cfg["replica"] and cfg["replica_mode"] == 1:
+                # the replica applies its own commits over carried ++ O(U) (NEXT-2)
+                items = carried_ids + [(g, it) for g in op["order"]]
+                rc = [[sg.update_values(cfg["seed"], items[q][0], items[q][1], idx, dt) for q in range(f, f + k)]
+                      for f, k in zip(op["replica_commit_first"], op["replica_commit_count"])]
+                r_ref, _ = commit_batch(r_ref, rc, cfg["lr"])
+                carried_ids = [items[i] for i in op["punted"]]
+                n_punted_total += len(carried_ids)
+                backup_ref = r_ref
+            if op["replica_boundary_commit"] >= 0 or (cfg["replica"] and cfg["replica_mode"] == 1):
                 # rank (rank+1) % world holds our mirror: gather it through the control group
                 mirrors = [None] * world
                 dist.all_gather_object(mirrors, (rank, sw.mirror.cpu().numpy() if sw.mirror is not None else None),
@@ -101,7 +117,8 @@ def main():
         sw.close()
         if rank == 0:
             print(f"MULTIGPU_OK {mode} cid={a.cid} world={world} S={cfg['S']} commits={op['n_commit']} "
-                  f"groups={op['n_groups']} boundary={op['replica_boundary_commit']}", flush=True)
+                  f"groups={op['n_groups']} boundary={op['replica_boundary_commit']} "
+                  f"punted_total={n_punted_total}", flush=True)
     dist.barrier(group=ctrl)
     dist.destroy_process_group()
 

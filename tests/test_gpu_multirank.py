@@ -34,6 +34,14 @@ def test_two_ranks_momentum_with_mirror():
     assert "MULTIGPU_OK fold" in out
 
 
+def test_two_ranks_replica_trees_with_retention():
+    # config 5 (replica of shard j on GPU j+1), count-style Div_max so that updates are punted
+    out = _run(2, "--cid", "5", "--S", "200003", "--steps", "4", "--replica-mode", "1", "--div-max", "20",
+               "--workers", "32", "--modes", "fold,tree")
+    assert "MULTIGPU_OK fold" in out and "MULTIGPU_OK tree" in out
+    assert "punted_total=0" not in out
+
+
 def test_all_gpus_if_several():
     n = torch.cuda.device_count()
     if n < 4:
