@@ -84,6 +84,7 @@ struct mlf_ctx {
   std::vector<void *> retain;                     // [world * n_retain]
   std::vector<std::vector<uint8_t>> used;         // [world][n_retain]
   std::vector<std::pair<int, int>> carried;       // (rank, slot)
+  std::vector<std::pair<int, int>> to_free;       // slots released at the next batch
   int64_t retained_bytes = 0;
   bool started = false, pending = false, sticky = false, phase1_done = false;
   int64_t launches = 0, h2d = 0, d2h = 0;
@@ -506,7 +507,11 @@ static void replicate_trees(mlf_ctx *c, const mlf_plan_out *p) {
   // update until the replica has it)
   const size_t bytes = (size_t)c->cfg.model_elems * c->elem_bytes;
   std::vector<std::pair<int, int>> next;
-  for (int i = 0; i < p->replica_frozen && i < n_c; ++i) c->used[c->carried[i].first][c->carried[i].second] = 0;
+  // slots whose carried item the previous batch froze become free only now: in that batch
+  // another rank's replica kernel may still have been reading them
+  for (auto &rs : c->to_free) c->used[rs.first][rs.second] = 0;
+  c->to_free.clear();
+  for (int i = 0; i < p->replica_frozen && i < n_c; ++i) c->to_free.push_back(c->carried[i]);
   for (int i = p->replica_frozen; i < n_c + p->n_commit; ++i) {
     if (i < n_c) {
       next.push_back(c->carried[i]);
