@@ -58,7 +58,7 @@ class Workload:
         self.replica_mode = cfg.get("replica_mode", 0) if cfg["replica"] else 0
         self.retain = None
         if self.replica_mode == 1 and retain_table is None:
-            n_ret = cfg.get("n_retain", cfg["W"])
+            n_ret = cfg.get("n_retain", 2 * cfg["W"])
             self.retain = torch.empty((n_ret, -(-self.S // 64) * 64), dtype=tdt, device=dev)
             retain_table = [self.retain[i].data_ptr() for i in range(n_ret)]
         self.fill_w0()

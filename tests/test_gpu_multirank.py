@@ -22,7 +22,7 @@ def _run(nproc, *args, timeout=600):
     return r.stdout
 
 
-@pytest.mark.parametrize("cid,extra", [(3, []), (4, ["--steps", "3"]), (5, ["--S", "300007"]),
+@pytest.mark.parametrize("cid,extra", [(3, []), (4, ["--steps", "3"]), (5, ["--S", "300007", "--workers", "64"]),
                                         (3, ["--dtype", "bf16", "--kernel", "bulk"])])
 def test_two_ranks_bitwise(cid, extra):
     out = _run(2, "--cid", str(cid), *extra)
@@ -30,7 +30,7 @@ def test_two_ranks_bitwise(cid, extra):
 
 
 def test_two_ranks_momentum_with_mirror():
-    out = _run(2, "--cid", "5", "--S", "300007", "--gamma", "0.9", "--modes", "fold")
+    out = _run(2, "--cid", "5", "--S", "300007", "--gamma", "0.9", "--modes", "fold", "--workers", "64")
     assert "MULTIGPU_OK fold" in out
 
 
