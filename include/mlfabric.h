@@ -122,6 +122,12 @@ typedef struct {
    * the frozen replica commits — its own Alg. 3 grouping — and exactly the frozen prefix
    * is frozen, the rest punted) */
   int32_t replica_mode;
+  /* 0 = asynchronous SGD (Alg. 2 ordering, deadlines, drops).  1 = synchronous SGD/PS
+   * (MLfabric-S: "update ordering does not apply ... aggregation here starts
+   * with a list of updates"): O(U) = the batch in submission order, nothing dropped, Alg. 3
+   * over that list; one model version per batch (R22).  Also the AllReduce realisation
+   * (P:1297-1308): push every update to the (sharded) root with a sync plan, then get. */
+  int32_t sync_mode;
 } mlf_plan_params;
 
 /* Plan outputs.  All arrays are caller-allocated; `capacity` is their length
@@ -153,6 +159,8 @@ typedef struct {
   int32_t *replica_commit_count;
   int32_t *replica_commit_group;   /* 0 direct to the replica, i >= 1 via replica_agg[i-1] */
   int64_t replica_bytes;           /* bytes those commits deliver to the replica nodes */
+  uint8_t sync_mode;               /* copied from the params: the executor advances the version by
+                                      1 per batch in sync mode, by n_commit otherwise (R2, R22) */
 } mlf_plan_out;
 
 /* Alg. 2 -> Alg. 3 -> §5.3 on one batch.  Pure; may run concurrently. */
@@ -298,6 +306,13 @@ typedef struct {
 } mlf_ipc_event;
 mlf_status mlf_phase_event_export(mlf_ctx *ctx, mlf_ipc_event *out);
 mlf_status mlf_phase_events_open(mlf_ctx *ctx, int32_t n, const mlf_ipc_event *peer_events);
+
+/* get(server, model) of the whole model on one GPU (Table 1): copy n shards (local
+ * or mapped peer fp32 buffers) into dst[begin_i .. begin_i + elems_i).  copy_engine = 0:
+ * SM peer loads through the library's copy kernel (bulk of each shard) — the NVLink
+ * all-gather; 1: one cudaMemcpyAsync per shard on a copy engine.  Completes on `stream`. */
+mlf_status mlf_gather(int32_t device, float *dst, int32_t n, const float *const *shard, const int64_t *begin,
+                      const int64_t *elems, int32_t copy_engine, void *stream);
 
 /* ======================================================================
  * Test infrastructure kernels (not on the hot path)

@@ -13,7 +13,7 @@ from dataclasses import dataclass, field
 
 from .aggregation import chained_commit_times, plan_aggregation
 from .netmodel import Net, component_bytes
-from .ordering import Item, order_final
+from .ordering import Item, OrderResult, order_final
 from .replication import plan_replication
 
 # status codes (same numbering as mlf_status, defined independently)
@@ -40,6 +40,7 @@ class Params:
     carried: list = field(default_factory=list)        # Items (node, size, norm), in order
     shard_weights: list | None = None                  # None = equal weights
     replica_mode: int = 0                              # 0 mirror (R16), 1 replica trees (NEXT-2)
+    sync_mode: int = 0                                 # 1: MLfabric-S, Alg. 3 over the list (NEXT-3)
 
 
 def validate(net: Net, batch: list, prm: Params) -> list:
@@ -58,6 +59,8 @@ def validate(net: Net, batch: list, prm: Params) -> list:
         raise PlanError(E_INVALID, "replica count must equal server count")
     if prm.replica_mode not in (0, 1):
         raise PlanError(E_INVALID, "replica_mode")
+    if prm.sync_mode not in (0, 1):
+        raise PlanError(E_INVALID, "sync_mode")
     if prm.tau_max < 0 or not (prm.div_max >= 0) or not (0.0 <= prm.gamma < 1.0):
         raise PlanError(E_INVALID, "tau_max / div_max / gamma")
     if not (prm.hist_norm >= 0 and math.isfinite(prm.hist_norm)):
@@ -85,8 +88,13 @@ def plan(net: Net, batch: list, prm: Params) -> dict:
     """Compute the batch plan; returns the integer outputs of mlf_plan as a dict."""
     w = validate(net, batch, prm)
     n = len(batch)
-    # 1. ordering (Alg. 2, App. B.2)
-    ores = order_final(net, batch, prm.servers, w, prm.tau_max, prm.v_init)
+    # 1. ordering (Alg. 2, App. B.2); synchronous mode (P:1264-1268): "update ordering
+    #    does not apply ... aggregation here starts with a list of updates" — the batch in
+    #    submission order, nothing dropped (R22)
+    if prm.sync_mode:
+        ores = OrderResult(list(range(n)), [0] * n)
+    else:
+        ores = order_final(net, batch, prm.servers, w, prm.tau_max, prm.v_init)
     order = ores.order
     ordered_items = [batch[g] for g in order]
     # 2. aggregation (Alg. 3) on the batch-start network (R10)
@@ -112,7 +120,7 @@ def plan(net: Net, batch: list, prm: Params) -> dict:
         "replica_frozen": 0, "replica_boundary_commit": -1, "n_punted": 0, "punted": [],
         "delayed_last": 0, "t_total_ns": times[-1] if times else 0,
         "n_replica_commits": 0, "replica_commit_first": [], "replica_commit_count": [],
-        "replica_commit_group": [], "replica_bytes": 0,
+        "replica_commit_group": [], "replica_bytes": 0, "sync_mode": int(prm.sync_mode),
     }
     # 3. replication (§5.3) on the network after the server plan's reservations
     if prm.replicas:

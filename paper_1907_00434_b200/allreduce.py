@@ -1,0 +1,112 @@
+"""AllReduce through MLfabric's push/get — NEXT-3, on one box of GPUs.
+
+"MLfabric would implement AllReduce through successive calls to push(root, update, norm)
+and get(root, update), using a synchronous consistency model; root ... acts as the root of
+the aggregation topology, which is a dynamically constructed tree".
+
+B200 realisation: the root is the sharded parameter server of multigpu.py (shard j on GPU
+j: all NVLink ports of the box serve the root), the plan is a synchronous one (MLfabric-S,
+P:1264-1268: Alg. 3 over the list of updates, nothing dropped), and the "model" starts at
+zero with lr = -1, so the fused commit computes w = 0 - (-1 * x) = the sum of the updates
+in the plan's fold order (push = a plan-driven reduce-scatter fused into the commit
+kernel).  get = every GPU gathers all shards over NVLink (mlf_gather, SM peer loads).
+Host plumbing only; all bytes move in libmlfabric's kernels.
+"""
+from __future__ import annotations
+
+import time
+
+import torch
+import torch.distributed as dist
+
+from synthgen import configs as cfgs
+
+from . import mlfabric as m
+from .multigpu import IpcMapper, ShardedWorkload, max_over_ranks
+
+
+def allreduce_config(S: int, world: int, dtype: str = "f32", workers: int | None = None) -> dict:
+    """One virtual worker per GPU (or `workers`), box model, synchronous plan, lr = -1."""
+    W = workers or world
+    cfg = cfgs.config(3, G=world, scale_S=S, workers=W, tau=W, dtype=dtype)
+    cfg["sync_mode"] = 1
+    cfg["lr"] = -1.0
+    return cfg
+
+
+class MlfAllReduce:
+    def __init__(self, cfg: dict, rank: int, world: int, device: int, ctrl):
+        self.cfg, self.rank, self.world, self.device, self.ctrl = cfg, rank, world, device, ctrl
+        self.sw = ShardedWorkload(cfg, rank, world, device, ctrl, mode="fold")
+        dev = torch.device("cuda", device)
+        self.out = torch.empty(cfg["S"], dtype=torch.float32, device=dev)
+        blobs = [None] * world
+        dist.all_gather_object(blobs, (rank, m.ipc_export(device, self.sw.wl.w.data_ptr())), group=ctrl)
+        self.mapper = IpcMapper(device)
+        self.shard_ptrs = [self.sw.wl.w.data_ptr() if r == rank else self.mapper.open(b) for r, b in sorted(blobs)]
+        self.begins = [b for (b, _) in cfg["shards"]]
+        self.elems = [n for (_, n) in cfg["shards"]]
+
+    def run(self, iteration: int, flush=None):
+        """push (sharded fused reduce) then get (gather).  Returns (plan, push ms, get ms, wall ms),
+        device times max over ranks."""
+        stream = torch.cuda.current_stream()
+        t0 = time.perf_counter()
+        self.sw.wl.w.zero_()                      # the root's accumulator
+        pd, ms_push = self.sw.step(iteration, flush=flush)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        m.gather(self.device, self.out.data_ptr(), self.shard_ptrs, self.begins, self.elems, stream=stream.cuda_stream)
+        e1.record(stream)
+        e1.synchronize()
+        self.sw.barrier()                         # nobody zeroes a shard another rank still reads
+        wall = (time.perf_counter() - t0) * 1e3
+        return pd, max_over_ranks(ms_push, self.ctrl), max_over_ranks(e0.elapsed_time(e1), self.ctrl), \
+            max_over_ranks(wall, self.ctrl)
+
+    def close(self):
+        self.sw.close()
+        self.mapper.close()
+
+
+def bench_allreduce(S: int, rank: int, world: int, device: int, ctrl, steps: int = 5, warmup: int = 2,
+                    flush=None) -> dict:
+    """MLfabric AllReduce vs NCCL all_reduce on the same per-GPU buffer of S fp32 values."""
+    cfg = allreduce_config(S, world)
+    ar = MlfAllReduce(cfg, rank, world, device, ctrl)
+    ar.sw.fill(0)
+    push = get = wall = 0.0
+    for s in range(warmup + steps):
+        _, mp, mg, mw = ar.run(s, flush=flush)
+        if s >= warmup:
+            push, get, wall = push + mp, get + mg, wall + mw
+    ar.close()
+    # NCCL on the default (NCCL) process group, same bytes per GPU
+    t = torch.ones(S, dtype=torch.float32, device=torch.device("cuda", device))
+    nccl_ms = None
+    if dist.get_backend() == "nccl":
+        for _ in range(warmup):
+            dist.all_reduce(t)
+        torch.cuda.synchronize()
+        acc = 0.0
+        for _ in range(steps):
+            if flush is not None:
+                flush()
+            dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            dist.all_reduce(t)
+            e1.record()
+            e1.synchronize()
+            acc += max_over_ranks(e0.elapsed_time(e1), ctrl)
+        nccl_ms = acc / steps
+    nbytes = S * 4
+    dev_ms = (push + get) / steps
+
+    def busbw(ms):
+        return round(2 * (world - 1) / world * nbytes / (ms / 1e3) / 1e9, 1) if ms else None
+
+    return {"bytes_per_gpu": nbytes, "mlfabric_device_ms": round(dev_ms, 4),
+            "mlfabric_push_ms": round(push / steps, 4), "mlfabric_get_ms": round(get / steps, 4),
+            "mlfabric_wall_ms": round(wall / steps, 3), "mlfabric_busbw_GBps": busbw(dev_ms),
+            "nccl_ms": round(nccl_ms, 4) if nccl_ms else None, "nccl_busbw_GBps": busbw(nccl_ms)}

@@ -570,7 +570,7 @@ static void phase_commit(mlf_ctx *c, const mlf_plan_out *p) {
   c->started = false;
   c->pending = true;
   // version accounting (R2): every committed update advances the version
-  c->version += p->n_commit;
+  c->version += p->sync_mode ? (p->n_commit > 0 ? 1 : 0) : p->n_commit;   // R22 / R2
   for (int w : c->b_worker) {
     c->in_flight[w] = 1;
     c->in_batch[w] = 0;
@@ -749,6 +749,32 @@ extern "C" mlf_status mlf_copy_kernel(int32_t device, void *dst, const void *src
     int sm = 148;
     CK(cudaDeviceGetAttribute(&sm, cudaDevAttrMultiProcessorCount, device));
     CK(launch_copy(dst, src, bytes, static_cast<cudaStream_t>(stream), sm));
+  });
+}
+
+extern "C" mlf_status mlf_gather(int32_t device, float *dst, int32_t n, const float *const *shard,
+                                 const int64_t *begin, const int64_t *elems, int32_t copy_engine, void *stream) {
+  return guard([&] {
+    if (!dst || n < 0 || (n > 0 && (!shard || !begin || !elems))) throw Fail{MLF_E_INVALID, "gather arguments"};
+    CK(cudaSetDevice(device));
+    int sm = 148;
+    CK(cudaDeviceGetAttribute(&sm, cudaDevAttrMultiProcessorCount, device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    for (int i = 0; i < n; ++i) {
+      if (elems[i] < 0 || begin[i] < 0 || (elems[i] > 0 && !shard[i])) throw Fail{MLF_E_INVALID, "gather shard"};
+      float *d = dst + begin[i];
+      const int64_t bytes = elems[i] * 4;
+      const bool aligned = ((reinterpret_cast<uintptr_t>(d) | reinterpret_cast<uintptr_t>(shard[i])) & 15) == 0;
+      if (copy_engine || !aligned) {
+        if (bytes) CK(cudaMemcpyAsync(d, shard[i], (size_t)bytes, cudaMemcpyDeviceToDevice, s));
+        continue;
+      }
+      const int64_t body = bytes & ~int64_t(15);
+      CK(launch_copy(d, shard[i], body, s, sm));
+      if (bytes > body)
+        CK(cudaMemcpyAsync(reinterpret_cast<char *>(d) + body, reinterpret_cast<const char *>(shard[i]) + body,
+                           (size_t)(bytes - body), cudaMemcpyDeviceToDevice, s));
+    }
   });
 }
 

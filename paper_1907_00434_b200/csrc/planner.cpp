@@ -733,6 +733,7 @@ static mlf_status plan_impl(const mlf_net *net, const mlf_batch *batch, const ml
     c.raggs.push_back(prm->replica_agg[i]);
   }
   if (prm->replica_mode != 0 && prm->replica_mode != 1) throw PlanFail{MLF_E_INVALID, "replica_mode"};
+  if (prm->sync_mode != 0 && prm->sync_mode != 1) throw PlanFail{MLF_E_INVALID, "sync_mode"};
   if (prm->tau_max < 0 || !(prm->div_max >= 0) || !(prm->gamma >= 0.0 && prm->gamma < 1.0))
     throw PlanFail{MLF_E_INVALID, "tau_max / div_max / gamma"};
   if (!(prm->hist_norm >= 0 && std::isfinite(prm->hist_norm))) throw PlanFail{MLF_E_INVALID, "hist_norm"};
@@ -784,7 +785,14 @@ static mlf_status plan_impl(const mlf_net *net, const mlf_batch *batch, const ml
   }
 
   // 1. ordering
-  OrderRes ores = order_final(c, items, prm->tau_max, prm->v_init);
+  // (sync mode: no ordering — the list in submission order, nothing dropped)
+  OrderRes ores;
+  if (prm->sync_mode) {
+    for (int g = 0; g < n; ++g) ores.order.push_back(g);
+    ores.reason.assign(n, 0);
+  } else {
+    ores = order_final(c, items, prm->tau_max, prm->v_init);
+  }
   std::vector<Item> ordered;
   for (int g : ores.order) ordered.push_back(items[g]);
   // 2. aggregation on the batch-start network (R10)
@@ -817,6 +825,7 @@ static mlf_status plan_impl(const mlf_net *net, const mlf_batch *batch, const ml
   out->n_punted = 0;
   out->n_replica_commits = 0;
   out->replica_bytes = 0;
+  out->sync_mode = (uint8_t)prm->sync_mode;
   out->delayed_last = 0;
   out->t_total_ns = times.empty() ? 0 : times.back();
 

@@ -98,7 +98,8 @@ class Workload:
         prm, k2 = m.make_params(c["servers"], aggs=c["aggs"], replicas=c["replicas"], raggs=c["raggs"],
                                 v_init=self.v_init, tau_max=c["tau"], div_max=c["div_max"],
                                 gamma=c.get("gamma", 0.0), hist_norm=0.0, carried=self.carried,
-                                shard_weights=weights, replica_mode=self.replica_mode)
+                                shard_weights=weights, replica_mode=self.replica_mode,
+                                sync_mode=c.get("sync_mode", 0))
         return net, prm, (k1, k2)
 
     def submit_all(self, iteration: int):
@@ -115,7 +116,10 @@ class Workload:
     def after_commit(self, plan_dict: dict, draws):
         """Harness bookkeeping: versions, punted replica items for the next batch."""
         self.v_prev = self.v_init
-        self.v_init += plan_dict["n_commit"]
+        if plan_dict.get("sync_mode"):
+            self.v_init += 1 if plan_dict["n_commit"] else 0     # one version per iteration (R22)
+        else:
+            self.v_init += plan_dict["n_commit"]
         if self.cfg["replica"]:
             items = list(self.carried) + [dict(node=self.cfg["worker_node"][g], size=self.S * self.cfg["e"],
                                                norm=draws[g]["norm"]) for g in plan_dict["order"]]

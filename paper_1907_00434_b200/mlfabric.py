@@ -24,7 +24,7 @@ EXPORTS = (
     "mlf_plan", "mlf_init", "mlf_submit_update", "mlf_set_update_host", "mlf_batch_view", "mlf_version",
     "mlf_execute", "mlf_execute_phase", "mlf_sync", "mlf_pull_model", "mlf_stats", "mlf_destroy",
     "mlf_last_error", "mlf_ipc_export", "mlf_ipc_open", "mlf_ipc_close", "mlf_phase_event_export",
-    "mlf_phase_events_open", "mlf_synth_fill", "mlf_copy_kernel", "mlf_copy_engine",
+    "mlf_phase_events_open", "mlf_gather", "mlf_synth_fill", "mlf_copy_kernel", "mlf_copy_engine",
 )
 
 
@@ -61,7 +61,7 @@ class MlfPlanParams(C.Structure):
                 ("v_init", C.c_int64), ("tau_max", C.c_int32),
                 ("div_max", C.c_double), ("gamma", C.c_double), ("hist_norm", C.c_double),
                 ("n_carried", C.c_int32), ("carried_node", _i32p), ("carried_bytes", _i64p),
-                ("carried_norm", _f64p), ("replica_mode", C.c_int32)]
+                ("carried_norm", _f64p), ("replica_mode", C.c_int32), ("sync_mode", C.c_int32)]
 
 
 class MlfPlanOut(C.Structure):
@@ -72,7 +72,7 @@ class MlfPlanOut(C.Structure):
                 ("n_punted", C.c_int32), ("punted", _i32p), ("delayed_last", C.c_uint8),
                 ("t_total_ns", C.c_int64), ("n_replica_commits", C.c_int32),
                 ("replica_commit_first", _i32p), ("replica_commit_count", _i32p),
-                ("replica_commit_group", _i32p), ("replica_bytes", C.c_int64)]
+                ("replica_commit_group", _i32p), ("replica_bytes", C.c_int64), ("sync_mode", C.c_uint8)]
 
 
 class MlfConfig(C.Structure):
@@ -117,6 +117,7 @@ _lib.mlf_synth_fill.argtypes = [C.c_int32, _p, C.c_int64, C.c_int64, C.c_int32, 
                                 C.c_int64, C.c_int64, C.c_int32, _p]
 _lib.mlf_copy_kernel.argtypes = [C.c_int32, _p, _p, C.c_int64, _p]
 _lib.mlf_copy_engine.argtypes = [C.c_int32, _p, _p, C.c_int64, _p]
+_lib.mlf_gather.argtypes = [C.c_int32, _p, C.c_int32, C.POINTER(_p), _i64p, _i64p, C.c_int32, _p]
 
 
 def lib():
@@ -141,7 +142,7 @@ def _ptr(a: np.ndarray | None, ct):
 # ----------------------------------------------------------------- planning
 def plan(n_nodes, nic_up, nic_down, batch, servers, *, bw=None, site=None, aggs=(), replicas=(), raggs=(),
          v_init=0, tau_max=1, div_max=math.inf, gamma=0.0, hist_norm=0.0, carried=(), shard_weights=None,
-         replica_mode=0) -> dict:
+         replica_mode=0, sync_mode=0) -> dict:
     """mlf_plan.  `batch` = list of dicts (node, size, version, t_avail, norm) or a dict of arrays;
     `carried` = list of dicts (node, size, norm).  Returns the plan as a dict of Python lists."""
     keep = []
@@ -174,7 +175,7 @@ def plan(n_nodes, nic_up, nic_down, batch, servers, *, bw=None, site=None, aggs=
     prm = MlfPlanParams(len(sv), _ptr(sv, C.c_int32), _ptr(sw, C.c_int64), len(ag), _ptr(ag, C.c_int32),
                         len(rp), _ptr(rp, C.c_int32), len(ra), _ptr(ra, C.c_int32), int(v_init), int(tau_max),
                         float(div_max), float(gamma), float(hist_norm), len(cn), _ptr(cn, C.c_int32),
-                        _ptr(cb, C.c_int64), _ptr(cm, C.c_double), int(replica_mode))
+                        _ptr(cb, C.c_int64), _ptr(cm, C.c_double), int(replica_mode), int(sync_mode))
     return plan_raw(net, b, prm, n + len(cn), keep)
 
 
@@ -221,7 +222,7 @@ class PlanBuffers:
             "replica_commit_first": self.rfirst[:o.n_replica_commits].tolist(),
             "replica_commit_count": self.rcount[:o.n_replica_commits].tolist(),
             "replica_commit_group": self.rgroup[:o.n_replica_commits].tolist(),
-            "replica_bytes": o.replica_bytes,
+            "replica_bytes": o.replica_bytes, "sync_mode": int(o.sync_mode),
         }
 
 
@@ -258,6 +259,7 @@ def plan_from_dict(d: dict) -> MlfPlanOut:
     b.rcount[:len(rf)] = d.get("replica_commit_count", [])
     b.rgroup[:len(rf)] = d.get("replica_commit_group", [0] * len(rf))
     o.replica_bytes = d.get("replica_bytes", 0)
+    o.sync_mode = d.get("sync_mode", 0)
     return b
 
 
@@ -374,7 +376,7 @@ def make_net(n_nodes, nic_up, nic_down, bw=None, site=None):
 
 
 def make_params(servers, *, aggs=(), replicas=(), raggs=(), v_init=0, tau_max=1, div_max=math.inf, gamma=0.0,
-                hist_norm=0.0, carried=(), shard_weights=None, replica_mode=0):
+                hist_norm=0.0, carried=(), shard_weights=None, replica_mode=0, sync_mode=0):
     """(MlfPlanParams, keep-alive arrays)."""
     sv, ag = _arr(servers, np.int32), _arr(list(aggs), np.int32)
     rp, ra = _arr(list(replicas), np.int32), _arr(list(raggs), np.int32)
@@ -385,7 +387,7 @@ def make_params(servers, *, aggs=(), replicas=(), raggs=(), v_init=0, tau_max=1,
     prm = MlfPlanParams(len(sv), _ptr(sv, C.c_int32), _ptr(sw, C.c_int64), len(ag), _ptr(ag, C.c_int32),
                         len(rp), _ptr(rp, C.c_int32), len(ra), _ptr(ra, C.c_int32), int(v_init), int(tau_max),
                         float(div_max), float(gamma), float(hist_norm), len(cn), _ptr(cn, C.c_int32),
-                        _ptr(cb, C.c_int64), _ptr(cm, C.c_double), int(replica_mode))
+                        _ptr(cb, C.c_int64), _ptr(cm, C.c_double), int(replica_mode), int(sync_mode))
     return prm, (sv, ag, rp, ra, sw, cn, cb, cm)
 
 
@@ -417,6 +419,14 @@ def synth_fill(device: int, dst_ptr: int, n: int, *, elem_offset: int = 0, dtype
 
 def copy_kernel(device: int, dst_ptr: int, src_ptr: int, nbytes: int, stream=None):
     _check(_lib.mlf_copy_kernel(device, dst_ptr, src_ptr, int(nbytes), stream))
+
+
+def gather(device: int, dst_ptr: int, shard_ptrs, begins, elems, copy_engine: bool = False, stream=None):
+    """mlf_gather: the whole model from its shards (local or mapped peer pointers)."""
+    n = len(shard_ptrs)
+    sp = (_p * max(n, 1))(*shard_ptrs)
+    b, e = _arr(begins, np.int64), _arr(elems, np.int64)
+    _check(_lib.mlf_gather(device, dst_ptr, n, sp, _ptr(b, C.c_int64), _ptr(e, C.c_int64), int(copy_engine), stream))
 
 
 def copy_engine(device: int, dst_ptr: int, src_ptr: int, nbytes: int, stream=None):

@@ -33,6 +33,7 @@ class Instance:
     carried: list = field(default_factory=list)    # dicts: node, size, norm
     shard_weights: list | None = None
     replica_mode: int = 0
+    sync_mode: int = 0
 
 
 def random_instance(seed: int, idx: int, max_n: int = 8, max_servers: int = 2,
@@ -108,7 +109,8 @@ def random_instance(seed: int, idx: int, max_n: int = 8, max_servers: int = 2,
     if G > 1 and ri(0, 1):
         weights = [ri(1, 9) for _ in range(G)]
     return Instance(n_nodes, nic_up, nic_down, bw, site, batch, servers, aggs, replicas, raggs,
-                    v_init, tau, div_max, gamma, hist, carried, weights, replica_mode=ri(0, 1))
+                    v_init, tau, div_max, gamma, hist, carried, weights, replica_mode=ri(0, 1),
+                    sync_mode=1 if ri(0, 4) == 0 else 0)
 
 
 def to_oracle(inst: Instance):
@@ -120,5 +122,5 @@ def to_oracle(inst: Instance):
     prm = Params(servers=inst.servers, aggs=inst.aggs, replicas=inst.replicas, raggs=inst.raggs,
                  v_init=inst.v_init, tau_max=inst.tau_max, div_max=inst.div_max, gamma=inst.gamma,
                  hist_norm=inst.hist_norm, carried=carried, shard_weights=inst.shard_weights,
-                 replica_mode=inst.replica_mode)
+                 replica_mode=inst.replica_mode, sync_mode=inst.sync_mode)
     return net, batch, prm

@@ -42,6 +42,14 @@ def test_two_ranks_replica_trees_with_retention():
     assert "punted_total=0" not in out
 
 
+def test_two_ranks_allreduce_push_get():
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", "--nnodes=1", "--nproc-per-node=2",
+           os.path.join(HERE, "allreduce_check.py"), "--S", "500009", "--workers", "8"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, MASTER_ADDR="127.0.0.1", OMP_NUM_THREADS="1"))
+    assert r.returncode == 0 and "ALLREDUCE_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
 def test_all_gpus_if_several():
     n = torch.cuda.device_count()
     if n < 4:

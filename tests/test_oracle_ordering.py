@@ -114,9 +114,21 @@ def test_lookahead_never_fires_on_sjf_picks():
         assert sorted(res.order) == list(range(len(batch)))
 
 
+def test_sync_mode_keeps_the_list():
+    # MLfabric-S: no ordering, no drops; Alg. 3 still groups the list
+    for i in range(200):
+        inst = random_instance(4321, i, max_n=8, replica=False)
+        inst.sync_mode = 1
+        net, batch, prm = to_oracle(inst)
+        p = plan(net, batch, prm)
+        assert p["order"] == list(range(len(batch))) and set(p["drop_reason"]) <= {0}
+        assert sum(p["commit_count"]) == len(batch)
+
+
 def test_delay_bound_invariant_1000_batches():
     for i in range(1000):
         inst = random_instance(1234, i, max_n=8, replica=(i % 3 == 0))
+        inst.sync_mode = 0                     # the delay bound is an asynchronous-SGD notion
         net, batch, prm = to_oracle(inst)
         p = plan(net, batch, prm)
         check_plan(p, [b.version for b in batch], inst.tau_max, inst.v_init, len(inst.aggs))

@@ -19,7 +19,8 @@ def cpp_plan(inst):
     return m.plan(inst.n_nodes, inst.nic_up, inst.nic_down, inst.batch, inst.servers, bw=inst.bw, site=inst.site,
                   aggs=inst.aggs, replicas=inst.replicas, raggs=inst.raggs, v_init=inst.v_init,
                   tau_max=inst.tau_max, div_max=inst.div_max, gamma=inst.gamma, hist_norm=inst.hist_norm,
-                  carried=inst.carried, shard_weights=inst.shard_weights, replica_mode=inst.replica_mode)
+                  carried=inst.carried, shard_weights=inst.shard_weights, replica_mode=inst.replica_mode,
+                  sync_mode=inst.sync_mode)
 
 
 def both(inst):
