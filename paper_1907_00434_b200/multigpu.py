@@ -372,6 +372,11 @@ def run_bench_multi(a):
     for i, mode in enumerate(modes):
         results[mode] = run(mode, a.steps if i == 0 else max(3, a.steps // 2), a.warmup if i == 0 else 2,
                             clocks=(i == 0))
+    ar = None
+    if not a.no_variants:
+        # NEXT-3: AllReduce via push/get vs NCCL all_reduce, ResNet-50-sized buffer per GPU
+        from .allreduce import bench_allreduce
+        ar = bench_allreduce(25_600_000, rank, world, local, ctrl, steps=5, warmup=2, flush=l2_flush)
     e2e = None
     if not a.no_e2e:
         e2e = e2e_multi(cfgs.config(cid, G=world, tau=a.tau, dtype=a.dtype), rank, world, local, ctrl,
@@ -420,6 +425,8 @@ def run_bench_multi(a):
             "value": round(sum(r["bytes"] for r in recs2) / T2 / 1e9, 2), "unit": "GB/s",
             "ms_per_step": round(T2 * 1e3 / len(recs2), 4),
             "roofline_frac": round(sum(r["t_roof"] for r in recs2) / T2, 4)}}
+    if ar is not None:
+        line.setdefault("variants", {})["allreduce_push_get_vs_nccl"] = ar
     if e2e is not None:
         line["e2e"] = e2e
     print(json.dumps(line), flush=True)
