@@ -760,21 +760,27 @@ extern "C" mlf_status mlf_gather(int32_t device, float *dst, int32_t n, const fl
     int sm = 148;
     CK(cudaDeviceGetAttribute(&sm, cudaDevAttrMultiProcessorCount, device));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    GatherArgs g{};
     for (int i = 0; i < n; ++i) {
       if (elems[i] < 0 || begin[i] < 0 || (elems[i] > 0 && !shard[i])) throw Fail{MLF_E_INVALID, "gather shard"};
       float *d = dst + begin[i];
       const int64_t bytes = elems[i] * 4;
       const bool aligned = ((reinterpret_cast<uintptr_t>(d) | reinterpret_cast<uintptr_t>(shard[i])) & 15) == 0;
-      if (copy_engine || !aligned) {
+      if (copy_engine || !aligned || g.n == kMaxShards) {
         if (bytes) CK(cudaMemcpyAsync(d, shard[i], (size_t)bytes, cudaMemcpyDeviceToDevice, s));
         continue;
       }
       const int64_t body = bytes & ~int64_t(15);
-      CK(launch_copy(d, shard[i], body, s, sm));
+      g.vstart[g.n] = g.total_v;
+      g.dst[g.n] = d;
+      g.src[g.n] = shard[i];
+      g.total_v += body / 16;
+      ++g.n;
       if (bytes > body)
         CK(cudaMemcpyAsync(reinterpret_cast<char *>(d) + body, reinterpret_cast<const char *>(shard[i]) + body,
                            (size_t)(bytes - body), cudaMemcpyDeviceToDevice, s));
     }
+    CK(launch_gather(g, s, sm));
   });
 }
 

@@ -66,6 +66,17 @@ cudaError_t launch_synth(void *dst, int64_t n, int64_t elem_offset, int dtype, u
                          int variant, cudaStream_t s);
 cudaError_t launch_copy(void *dst, const void *src, int64_t bytes, cudaStream_t s, int sm_count);
 
+// one launch gathering up to kMaxShards 16-byte-aligned pieces (float4 counts)
+constexpr int kMaxShards = 16;
+struct GatherArgs {
+  int32_t n;
+  int64_t total_v;                 // float4s over all pieces
+  int64_t vstart[kMaxShards];      // prefix sums of the pieces' float4 counts
+  float *dst[kMaxShards];
+  const float *src[kMaxShards];
+};
+cudaError_t launch_gather(const GatherArgs &a, cudaStream_t s, int sm_count);
+
 // host-side splitmix64 key derivation (same definition as synthgen.stream_key)
 uint64_t synth_stream_key(uint64_t seed, uint64_t kind, uint64_t a, uint64_t b);
 

@@ -76,6 +76,26 @@ __global__ void __launch_bounds__(256) copy_kernel(float4 *__restrict__ dst, con
   for (; i < nv; i += stride) __stcs(dst + i, __ldcs(src + i));
 }
 
+// get of the whole model: every shard (local or peer) copied in ONE launch, so the reads
+// from all peers are in flight together instead of one peer per launch
+__global__ void __launch_bounds__(256) gather_kernel(const __grid_constant__ GatherArgs a) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int j = 0;
+  for (; i < a.total_v; i += stride) {
+    while (j + 1 < a.n && i >= a.vstart[j + 1]) ++j;
+    while (j > 0 && i < a.vstart[j]) --j;
+    const int64_t v = i - a.vstart[j];
+    __stcs(reinterpret_cast<float4 *>(a.dst[j]) + v, __ldcs(reinterpret_cast<const float4 *>(a.src[j]) + v));
+  }
+}
+
+cudaError_t launch_gather(const GatherArgs &a, cudaStream_t s, int sm_count) {
+  if (a.total_v <= 0) return cudaSuccess;
+  gather_kernel<<<sm_count * 8, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_copy(void *dst, const void *src, int64_t bytes, cudaStream_t s, int sm_count) {
   int64_t nv = bytes / 16;
   if (nv <= 0) return cudaSuccess;
