@@ -216,6 +216,13 @@ typedef struct {
   int32_t replica_mode;
   int32_t n_retain;
   void *const *retain_slot;
+  /* Fused get (Table 1 get; the pull of the new model by every GPU): the commit pass
+   * also stores each final w tile of this shard into n_bcast full-length fp32 model views
+   * (bcast[i] + shard_begin; local or mapped peer pointers) — the all-gather of the new
+   * model overlapped tile by tile with the reduce.  Used by the AllReduce realisation
+   * (P:1297-1308).  gamma = 0 only; at most 8 destinations. */
+  int32_t n_bcast;
+  float *const *bcast;
 } mlf_config;
 
 typedef struct mlf_ctx mlf_ctx;

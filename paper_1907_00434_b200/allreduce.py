@@ -35,11 +35,16 @@ def allreduce_config(S: int, world: int, dtype: str = "f32", workers: int | None
 
 
 class MlfAllReduce:
-    def __init__(self, cfg: dict, rank: int, world: int, device: int, ctrl):
+    """fused = True: the commit kernel of every shard also stores its final tiles into every
+    GPU's result view (push and get in ONE kernel per GPU, NVLink stores overlapped with the
+    reduce); fused = False: push, barrier, then get with mlf_gather (peer loads)."""
+
+    def __init__(self, cfg: dict, rank: int, world: int, device: int, ctrl, fused: bool = True):
         self.cfg, self.rank, self.world, self.device, self.ctrl = cfg, rank, world, device, ctrl
-        self.sw = ShardedWorkload(cfg, rank, world, device, ctrl, mode="fold")
+        self.fused = fused
+        self.sw = ShardedWorkload(cfg, rank, world, device, ctrl, mode="fold", fused_get=fused)
         dev = torch.device("cuda", device)
-        self.out = torch.empty(cfg["S"], dtype=torch.float32, device=dev)
+        self.out = self.sw.view[:cfg["S"]] if fused else torch.empty(cfg["S"], dtype=torch.float32, device=dev)
         blobs = [None] * world
         dist.all_gather_object(blobs, (rank, m.ipc_export(device, self.sw.wl.w.data_ptr())), group=ctrl)
         self.mapper = IpcMapper(device)
@@ -54,6 +59,9 @@ class MlfAllReduce:
         t0 = time.perf_counter()
         self.sw.wl.w.zero_()                      # the root's accumulator
         pd, ms_push = self.sw.step(iteration, flush=flush)
+        if self.fused:                            # every view was written by the commits
+            wall = (time.perf_counter() - t0) * 1e3
+            return pd, max_over_ranks(ms_push, self.ctrl), 0.0, max_over_ranks(wall, self.ctrl)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         m.gather(self.device, self.out.data_ptr(), self.shard_ptrs, self.begins, self.elems, stream=stream.cuda_stream)
@@ -73,14 +81,17 @@ def bench_allreduce(S: int, rank: int, world: int, device: int, ctrl, steps: int
                     flush=None) -> dict:
     """MLfabric AllReduce vs NCCL all_reduce on the same per-GPU buffer of S fp32 values."""
     cfg = allreduce_config(S, world)
-    ar = MlfAllReduce(cfg, rank, world, device, ctrl)
-    ar.sw.fill(0)
-    push = get = wall = 0.0
-    for s in range(warmup + steps):
-        _, mp, mg, mw = ar.run(s, flush=flush)
-        if s >= warmup:
-            push, get, wall = push + mp, get + mg, wall + mw
-    ar.close()
+    res = {}
+    for fused in (True, False):
+        ar = MlfAllReduce(cfg, rank, world, device, ctrl, fused=fused)
+        ar.sw.fill(0)
+        push = get = wall = 0.0
+        for s in range(warmup + steps):
+            _, mp, mg, mw = ar.run(s, flush=flush)
+            if s >= warmup:
+                push, get, wall = push + mp, get + mg, wall + mw
+        ar.close()
+        res[fused] = (push / steps, get / steps, wall / steps)
     # NCCL on the default (NCCL) process group, same bytes per GPU
     t = torch.ones(S, dtype=torch.float32, device=torch.device("cuda", device))
     nccl_ms = None
@@ -101,12 +112,16 @@ def bench_allreduce(S: int, rank: int, world: int, device: int, ctrl, steps: int
             acc += max_over_ranks(e0.elapsed_time(e1), ctrl)
         nccl_ms = acc / steps
     nbytes = S * 4
-    dev_ms = (push + get) / steps
 
     def busbw(ms):
         return round(2 * (world - 1) / world * nbytes / (ms / 1e3) / 1e9, 1) if ms else None
 
-    return {"bytes_per_gpu": nbytes, "mlfabric_device_ms": round(dev_ms, 4),
-            "mlfabric_push_ms": round(push / steps, 4), "mlfabric_get_ms": round(get / steps, 4),
-            "mlfabric_wall_ms": round(wall / steps, 3), "mlfabric_busbw_GBps": busbw(dev_ms),
-            "nccl_ms": round(nccl_ms, 4) if nccl_ms else None, "nccl_busbw_GBps": busbw(nccl_ms)}
+    fp, _, fw = res[True]
+    gp, gg, gw = res[False]
+    return {"bytes_per_gpu": nbytes,
+            "mlfabric_fused_ms": round(fp, 4), "mlfabric_fused_busbw_GBps": busbw(fp),
+            "mlfabric_fused_wall_ms": round(fw, 3),
+            "mlfabric_push_then_gather_ms": round(gp + gg, 4), "push_ms": round(gp, 4), "gather_ms": round(gg, 4),
+            "mlfabric_push_then_gather_busbw_GBps": busbw(gp + gg),
+            "nccl_ms": round(nccl_ms, 4) if nccl_ms else None, "nccl_busbw_GBps": busbw(nccl_ms),
+            "timing": "device time (CUDA events), max over ranks; busbw = 2(N-1)/N * bytes / time"}

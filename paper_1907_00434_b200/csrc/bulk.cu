@@ -182,6 +182,14 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_bulk(const __grid_co
         const int c = tid + k * kConsumers;
         if (c * 4 < cnt) __stcs(reinterpret_cast<float4 *>(a.w + e0) + c, w[k]);
       }
+      // fused get: the new model tile goes straight to every destination (NVLink stores)
+      for (int b = 0; b < a.n_bcast; ++b) {
+#pragma unroll
+        for (int k = 0; k < kChunks; ++k) {
+          const int c = tid + k * kConsumers;
+          if (c * 4 < cnt) __stcs(reinterpret_cast<float4 *>(a.bcast[b] + e0) + c, w[k]);
+        }
+      }
     }
     // ragged tail (< 8 elements) on CTA 0
     const int64_t tail = a.n - n_bulk;
@@ -202,6 +210,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_bulk(const __grid_co
         }
       }
       a.w[e] = wv;
+      for (int b = 0; b < a.n_bcast; ++b) a.bcast[b][e] = wv;
     }
   }
 }

@@ -141,7 +141,7 @@ static int blocks_for(const void *fn, int sm_count, int threads) {
 }
 
 cudaError_t launch_commit(const CommitArgs &a, cudaStream_t s, int sm_count, CommitImpl impl) {
-  if (impl == CommitImpl::kBulk) return launch_commit_bulk(a, s, sm_count);
+  if (impl == CommitImpl::kBulk || a.n_bcast > 0) return launch_commit_bulk(a, s, sm_count);
   constexpr int kThreads = 256;
   constexpr int kU = 8;
   static int grid = 0;

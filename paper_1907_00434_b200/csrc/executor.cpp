@@ -66,6 +66,7 @@ struct mlf_ctx {
   std::vector<void *> slot;
   std::vector<int32_t> worker_rank, node_rank, worker_node;
   std::vector<float *> agg_scratch;
+  std::vector<float *> bcast;                     // fused-get destinations (full-length views)
   int sm_count = 148;
   int64_t version = 0;
   size_t elem_bytes = 4;
@@ -111,6 +112,12 @@ extern "C" mlf_status mlf_init(const mlf_config *cfg, int64_t v0, mlf_ctx **out)
     if (k.agg_slots < 0 || (k.agg_slots > 0 && !k.agg_scratch)) throw Fail{MLF_E_INVALID, "aggregate scratch"};
     if (!(k.gamma >= 0.f && k.gamma < 1.f)) throw Fail{MLF_E_INVALID, "gamma must be in [0, 1)"};
     if (k.replica_mode != 0 && k.replica_mode != 1) throw Fail{MLF_E_INVALID, "replica_mode"};
+    if (k.n_bcast < 0 || k.n_bcast > kMaxBcast || (k.n_bcast > 0 && !k.bcast))
+      throw Fail{MLF_E_INVALID, "fused get: 0..8 destinations"};
+    if (k.n_bcast > 0 && k.gamma != 0.f) throw Fail{MLF_E_INVALID, "fused get is implemented for gamma = 0"};
+    for (int i = 0; i < k.n_bcast; ++i)
+      if (!k.bcast[i] || (reinterpret_cast<uintptr_t>(k.bcast[i] + k.shard_begin) & 15))
+        throw Fail{MLF_E_INVALID, "fused get destination null or misaligned"};
     if (k.replica_mode == 1) {
       if (k.shard_elems > 0 && !k.backup_shard) throw Fail{MLF_E_INVALID, "replica trees need the replica shard"};
       if (k.gamma != 0.f) throw Fail{MLF_E_INVALID, "replica trees are implemented for gamma = 0"};
@@ -169,6 +176,7 @@ extern "C" mlf_status mlf_init(const mlf_config *cfg, int64_t v0, mlf_ctx **out)
       c->node_rank.push_back(r);
     }
     for (int i = 0; i < k.world * k.agg_slots; ++i) c->agg_scratch.push_back(k.agg_scratch[i]);
+    for (int i = 0; i < k.n_bcast; ++i) c->bcast.push_back(k.bcast[i]);
     if (k.replica_mode == 1) {
       for (int i = 0; i < k.world * k.n_retain; ++i) c->retain.push_back(k.retain_slot[i]);
       c->used.assign(k.world, std::vector<uint8_t>(k.n_retain, 0));
@@ -450,10 +458,12 @@ static void launch_momentum(mlf_ctx *c, const mlf_plan_out *p, const std::vector
 
 // The fused commit pass of `ops` (commit order) over w (this rank's slice, src_off =
 // shard_begin), launches split at commit boundaries when the list exceeds kMaxOps.
-static void launch_ops(mlf_ctx *c, float *w, float *backup, const std::vector<CommitOp> &ops, int boundary) {
+static void launch_ops(mlf_ctx *c, float *w, float *backup, const std::vector<CommitOp> &ops, int boundary,
+                       bool bcast = false) {
   size_t i0 = 0;
   bool first_launch = true;
-  while (i0 < ops.size() || (first_launch && c->cfg.shard_elems > 0 && (boundary == 0))) {
+  bcast = bcast && !c->bcast.empty();
+  while (i0 < ops.size() || (first_launch && c->cfg.shard_elems > 0 && (boundary == 0 || bcast))) {
     size_t i1 = std::min(ops.size(), i0 + (size_t)kMaxOps);
     if (i1 < ops.size())
       while (i1 > i0 && !(ops[i1 - 1].flag & kOpLast)) --i1;
@@ -467,6 +477,9 @@ static void launch_ops(mlf_ctx *c, float *w, float *backup, const std::vector<Co
     a.n_ops = (int32_t)(i1 - i0);
     a.backup_after = -2;
     if (first_launch && boundary == 0) a.backup_after = -1;
+    a.n_bcast = 0;
+    if (bcast && i1 == ops.size())                  // only the pass that finishes w broadcasts it
+      for (float *d : c->bcast) a.bcast[a.n_bcast++] = d + c->cfg.shard_begin;
     for (size_t q = i0; q < i1; ++q) {
       a.op[q - i0] = ops[q].ptr;
       a.flag[q - i0] = ops[q].flag;
@@ -563,7 +576,7 @@ static void phase_commit(mlf_ctx *c, const mlf_plan_out *p) {
   if (c->cfg.gamma != 0.f)
     launch_momentum(c, p, ops, boundary);
   else
-    launch_ops(c, c->cfg.model_shard, trees ? nullptr : c->cfg.backup_shard, ops, boundary);
+    launch_ops(c, c->cfg.model_shard, trees ? nullptr : c->cfg.backup_shard, ops, boundary, true);
   if (trees) replicate_trees(c, p);
   record_start(c);
   CK(cudaEventRecord(c->ev_stop, c->stream));

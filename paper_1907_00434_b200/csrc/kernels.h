@@ -9,6 +9,7 @@ namespace mlf {
 // Operands per fused-commit launch (kernel parameter space, CUDA >= 12.1 allows
 // 32 KB of parameters).  Longer commit lists are split at commit boundaries.
 constexpr int kMaxOps = 1024;
+constexpr int kMaxBcast = 8;
 
 // flag bits per operand
 constexpr uint8_t kOpFirst = 1;   // first member of its commit: x = u (not x += u)
@@ -26,6 +27,11 @@ struct CommitArgs {
   int32_t backup_after; // -2: no mirror store; -1: store the loaded w; k: store w after op k
   const void *op[kMaxOps];
   uint8_t flag[kMaxOps];
+  // fused get (bulk kernel only): the final w of every tile is also stored to these
+  // destinations (already offset to this shard; local or peer), i.e. the all-gather of the
+  // new model happens tile by tile inside the commit pass
+  int32_t n_bcast;
+  float *bcast[kMaxBcast];
 };
 
 // tree_reduce: out[i] = left fold of members, fp32 (an aggregator's sum).

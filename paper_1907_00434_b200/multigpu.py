@@ -81,7 +81,8 @@ class IpcMapper:
 class ShardedWorkload:
     """Rank `rank`'s part of a config sharded over `world` GPUs."""
 
-    def __init__(self, cfg: dict, rank: int, world: int, device: int, ctrl, mode: str = "fold", variant: int = 0):
+    def __init__(self, cfg: dict, rank: int, world: int, device: int, ctrl, mode: str = "fold", variant: int = 0,
+                 fused_get: bool = False):
         assert cfg["G"] == world, "config shard count must equal the world size"
         self.cfg, self.rank, self.world, self.ctrl, self.mode = cfg, rank, world, ctrl, mode
         dev = torch.device("cuda", device)
@@ -107,6 +108,8 @@ class ShardedWorkload:
             self.n_retain = cfg.get("n_retain", max(len(local), 1) * 2)
             self.retain = torch.empty((self.n_retain, -(-S // 64) * 64), dtype=tdt, device=dev)
         self.n_slots = agg_slots_needed(cfg, world) if mode == "tree" else 0
+        # fused get: every GPU holds a full-length view of the model, written by all shards' commits
+        self.view = torch.empty(-(-S // 64) * 64, dtype=torch.float32, device=dev) if fused_get else None
         self.scratch = (torch.empty((self.n_slots, self.row), dtype=torch.float32, device=dev)
                         if self.n_slots else None)
         torch.cuda.synchronize(dev)
@@ -116,7 +119,8 @@ class ShardedWorkload:
                 "mirror_h": (m.ipc_export(device, self.mirror_h.data_ptr())
                              if self.mirror_h is not None else None),
                 "scratch": m.ipc_export(device, self.scratch.data_ptr()) if self.scratch is not None else None,
-                "retain": m.ipc_export(device, self.retain.data_ptr()) if self.retain is not None else None}
+                "retain": m.ipc_export(device, self.retain.data_ptr()) if self.retain is not None else None,
+                "view": m.ipc_export(device, self.view.data_ptr()) if self.view is not None else None}
         allinfo = [None] * world
         dist.all_gather_object(allinfo, mine, group=ctrl)
         allinfo.sort(key=lambda d: d["rank"])
@@ -147,9 +151,14 @@ class ShardedWorkload:
             for info in allinfo:
                 base = self.retain.data_ptr() if info["rank"] == rank else self.mapper.open(info["retain"])
                 retain_tab += [base + s * rowb for s in range(self.n_retain)]
+        bcast = None
+        if self.view is not None:
+            bcast = [self.view.data_ptr() if info["rank"] == rank else self.mapper.open(info["view"])
+                     for info in allinfo]
         self.wl = Workload(cfg, device=device, rank=rank, world=world, variant=variant, peer_slots=peer_slots,
                            backup_ptr=backup_ptr, agg_slots=self.n_slots, agg_scratch=scratch_tab,
-                           slot_tensors=slot_tensors, backup_h_ptr=backup_h_ptr, retain_table=retain_tab)
+                           slot_tensors=slot_tensors, backup_h_ptr=backup_h_ptr, retain_table=retain_tab,
+                           bcast=bcast)
         ev = self.wl.ctx.phase_event()
         evs = [None] * world
         dist.all_gather_object(evs, (rank, ev), group=ctrl)

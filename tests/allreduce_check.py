@@ -36,11 +36,20 @@ def main():
     device = local % torch.cuda.device_count()
     torch.cuda.set_device(device)
     cfg = allreduce_config(a.S, world, workers=a.workers)
-    ar = MlfAllReduce(cfg, rank, world, device, ctrl)
     rng = np.random.default_rng(7)
     idx = np.unique(np.concatenate([rng.integers(0, cfg["S"], 8000), np.arange(cfg["S"] - 11, cfg["S"])]))
+    for fused in (True, False):
+        check(cfg, rank, world, device, ctrl, idx, a.steps, fused)
+    if rank == 0:
+        print(f"ALLREDUCE_OK world={world} S={cfg['S']} workers={cfg['W']}", flush=True)
+    dist.barrier(group=ctrl)
+    dist.destroy_process_group()
+
+
+def check(cfg, rank, world, device, ctrl, idx, steps, fused):
+    ar = MlfAllReduce(cfg, rank, world, device, ctrl, fused=fused)
     v = vp = 0
-    for it in range(a.steps):
+    for it in range(steps):
         ar.sw.fill(it)
         pd, _, _, _ = ar.run(it)
         up, down, site = configs.network(cfg, it)
@@ -54,13 +63,10 @@ def main():
         ref, _ = commit_batch(np.zeros(len(idx), np.float32),
                               commits_from_plan(op, lambda g: sg.update_values(cfg["seed"], g, it, idx)), -1.0)
         got = ar.out.cpu().numpy()[idx]
-        assert np.array_equal(got.view(np.uint32), ref.view(np.uint32)), f"rank {rank}: allreduce mismatch"
+        assert np.array_equal(got.view(np.uint32), ref.view(np.uint32)), \
+            f"rank {rank}: allreduce mismatch (fused={fused})"
         vp, v = v, v + 1
     ar.close()
-    if rank == 0:
-        print(f"ALLREDUCE_OK world={world} S={cfg['S']} workers={cfg['W']} groups={pd['n_groups']}", flush=True)
-    dist.barrier(group=ctrl)
-    dist.destroy_process_group()
 
 
 if __name__ == "__main__":
