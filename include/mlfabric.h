@@ -245,6 +245,13 @@ mlf_status mlf_submit_update(mlf_ctx *ctx, int32_t worker, int64_t version,
  * no bytes).  NULL unregisters. */
 mlf_status mlf_set_update_host(mlf_ctx *ctx, int32_t worker, const void *host_ptr);
 
+/* Optional: pinned host buffer (full model length, fp32) that every mlf_execute fills with
+ * this rank's shard of the new model (get), at dst + shard_begin.  With host-resident
+ * updates on one GPU, mlf_execute then runs as a pipeline over element chunks: the H2D copy
+ * of chunk k+1 of the committed updates, the commit of chunk k and the D2H copy of chunk
+ * k-1 overlap (copy engines in both directions + SMs).  NULL unregisters. */
+mlf_status mlf_set_pull_host(mlf_ctx *ctx, void *host_dst);
+
 /* Borrow the current batch as planner input (arrays valid until the next
  * submit/execute).  bytes = model_elems * sizeof(dtype), node = worker_node[worker]. */
 mlf_status mlf_batch_view(mlf_ctx *ctx, mlf_batch *out);

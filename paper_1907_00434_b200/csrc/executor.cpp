@@ -67,6 +67,9 @@ struct mlf_ctx {
   std::vector<int32_t> worker_rank, node_rank, worker_node;
   std::vector<float *> agg_scratch;
   std::vector<float *> bcast;                     // fused-get destinations (full-length views)
+  void *pull_host = nullptr;                      // e2e pipeline: D2H target of the new shard
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;  // copy streams of the e2e pipeline
+  std::vector<cudaEvent_t> pipe_ev;
   int sm_count = 148;
   int64_t version = 0;
   size_t elem_bytes = 4;
@@ -197,6 +200,8 @@ extern "C" mlf_status mlf_init(const mlf_config *cfg, int64_t v0, mlf_ctx **out)
       CK(cudaEventCreate(&c->ev_start));
       CK(cudaEventCreate(&c->ev_stop));
       if (k.world > 1) CK(cudaEventCreateWithFlags(&c->ev_phase, cudaEventInterprocess | cudaEventDisableTiming));
+      CK(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
     } catch (...) {
       delete c;
       throw;
@@ -211,6 +216,9 @@ extern "C" void mlf_destroy(mlf_ctx *c) {
   if (c->ev_stop) cudaEventDestroy(c->ev_stop);
   for (auto e : c->peer_events) cudaEventDestroy(e);
   if (c->ev_phase) cudaEventDestroy(c->ev_phase);
+  for (auto e : c->pipe_ev) cudaEventDestroy(e);
+  if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
+  if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
   delete c;
 }
 
@@ -244,6 +252,13 @@ extern "C" mlf_status mlf_submit_update(mlf_ctx *c, int32_t worker, int64_t vers
     c->b_version.push_back(version);
     c->b_tavail.push_back(t_avail_ns);
     c->b_norm.push_back(norm);
+  });
+}
+
+extern "C" mlf_status mlf_set_pull_host(mlf_ctx *c, void *host_dst) {
+  return guard([&] {
+    check_ctx(c);
+    c->pull_host = host_dst;
   });
 }
 
@@ -348,6 +363,7 @@ static void record_start(mlf_ctx *c) {
 }
 
 static void reduce_local_groups(mlf_ctx *c, const mlf_plan_out *p);
+static bool pipelined(const mlf_ctx *c, const mlf_plan_out *p);
 
 static void phase_stage(mlf_ctx *c, const mlf_plan_out *p) {
   CK(cudaSetDevice(c->cfg.device));
@@ -355,8 +371,9 @@ static void phase_stage(mlf_ctx *c, const mlf_plan_out *p) {
   if (c->cfg.world > 1) record_start(c);
   const size_t bytes = (size_t)c->cfg.model_elems * c->elem_bytes;
   // committed host-resident updates homed on this rank move host -> device;
-  // dropped ones never move ("dropped at the worker itself")
-  for (int i = 0; i < p->n_commit; ++i) {
+  // dropped ones never move ("dropped at the worker itself").
+  // (one GPU: the commit phase pipelines these copies chunk by chunk instead)
+  for (int i = 0; i < p->n_commit && !pipelined(c, p); ++i) {
     int w = c->b_worker[p->order[i]];
     if (c->host_src[w] && c->worker_rank[w] == c->cfg.rank) {
       record_start(c);
@@ -459,27 +476,28 @@ static void launch_momentum(mlf_ctx *c, const mlf_plan_out *p, const std::vector
 // The fused commit pass of `ops` (commit order) over w (this rank's slice, src_off =
 // shard_begin), launches split at commit boundaries when the list exceeds kMaxOps.
 static void launch_ops(mlf_ctx *c, float *w, float *backup, const std::vector<CommitOp> &ops, int boundary,
-                       bool bcast = false) {
+                       bool bcast = false, int64_t off = 0, int64_t len = -1) {
   size_t i0 = 0;
   bool first_launch = true;
   bcast = bcast && !c->bcast.empty();
-  while (i0 < ops.size() || (first_launch && c->cfg.shard_elems > 0 && (boundary == 0 || bcast))) {
+  if (len < 0) len = c->cfg.shard_elems;
+  while (i0 < ops.size() || (first_launch && len > 0 && (boundary == 0 || bcast))) {
     size_t i1 = std::min(ops.size(), i0 + (size_t)kMaxOps);
     if (i1 < ops.size())
       while (i1 > i0 && !(ops[i1 - 1].flag & kOpLast)) --i1;
     if (i1 == i0 && i0 < ops.size()) throw Fail{MLF_E_CAPACITY, "a single commit has more than kMaxOps members"};
     CommitArgs a;
-    a.w = w;
-    a.backup = backup;
-    a.n = c->cfg.shard_elems;
-    a.src_off = c->cfg.shard_begin;
+    a.w = w + off;
+    a.backup = backup ? backup + off : nullptr;
+    a.n = len;
+    a.src_off = c->cfg.shard_begin + off;
     a.lr = c->cfg.lr;
     a.n_ops = (int32_t)(i1 - i0);
     a.backup_after = -2;
     if (first_launch && boundary == 0) a.backup_after = -1;
     a.n_bcast = 0;
     if (bcast && i1 == ops.size())                  // only the pass that finishes w broadcasts it
-      for (float *d : c->bcast) a.bcast[a.n_bcast++] = d + c->cfg.shard_begin;
+      for (float *d : c->bcast) a.bcast[a.n_bcast++] = d + c->cfg.shard_begin + off;
     for (size_t q = i0; q < i1; ++q) {
       a.op[q - i0] = ops[q].ptr;
       a.flag[q - i0] = ops[q].flag;
@@ -494,6 +512,90 @@ static void launch_ops(mlf_ctx *c, float *w, float *backup, const std::vector<Co
     i0 = i1;
     if (ops.empty()) break;
   }
+}
+
+// End-to-end pipeline (one GPU, host-resident updates and/or a host pull target): element
+// chunks flow H2D (copy stream) -> fused commit (compute stream) -> D2H (copy stream), so
+// the H2D of chunk k+1, the commit of chunk k and the D2H of chunk k-1 overlap.
+static constexpr int64_t kPipeChunk = 1 << 22;     // elements per chunk (16 MB of fp32)
+
+static bool pipelined(const mlf_ctx *c, const mlf_plan_out *p) {
+  if (c->cfg.world != 1 || c->cfg.gamma != 0.f || c->cfg.replica_mode != 0 || !c->bcast.empty()) return false;
+  if (c->pull_host) return true;
+  for (int i = 0; i < p->n_commit; ++i)
+    if (c->host_src[c->b_worker[p->order[i]]]) return true;
+  return false;
+}
+
+static cudaEvent_t pipe_event(mlf_ctx *c, size_t i) {
+  while (c->pipe_ev.size() <= i) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->pipe_ev.push_back(e);
+  }
+  return c->pipe_ev[i];
+}
+
+static void pipeline_commit(mlf_ctx *c, const mlf_plan_out *p, const std::vector<CommitOp> &ops, int boundary) {
+  if (ops.size() > (size_t)kMaxOps) {              // long lists: the plain (non-overlapped) path
+    for (int i = 0; i < p->n_commit; ++i) {
+      const int w = c->b_worker[p->order[i]];
+      if (c->host_src[w]) {
+        record_start(c);
+        CK(cudaMemcpyAsync(c->slot[w], c->host_src[w], (size_t)c->cfg.model_elems * c->elem_bytes,
+                           cudaMemcpyHostToDevice, c->stream));
+        c->h2d += (int64_t)c->cfg.model_elems * c->elem_bytes;
+      }
+    }
+    launch_ops(c, c->cfg.model_shard, c->cfg.backup_shard, ops, boundary);
+    if (c->pull_host) {
+      CK(cudaMemcpyAsync(static_cast<char *>(c->pull_host) + (size_t)c->cfg.shard_begin * 4, c->cfg.model_shard,
+                         (size_t)c->cfg.shard_elems * 4, cudaMemcpyDeviceToHost, c->stream));
+      c->d2h += c->cfg.shard_elems * 4;
+    }
+    return;
+  }
+  record_start(c);
+  size_t ev = 0;
+  const cudaEvent_t begin = pipe_event(c, ev++);
+  CK(cudaEventRecord(begin, c->stream));            // slots / w are free once earlier work is done
+  CK(cudaStreamWaitEvent(c->s_h2d, begin, 0));
+  CK(cudaStreamWaitEvent(c->s_d2h, begin, 0));
+  std::vector<int> host_w;
+  for (int i = 0; i < p->n_commit; ++i) {
+    const int w = c->b_worker[p->order[i]];
+    if (c->host_src[w]) host_w.push_back(w);
+  }
+  const int64_t n = c->cfg.shard_elems, e = (int64_t)c->elem_bytes;
+  for (int64_t off = 0; off < n || (off == 0 && n == 0); off += kPipeChunk) {
+    const int64_t len = std::min(kPipeChunk, n - off);
+    for (int w : host_w) {
+      const int64_t src = c->cfg.shard_begin + off;
+      CK(cudaMemcpyAsync(static_cast<char *>(c->slot[w]) + src * e, static_cast<const char *>(c->host_src[w]) + src * e,
+                         (size_t)(len * e), cudaMemcpyHostToDevice, c->s_h2d));
+      c->h2d += len * e;
+    }
+    const cudaEvent_t in = pipe_event(c, ev++);
+    CK(cudaEventRecord(in, c->s_h2d));
+    CK(cudaStreamWaitEvent(c->stream, in, 0));
+    // the mirror-at-pre-batch store (boundary 0) belongs to every chunk, so pass it through
+    launch_ops(c, c->cfg.model_shard, c->cfg.backup_shard, ops, boundary, false, off, len);
+    if (c->pull_host && len > 0) {
+      const cudaEvent_t done = pipe_event(c, ev++);
+      CK(cudaEventRecord(done, c->stream));
+      CK(cudaStreamWaitEvent(c->s_d2h, done, 0));
+      CK(cudaMemcpyAsync(static_cast<char *>(c->pull_host) + (size_t)(c->cfg.shard_begin + off) * 4,
+                         c->cfg.model_shard + off, (size_t)len * 4, cudaMemcpyDeviceToHost, c->s_d2h));
+      c->d2h += len * 4;
+    }
+    if (n == 0) break;
+  }
+  // the batch ends when the last D2H (and every H2D) has landed
+  const cudaEvent_t fin_h = pipe_event(c, ev++), fin_d = pipe_event(c, ev++);
+  CK(cudaEventRecord(fin_h, c->s_h2d));
+  CK(cudaEventRecord(fin_d, c->s_d2h));
+  CK(cudaStreamWaitEvent(c->stream, fin_h, 0));
+  CK(cudaStreamWaitEvent(c->stream, fin_d, 0));
 }
 
 // Replica trees (NEXT-2): apply the frozen replica commits (the replica's own Alg. 3
@@ -575,6 +677,8 @@ static void phase_commit(mlf_ctx *c, const mlf_plan_out *p) {
   const int boundary = (c->cfg.backup_shard && !trees) ? p->replica_boundary_commit : -1;
   if (c->cfg.gamma != 0.f)
     launch_momentum(c, p, ops, boundary);
+  else if (pipelined(c, p))
+    pipeline_commit(c, p, ops, boundary);
   else
     launch_ops(c, c->cfg.model_shard, trees ? nullptr : c->cfg.backup_shard, ops, boundary, true);
   if (trees) replicate_trees(c, p);

@@ -21,7 +21,8 @@ MLF_PHASE_AGGREGATE, MLF_PHASE_COMMIT = 1, 2
 
 # every symbol include/mlfabric.h declares
 EXPORTS = (
-    "mlf_plan", "mlf_init", "mlf_submit_update", "mlf_set_update_host", "mlf_batch_view", "mlf_version",
+    "mlf_plan", "mlf_init", "mlf_submit_update", "mlf_set_update_host", "mlf_set_pull_host", "mlf_batch_view",
+    "mlf_version",
     "mlf_execute", "mlf_execute_phase", "mlf_sync", "mlf_pull_model", "mlf_stats", "mlf_destroy",
     "mlf_last_error", "mlf_ipc_export", "mlf_ipc_open", "mlf_ipc_close", "mlf_phase_event_export",
     "mlf_phase_events_open", "mlf_gather", "mlf_synth_fill", "mlf_copy_kernel", "mlf_copy_engine",
@@ -100,6 +101,7 @@ _lib.mlf_plan.argtypes = [C.POINTER(MlfNet), C.POINTER(MlfBatch), C.POINTER(MlfP
 _lib.mlf_init.argtypes = [C.POINTER(MlfConfig), C.c_int64, C.POINTER(_p)]
 _lib.mlf_submit_update.argtypes = [_p, C.c_int32, C.c_int64, C.c_int64, C.c_double, _i32p]
 _lib.mlf_set_update_host.argtypes = [_p, C.c_int32, _p]
+_lib.mlf_set_pull_host.argtypes = [_p, _p]
 _lib.mlf_batch_view.argtypes = [_p, C.POINTER(MlfBatch)]
 _lib.mlf_version.argtypes = [_p, _i64p]
 _lib.mlf_execute.argtypes = [_p, C.POINTER(MlfPlanOut)]
@@ -321,6 +323,10 @@ class Context:
 
     def set_update_host(self, worker: int, host_ptr: int | None):
         _check(_lib.mlf_set_update_host(self._h, worker, host_ptr))
+
+    def set_pull_host(self, host_ptr: int | None):
+        """Every execute also delivers this rank's new shard to host_ptr + shard_begin (pinned)."""
+        _check(_lib.mlf_set_pull_host(self._h, host_ptr))
 
     def batch_view(self) -> MlfBatch:
         b = MlfBatch()

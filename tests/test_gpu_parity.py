@@ -192,6 +192,40 @@ def test_host_resident_updates_move_only_when_committed():
     assert stats[1] == 4 * S * 4                             # h2d bytes: committed updates only
 
 
+@pytest.mark.parametrize("S", [9_000_011, 4 << 22, 1000])
+def test_e2e_pipeline_h2d_commit_d2h(S):
+    """mlf_set_pull_host: chunked H2D / commit / D2H overlap inside mlf_execute (incl. a ragged
+    last chunk, an exact multiple of the chunk size and a single small chunk), with a mirror."""
+    rng = np.random.default_rng(S % 97)
+    W = 6
+    p = random_plan(rng, W, n_commit=5, boundary=2)
+    dev = torch.device("cuda", 0)
+    slots = [torch.empty(S, device=dev) for _ in range(W)]
+    hosts = []
+    for w, t in enumerate(slots):
+        m.synth_fill(0, t.data_ptr(), S, seed=SEED, kind=1, a=w, b=0)
+        hosts.append(t.cpu().pin_memory())
+        t.zero_()
+    wt = torch.empty(S, device=dev)
+    m.synth_fill(0, wt.data_ptr(), S, seed=SEED, kind=2)
+    bk = torch.full((S,), float("nan"), device=dev)
+    pulled = torch.full((S,), float("nan")).pin_memory()
+    ctx = m.Context(device=0, model_shard=wt, update_slots=slots, lr=0.01, model_elems=S, backup_shard=bk,
+                    stream=torch.cuda.current_stream().cuda_stream)
+    ctx.set_pull_host(pulled.data_ptr())
+    for w in range(W):
+        ctx.submit(w, 0)
+        ctx.set_update_host(w, hosts[w].data_ptr())
+    ctx.execute(m.plan_from_dict(p))
+    ctx.sync()
+    wr, br = oracle_run(S, sg.DTYPE_F32, p)
+    assert np.array_equal(bits(pulled.numpy()), bits(wr))
+    assert np.array_equal(bits(wt.cpu().numpy()), bits(wr)) and np.array_equal(bits(bk.cpu().numpy()), bits(br))
+    _, h2d, d2h = ctx.stats()
+    assert h2d == 5 * S * 4 and d2h == S * 4
+    ctx.close()
+
+
 def test_invalid_plan_rejected_without_device_work():
     dev = torch.device("cuda", 0)
     S = 64
