@@ -420,13 +420,22 @@ static cudaError_t launch_tile(const CommitArgs &a, cudaStream_t s, int sm_count
 // HBM copy roofline at config 2, tau 4, vs 93.5% at 2048 and 8192); NVLink-bound runs
 // are insensitive to the tile size.
 cudaError_t launch_commit_bulk(const CommitArgs &a, cudaStream_t s, int sm_count) {
-  static int tile = 0;
-  if (tile == 0) {
+  static int forced = -1;
+  if (forced < 0) {
     const char *e = getenv("MLF_BULK_TILE");
-    tile = e ? atoi(e) : 4096;
+    forced = e ? atoi(e) : 0;
+  }
+  // adaptive tile: the largest of 4096 / 2048 / 1024 elements that still deals >= 32 tiles to
+  // every persistent CTA, so the last wave's imbalance stays small (a shard of 6.4M elements,
+  // config 4 at 4 GPUs: 76.8% of the NVLink roofline at 2048 vs 70.8% at 4096)
+  int tile = forced;
+  if (tile == 0) {
+    const int64_t per_cta = (a.n / 4096) / (sm_count > 0 ? sm_count : 148);
+    tile = per_cta >= 32 ? 4096 : ((a.n / 2048) / (sm_count > 0 ? sm_count : 148) >= 32 ? 2048 : 1024);
   }
   if (tile == 8192) return launch_tile<8192, 6>(a, s, sm_count);
   if (tile == 2048) return launch_tile<2048, 24>(a, s, sm_count);
+  if (tile == 1024) return launch_tile<1024, 48>(a, s, sm_count);
   return launch_tile<4096, 12>(a, s, sm_count);
 }
 
