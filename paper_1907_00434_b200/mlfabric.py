@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libmlfabric.so")
+LIB_PATH = os.environ.get("MLF_LIB") or os.path.join(_HERE, "lib", "libmlfabric.so")
 
 MLF_OK, MLF_E_INVALID, MLF_E_STATE, MLF_E_CUDA, MLF_E_UNSCHEDULABLE, MLF_E_CAPACITY = range(6)
 MLF_F32, MLF_BF16 = 0, 1
