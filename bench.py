@@ -195,6 +195,7 @@ def cpu_baseline_oracle(cfg, dt, budget_s=15.0):
         v_prev, v_init = v_init, v_init + p["n_commit"]
         it += 1
     out = {"value": round(tot_b / tot_s / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+           "cpu": cpu_model(), "host_cores": os.cpu_count(),
            "sample": f"{it} batches of config{cfg['cid']}: full oracle plan + numpy numerics on the first "
                      f"{S_sample} of {cfg['S']} elements of every update (single-threaded numpy)"}
     try:
@@ -202,6 +203,16 @@ def cpu_baseline_oracle(cfg, dt, budget_s=15.0):
     except Exception as e:  # the single-core figure above is the reported baseline
         out["all_cores"] = {"error": str(e)[:200]}
     return out
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def _oracle_slice(args):
@@ -325,9 +336,11 @@ def run_single(a):
                    "l2": "flushed before every step (256 MiB write + 256 MiB read); operands >> L2"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
+                     "frac_of_8TBps_spec": round(achieved / 8000.0, 4),
                      "kernel": f"fused_commit_{a.kernel}",
                      "algorithmic_bytes_per_step": int(alg / len(recs))},
         "planner_ms": round(sum(r["plan_ms"] for r in recs) / len(recs), 3),
+        "step_ms_p10_p50_p90": [round(float(x), 4) for x in np.percentile([r["ms"] for r in recs], [10, 50, 90])],
         "gpu_launches": int(kl),
         "clocks": ck.summary(),
     }
