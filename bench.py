@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--config", type=int, default=None)
     ap.add_argument("--tau", type=int, default=None)
     ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
+    ap.add_argument("--gamma", type=float, default=0.0, help="momentum (NEXT-1); 0 = the north-star form")
     ap.add_argument("--no-variants", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -312,7 +313,7 @@ def run_single(a):
 
     # warm-up + timed region (barrier + synchronize on both sides: single process)
     torch.cuda.synchronize()
-    cfg, recs, T, ck, kl = measure(a.tau, a.dtype, a.steps, a.warmup, a.kernel, clocks=True)
+    cfg, recs, T, ck, kl = measure(a.tau, a.dtype, a.steps, a.warmup, a.kernel, clocks=True, gamma=a.gamma)
     torch.cuda.synchronize()
     tot_bytes = sum(r["bytes"] for r in recs)
     value = tot_bytes / (T / 1e3) / 1e9
@@ -337,7 +338,7 @@ def run_single(a):
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
                      "frac_of_8TBps_spec": round(achieved / 8000.0, 4),
-                     "kernel": f"fused_commit_{a.kernel}",
+                     "kernel": "fused_commit_momentum" if a.gamma else f"fused_commit_{a.kernel}",
                      "algorithmic_bytes_per_step": int(alg / len(recs))},
         "planner_ms": round(sum(r["plan_ms"] for r in recs) / len(recs), 3),
         "step_ms_p10_p50_p90": [round(float(x), 4) for x in np.percentile([r["ms"] for r in recs], [10, 50, 90])],
