@@ -41,6 +41,7 @@ def main():
     ap.add_argument("--replica-mode", type=int, default=0)
     ap.add_argument("--div-max", type=float, default=None)
     ap.add_argument("--workers", type=int, default=None)
+    ap.add_argument("--host", action="store_true", help="host-resident updates (the e2e path)")
     a = ap.parse_args()
     os.environ["MLF_COMMIT_IMPL"] = a.kernel
     rank, world, local, ctrl = init_dist()
@@ -66,6 +67,17 @@ def main():
         v_init = v_prev = 0
         for it in range(a.steps):
             sw.fill(it)
+            if a.host:
+                # e2e path: the updates live in pinned host memory; every rank stages its own
+                # committed ones in phase 1, peers read them in phase 2
+                hosts = {}
+                for w, t in sw.wl.slots.items():
+                    hosts[w] = t.cpu().pin_memory()
+                    sw.wl.ctx.set_update_host(w, hosts[w].data_ptr())
+                sw.slots_all.zero_()
+                torch.cuda.synchronize()
+                sw.two_phase = True
+                sw.barrier()
             pd, ms = sw.step(it)
             # oracle: same planner inputs
             up, down, site = configs.network(cfg, it)

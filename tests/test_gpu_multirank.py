@@ -42,6 +42,12 @@ def test_two_ranks_replica_trees_with_retention():
     assert "punted_total=0" not in out
 
 
+def test_two_ranks_host_resident_updates():
+    # the e2e path: each rank stages its committed host-resident updates (phase 1), peers read them
+    out = _run(2, "--cid", "3", "--S", "400009", "--steps", "2", "--host")
+    assert "MULTIGPU_OK fold" in out and "MULTIGPU_OK tree" in out
+
+
 def test_two_ranks_allreduce_push_get():
     cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", "--nnodes=1", "--nproc-per-node=2",
            os.path.join(HERE, "allreduce_check.py"), "--S", "500009", "--workers", "8"]
