@@ -705,6 +705,18 @@ extern "C" mlf_status mlf_execute_phase(mlf_ctx *c, const mlf_plan_out *p, int32
   mlf_status st = guard([&] {
     check_ctx(c);
     validate_plan(c, p);
+    if ((phase & MLF_PHASE_AGGREGATE) && (phase & MLF_PHASE_COMMIT) && c->cfg.world > 1) {
+      // one call for both phases gives the peers no point to order against: their phase 2
+      // could read our aggregates / staged updates before they exist
+      bool staged = false;
+      for (int i = 0; i < p->n_commit && !staged; ++i) {
+        const int w = c->b_worker[p->order[i]];
+        staged = c->host_src[w] && c->worker_rank[w] == c->cfg.rank;
+      }
+      if (tree_mode(c) || staged)
+        throw Fail{MLF_E_STATE, "tree mode / host-resident updates with world > 1 need two-phase execution "
+                                "(phase 1, a barrier across ranks, phase 2)"};
+    }
     if (phase & MLF_PHASE_AGGREGATE) {
       if (c->phase1_done) throw Fail{MLF_E_STATE, "phase 1 already ran for this batch"};
       phase_stage(c, p);
