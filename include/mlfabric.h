@@ -345,6 +345,8 @@ mlf_status mlf_synth_fill(int32_t device, void *dst, int64_t n, int64_t elem_off
 mlf_status mlf_copy_kernel(int32_t device, void *dst, const void *src, int64_t bytes, void *stream);
 /* The same copy on a copy engine (cudaMemcpyAsync device-to-device; peer pointers allowed). */
 mlf_status mlf_copy_engine(int32_t device, void *dst, const void *src, int64_t bytes, void *stream);
+/* The same copy with TMA bulk copies only (global -> shared -> global, 16 KB chunks). */
+mlf_status mlf_copy_bulk(int32_t device, void *dst, const void *src, int64_t bytes, void *stream);
 
 #ifdef __cplusplus
 }

@@ -913,6 +913,17 @@ extern "C" mlf_status mlf_gather(int32_t device, float *dst, int32_t n, const fl
   });
 }
 
+extern "C" mlf_status mlf_copy_bulk(int32_t device, void *dst, const void *src, int64_t bytes, void *stream) {
+  return guard([&] {
+    if (bytes % 16 != 0 || ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15))
+      throw Fail{MLF_E_INVALID, "bulk copy needs 16-byte aligned pointers and sizes"};
+    CK(cudaSetDevice(device));
+    int sm = 148;
+    CK(cudaDeviceGetAttribute(&sm, cudaDevAttrMultiProcessorCount, device));
+    CK(launch_bulk_copy(dst, src, bytes, static_cast<cudaStream_t>(stream), sm));
+  });
+}
+
 extern "C" mlf_status mlf_copy_engine(int32_t device, void *dst, const void *src, int64_t bytes, void *stream) {
   return guard([&] {
     if (bytes < 0 || (!dst && bytes) || (!src && bytes)) throw Fail{MLF_E_INVALID, "copy arguments"};

@@ -90,6 +90,73 @@ __global__ void __launch_bounds__(256) gather_kernel(const __grid_constant__ Gat
   }
 }
 
+// Copy with TMA bulk copies only (denominator probe): one elected thread per CTA moves 16 KB
+// chunks global -> shared (cp.async.bulk ... mbarrier::complete_tx) -> global (bulk store),
+// kStages chunks in flight per SM.  Used to measure what TMA-driven peer reads can reach.
+namespace bulkcopy {
+constexpr int kChunk = 16384, kStages = 12;
+__device__ __forceinline__ uint32_t saddr(const void *p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+}  // namespace bulkcopy
+
+__global__ void __launch_bounds__(32, 1) bulk_copy_kernel(char *dst, const char *src, int64_t bytes) {
+  using namespace bulkcopy;
+  extern __shared__ __align__(128) uint8_t sm[];
+  uint64_t *full = reinterpret_cast<uint64_t *>(sm + (size_t)kStages * kChunk);
+  if (threadIdx.x != 0) return;
+  for (int s = 0; s < kStages; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(saddr(&full[s])));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  const int64_t n_chunks = (bytes + kChunk - 1) / kChunk;
+  // issue loads for up to kStages chunks, then per chunk: wait load, store it, refill the stage
+  int64_t c_load = blockIdx.x, c_store = blockIdx.x;
+  uint32_t L = 0, S = 0;
+  auto issue_load = [&](int64_t c, uint32_t stage) {
+    const uint32_t len = (uint32_t)((bytes - c * kChunk) < kChunk ? (bytes - c * kChunk) : kChunk);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(&full[stage])), "r"(len)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     saddr(sm + (size_t)stage * kChunk)),
+                 "l"(src + c * kChunk), "r"(len), "r"(saddr(&full[stage]))
+                 : "memory");
+  };
+  for (; L < (uint32_t)kStages && c_load < n_chunks; ++L, c_load += gridDim.x) issue_load(c_load, L);
+  for (; c_store < n_chunks; c_store += gridDim.x, ++S) {
+    const uint32_t stage = S % kStages, parity = (S / kStages) & 1;
+    asm volatile(
+        "{\n\t.reg .pred p;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W_%=;\n}" ::"r"(
+            saddr(&full[stage])),
+        "r"(parity)
+        : "memory");
+    const uint32_t len =
+        (uint32_t)((bytes - c_store * kChunk) < kChunk ? (bytes - c_store * kChunk) : kChunk);
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + c_store * kChunk),
+                 "r"(saddr(sm + (size_t)stage * kChunk)), "r"(len)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    if (c_load < n_chunks) {
+      // the stage is refilled only after its bulk store has read it
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      issue_load(c_load, stage);
+      c_load += gridDim.x;
+      ++L;
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+cudaError_t launch_bulk_copy(void *dst, const void *src, int64_t bytes, cudaStream_t s, int sm_count) {
+  using namespace bulkcopy;
+  if (bytes <= 0) return cudaSuccess;
+  const size_t smem = (size_t)kStages * kChunk + kStages * sizeof(uint64_t);
+  static bool init = false;
+  if (!init) {
+    cudaError_t e = cudaFuncSetAttribute(bulk_copy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    init = true;
+  }
+  bulk_copy_kernel<<<sm_count, 32, smem, s>>>(static_cast<char *>(dst), static_cast<const char *>(src), bytes);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_gather(const GatherArgs &a, cudaStream_t s, int sm_count) {
   if (a.total_v <= 0) return cudaSuccess;
   gather_kernel<<<sm_count * 8, 256, 0, s>>>(a);

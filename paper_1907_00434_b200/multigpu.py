@@ -268,7 +268,8 @@ def measure_nvlink(device: int, rank: int, world: int, ctrl, nbytes: int = 1 << 
     mp = IpcMapper(device)
     peer = mp.open(blobs[(rank + 1) % world])
     out = {}
-    for name, fn in (("sm_peer_loads", m.copy_kernel), ("copy_engine", m.copy_engine)):
+    for name, fn in (("sm_peer_loads", m.copy_kernel), ("copy_engine", m.copy_engine),
+                     ("tma_bulk", m.copy_bulk)):
         best = 0.0
         for _ in range(4):
             dist.barrier(group=ctrl)
@@ -340,7 +341,7 @@ def run_bench_multi(a):
     nv_meas = measure_nvlink(local, rank, world, ctrl)
     # denominator: the best of this run's two measurements and the pool's measured peer copy
     # (770 GB/s per direction, B200_PROFILING.md) — never the slower of them
-    b_nv = max(NV_GUIDE_GBPS, nv_meas["copy_engine"], nv_meas["sm_peer_loads"])
+    b_nv = max(NV_GUIDE_GBPS, nv_meas["copy_engine"], nv_meas["sm_peer_loads"], nv_meas["tma_bulk"])
     flush_w = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     flush_r = torch.ones(64 << 20, dtype=torch.float32, device=dev)
 

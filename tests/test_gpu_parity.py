@@ -226,6 +226,18 @@ def test_e2e_pipeline_h2d_commit_d2h(S):
     ctx.close()
 
 
+@pytest.mark.parametrize("nbytes", [16, 16384, 16400, 5 * 16384 + 48, 200_000_016])
+def test_denominator_copy_kernels(nbytes):
+    # the roofline denominators are measured with these kernels: they must copy exactly
+    dev = torch.device("cuda", 0)
+    src = torch.randint(0, 255, (nbytes,), dtype=torch.uint8, device=dev)
+    for fn in (m.copy_kernel, m.copy_bulk, m.copy_engine):
+        dst = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+        fn(0, dst.data_ptr(), src.data_ptr(), nbytes, torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        assert torch.equal(dst, src), fn.__name__
+
+
 def test_invalid_plan_rejected_without_device_work():
     dev = torch.device("cuda", 0)
     S = 64
