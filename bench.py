@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--tau", type=int, default=None)
     ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
     ap.add_argument("--gamma", type=float, default=0.0, help="momentum (NEXT-1); 0 = the north-star form")
+    ap.add_argument("--mode", default="fold", choices=["fold", "staged", "tree"],
+                    help="N > 1 transport: fold (SM peer loads), staged (copy-engine staging), tree")
     ap.add_argument("--no-variants", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")

@@ -223,6 +223,12 @@ typedef struct {
    * (P:1297-1308).  gamma = 0 only; at most 8 destinations. */
   int32_t n_bcast;
   float *const *bcast;
+  /* Copy-engine staging (world > 1, fold mode, gamma = 0): operand slices homed on other
+   * GPUs are pulled over NVLink by the copy engines into this local buffer, chunk by chunk
+   * and double-buffered, while the commit kernel folds the previous chunk from local HBM
+   * (copy engines reach a higher NVLink rate than SM peer reads).  NULL / 0 = SM peer reads. */
+  void *stage_buf;
+  int64_t stage_bytes;
 } mlf_config;
 
 typedef struct mlf_ctx mlf_ctx;

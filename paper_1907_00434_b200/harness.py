@@ -22,7 +22,8 @@ class Workload:
 
     def __init__(self, cfg: dict, *, device: int = 0, rank: int = 0, world: int = 1, variant: int = 0,
                  peer_slots=None, backup_ptr=None, agg_slots: int = 0, agg_scratch=None, stream=None,
-                 slot_tensors: dict | None = None, backup_h_ptr=None, retain_table=None, bcast=None):
+                 slot_tensors: dict | None = None, backup_h_ptr=None, retain_table=None, bcast=None,
+                 stage=None):
         self.cfg = cfg
         self.device, self.rank, self.world = device, rank, world
         self.variant = variant
@@ -72,7 +73,8 @@ class Workload:
                              stream=self.stream.cuda_stream, v0=0, worker_node=cfg["worker_node"],
                              gamma=self.gamma, history=self.h,
                              backup_history=(backup_h_ptr if backup_h_ptr is not None else self.backup_h),
-                             replica_mode=self.replica_mode, retain_slots=retain_table, bcast=bcast)
+                             replica_mode=self.replica_mode, retain_slots=retain_table, bcast=bcast,
+                             stage=stage)
         self.v_init, self.v_prev = 0, 0
         self.iteration = 0
         self.carried = []

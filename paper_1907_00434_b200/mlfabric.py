@@ -86,7 +86,8 @@ class MlfConfig(C.Structure):
                 ("worker_node", _i32p), ("agg_slots", C.c_int32), ("agg_scratch", C.POINTER(_p)),
                 ("stream", _p), ("gamma", C.c_float), ("history_shard", _p), ("backup_history", _p),
                 ("replica_mode", C.c_int32), ("n_retain", C.c_int32), ("retain_slot", C.POINTER(_p)),
-                ("n_bcast", C.c_int32), ("bcast", C.POINTER(_p))]
+                ("n_bcast", C.c_int32), ("bcast", C.POINTER(_p)),
+                ("stage_buf", _p), ("stage_bytes", C.c_int64)]
 
 
 class MlfIpcHandle(C.Structure):
@@ -276,7 +277,8 @@ class Context:
                  shard_begin: int = 0, rank: int = 0, world: int = 1, dtype: int = MLF_F32,
                  backup_shard=None, worker_rank=None, node_rank=None, n_nodes=None, agg_slots: int = 0,
                  agg_scratch=None, stream=None, v0: int = 0, worker_node=None, gamma: float = 0.0,
-                 history=None, backup_history=None, replica_mode: int = 0, retain_slots=None, bcast=None):
+                 history=None, backup_history=None, replica_mode: int = 0, retain_slots=None, bcast=None,
+                 stage=None):
         """update_slots: list of int device pointers (or torch tensors); model_shard/backup_shard:
         torch tensors or int pointers; stream: int cudaStream_t (None -> default stream)."""
         def ptr(x):
@@ -307,6 +309,9 @@ class Context:
         if bc:
             self.cfg.n_bcast = len(bc)
             self.cfg.bcast = self._bc
+        if stage is not None:                       # copy-engine staging buffer (torch tensor)
+            self.cfg.stage_buf = ptr(stage)
+            self.cfg.stage_bytes = stage.numel() * stage.element_size()
         self._h = _p()
         _check(_lib.mlf_init(C.byref(self.cfg), int(v0), C.byref(self._h)))
         self._bufs = None

@@ -82,7 +82,10 @@ class ShardedWorkload:
     """Rank `rank`'s part of a config sharded over `world` GPUs."""
 
     def __init__(self, cfg: dict, rank: int, world: int, device: int, ctrl, mode: str = "fold", variant: int = 0,
-                 fused_get: bool = False):
+                 fused_get: bool = False, stage_mib: int = 0):
+        """mode: "fold" (SM peer loads inside the commit kernel), "tree" (tree_reduce on the
+        aggregator GPU first) or "staged" (fold whose remote operand slices are pulled by the
+        copy engines into a local staging buffer of stage_mib MiB, default 4096)."""
         assert cfg["G"] == world, "config shard count must equal the world size"
         self.cfg, self.rank, self.world, self.ctrl, self.mode = cfg, rank, world, ctrl, mode
         dev = torch.device("cuda", device)
@@ -108,6 +111,8 @@ class ShardedWorkload:
             self.n_retain = cfg.get("n_retain", max(len(local), 1) * 2)
             self.retain = torch.empty((self.n_retain, -(-S // 64) * 64), dtype=tdt, device=dev)
         self.n_slots = agg_slots_needed(cfg, world) if mode == "tree" else 0
+        self.stage = (torch.empty((stage_mib or 4096) << 18, dtype=torch.float32, device=dev)
+                      if mode == "staged" else None)
         # fused get: every GPU holds a full-length view of the model, written by all shards' commits
         self.view = torch.empty(-(-S // 64) * 64, dtype=torch.float32, device=dev) if fused_get else None
         self.scratch = (torch.empty((self.n_slots, self.row), dtype=torch.float32, device=dev)
@@ -158,7 +163,7 @@ class ShardedWorkload:
         self.wl = Workload(cfg, device=device, rank=rank, world=world, variant=variant, peer_slots=peer_slots,
                            backup_ptr=backup_ptr, agg_slots=self.n_slots, agg_scratch=scratch_tab,
                            slot_tensors=slot_tensors, backup_h_ptr=backup_h_ptr, retain_table=retain_tab,
-                           bcast=bcast)
+                           bcast=bcast, stage=self.stage)
         ev = self.wl.ctx.phase_event()
         evs = [None] * world
         dist.all_gather_object(evs, (rank, ev), group=ctrl)
@@ -377,7 +382,7 @@ def run_bench_multi(a):
 
     torch.cuda.synchronize()
     dist.barrier(group=ctrl)
-    modes = ["fold", "tree"] if not a.no_variants else ["fold"]
+    modes = [a.mode] + ([x for x in ("fold", "staged", "tree") if x != a.mode] if not a.no_variants else [])
     results = {}
     for i, mode in enumerate(modes):
         results[mode] = run(mode, a.steps if i == 0 else max(3, a.steps // 2), a.warmup if i == 0 else 2,
@@ -414,7 +419,10 @@ def run_bench_multi(a):
                    "committed_per_step": round(sum(r["commits"] for r in recs) / len(recs), 2),
                    "groups_per_step": round(sum(r["groups"] for r in recs) / len(recs), 2),
                    "l2": "flushed before every step (256 MiB write + 256 MiB read); operands >> L2",
-                   "parallelism": f"ps-shards{world} (one process per GPU, NVLink peer loads)"},
+                   "parallelism": f"ps-shards{world} (one process per GPU, " + {
+                       "fold": "NVLink peer loads in the commit kernel)",
+                       "staged": "copy-engine NVLink pulls into local staging + commit kernel)",
+                       "tree": "tree_reduce on the aggregator GPU + peer loads)"}[modes[0]]},
         "roofline": {"bound": "nvlink" if nv_bound else "hbm",
                      "achieved": round((nv_bytes if nv_bound else hbm_bytes) / T / 1e9, 1),
                      "peak": round(b_nv if nv_bound else peak_hbm, 1), "unit": "GB/s",
@@ -428,13 +436,13 @@ def run_bench_multi(a):
         "gpu_launches": int(kl),
         "clocks": ck.summary(),
     }
-    if len(modes) > 1:
-        cfg2, recs2, _, _ = results[modes[1]]
+    for mode2 in modes[1:]:
+        cfg2, recs2, _, _ = results[mode2]
         T2 = sum(r["ms"] for r in recs2) / 1e3
-        line["variants"] = {f"mode_{modes[1]}": {
+        line.setdefault("variants", {})[f"mode_{mode2}"] = {
             "value": round(sum(r["bytes"] for r in recs2) / T2 / 1e9, 2), "unit": "GB/s",
             "ms_per_step": round(T2 * 1e3 / len(recs2), 4),
-            "roofline_frac": round(sum(r["t_roof"] for r in recs2) / T2, 4)}}
+            "roofline_frac": round(sum(r["t_roof"] for r in recs2) / T2, 4)}
     if ar is not None:
         line.setdefault("variants", {})["allreduce_push_get_vs_nccl"] = ar
     if e2e is not None:

@@ -35,7 +35,8 @@ def main():
     ap.add_argument("--S", type=int, default=1_000_003)
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--dtype", default="f32")
-    ap.add_argument("--modes", default="fold,tree")
+    ap.add_argument("--modes", default="fold,tree,staged")
+    ap.add_argument("--stage-mib", type=int, default=0, help="staging buffer of the staged mode (0: 4096)")
     ap.add_argument("--kernel", default="bulk")
     ap.add_argument("--gamma", type=float, default=0.0)
     ap.add_argument("--replica-mode", type=int, default=0)
@@ -53,7 +54,7 @@ def main():
             continue                             # momentum runs in fold mode only
         cfg = configs.config(a.cid, G=world, dtype=a.dtype, scale_S=a.S, gamma=a.gamma,
                              replica_mode=a.replica_mode, div_max=a.div_max, workers=a.workers)
-        sw = ShardedWorkload(cfg, rank, world, device, ctrl, mode=mode)
+        sw = ShardedWorkload(cfg, rank, world, device, ctrl, mode=mode, stage_mib=a.stage_mib)
         b, n = cfg["shards"][rank]
         rng = np.random.default_rng(rank)
         idx = np.unique(np.concatenate([rng.integers(b, b + n, 5000), np.arange(b, min(b + 17, b + n)),

@@ -26,7 +26,13 @@ def _run(nproc, *args, timeout=600):
                                         (3, ["--dtype", "bf16", "--kernel", "bulk"])])
 def test_two_ranks_bitwise(cid, extra):
     out = _run(2, "--cid", str(cid), *extra)
-    assert "MULTIGPU_OK fold" in out and "MULTIGPU_OK tree" in out
+    assert "MULTIGPU_OK fold" in out and "MULTIGPU_OK tree" in out and "MULTIGPU_OK staged" in out
+
+
+def test_two_ranks_staged_minimum_chunk():
+    # copy-engine staging with a 2 MiB buffer: 4096-element chunks, many of them, ragged tail
+    out = _run(2, "--cid", "3", "--S", "300007", "--modes", "staged", "--stage-mib", "2", "--workers", "32")
+    assert "MULTIGPU_OK staged" in out
 
 
 def test_two_ranks_momentum_with_mirror():
@@ -37,15 +43,15 @@ def test_two_ranks_momentum_with_mirror():
 def test_two_ranks_replica_trees_with_retention():
     # config 5 (replica of shard j on GPU j+1), count-style Div_max so that updates are punted
     out = _run(2, "--cid", "5", "--S", "200003", "--steps", "4", "--replica-mode", "1", "--div-max", "20",
-               "--workers", "32", "--modes", "fold,tree")
-    assert "MULTIGPU_OK fold" in out and "MULTIGPU_OK tree" in out
+               "--workers", "32", "--modes", "fold,tree,staged")
+    assert "MULTIGPU_OK fold" in out and "MULTIGPU_OK tree" in out and "MULTIGPU_OK staged" in out
     assert "punted_total=0" not in out
 
 
 def test_two_ranks_host_resident_updates():
     # the e2e path: each rank stages its committed host-resident updates (phase 1), peers read them
     out = _run(2, "--cid", "3", "--S", "400009", "--steps", "2", "--host")
-    assert "MULTIGPU_OK fold" in out and "MULTIGPU_OK tree" in out
+    assert "MULTIGPU_OK fold" in out and "MULTIGPU_OK tree" in out and "MULTIGPU_OK staged" in out
 
 
 def test_two_ranks_allreduce_push_get():
@@ -61,4 +67,4 @@ def test_all_gpus_if_several():
     if n < 4:
         pytest.skip("needs >= 4 GPUs")
     out = _run(4, "--cid", "5", "--S", "2000011")
-    assert "MULTIGPU_OK fold" in out and "MULTIGPU_OK tree" in out
+    assert "MULTIGPU_OK fold" in out and "MULTIGPU_OK tree" in out and "MULTIGPU_OK staged" in out
