@@ -292,6 +292,81 @@ def measure_nvlink(device: int, rank: int, world: int, ctrl, nbytes: int = 1 << 
     return out
 
 
+def w_checksum(w: torch.Tensor) -> int:
+    """Exact integer digest of an fp32 tensor's bits (for bitwise comparisons across runs)."""
+    return int(w.view(torch.int32).to(torch.int64).sum().item())
+
+
+def nccl_baseline(cfg: dict, rank: int, world: int, local: int, ctrl, steps: int, warmup: int, flush=None):
+    """The library-collective baseline the fused path is measured against (SURVEY §8(e),
+    "measured alternative"): per batch, the plan's slices of every committed update travel
+    by NCCL grouped send/recv into a local staging buffer, then the same commit kernel folds
+    them from local HBM (a world = 1 context over this shard).  Timed with CUDA events on the
+    current stream around transfer + fold, max over ranks.  Needs the NCCL default group."""
+    assert dist.get_backend() == "nccl" and not cfg["replica"] and not cfg.get("gamma")
+    sw = ShardedWorkload(cfg, rank, world, local, ctrl, mode="fold")
+    sw.fill(0)
+    wl = sw.wl
+    S, W, e = cfg["S"], cfg["W"], cfg["e"]
+    b, n = cfg["shards"][rank]
+    tdt = wl.slots[wl.local_workers[0]].dtype if wl.local_workers else torch.float32
+    remote = [w for w in range(W) if cfg["home"][w] != rank]
+    row = {w: i for i, w in enumerate(remote)}
+    stage = torch.empty((max(len(remote), 1), -(-max(n, 1) // 64) * 64), dtype=tdt,
+                        device=torch.device("cuda", local))
+    # a world = 1 context over the same shard: local slots as they are, remote ones = staging
+    # rows shifted so that the kernel's slot + shard_begin lands on the row
+    ptrs = [wl.slots[w].data_ptr() if w in wl.slots else stage[row[w]].data_ptr() - b * e for w in range(W)]
+    st = torch.cuda.current_stream()
+    ctx2 = m.Context(device=local, model_shard=wl.w, update_slots=ptrs, lr=cfg["lr"], model_elems=S,
+                     shard_begin=b, dtype=wl.dt, node_rank=[0] * cfg["n_nodes"], n_nodes=cfg["n_nodes"],
+                     worker_node=cfg["worker_node"], stream=st.cuda_stream)
+    recs = []
+    for s in range(warmup + steps):
+        draws = cfgs.batch_draws(cfg, s, wl.v_init, wl.v_prev)
+        for w, d in enumerate(draws):
+            ctx2.submit(w, d["version"], d["t_avail"], d["norm"])
+        net, prm, keep = wl.net_params(s)
+        pb = ctx2.plan(net, prm)
+        pd = pb.to_dict(W)
+        if flush is not None:
+            flush()
+        st.synchronize()
+        sw.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        ops = []
+        for g in pd["order"]:
+            h = cfg["home"][g]
+            if h == rank:
+                for j in range(world):
+                    bj, nj = cfg["shards"][j]
+                    if j != rank and nj > 0:
+                        ops.append(dist.P2POp(dist.isend, wl.slots[g][bj:bj + nj], j))
+            elif n > 0:
+                ops.append(dist.P2POp(dist.irecv, stage[row[g], :n], h))
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+        ctx2.execute(pb)
+        e1.record(st)
+        ctx2.sync()
+        e1.synchronize()
+        ms = max_over_ranks(e0.elapsed_time(e1), ctrl)
+        wl.after_commit(pd, draws)
+        sw.barrier()
+        if s >= warmup:
+            recs.append(dict(ms=ms, bytes=committed_bytes(cfg, pd)))
+    digest = w_checksum(wl.w)
+    ctx2.close()
+    sw.close()
+    T = sum(r["ms"] for r in recs) / 1e3
+    return {"value": round(sum(r["bytes"] for r in recs) / T / 1e9, 2), "unit": "GB/s",
+            "ms_per_step": round(T * 1e3 / len(recs), 4), "w_digest": digest,
+            "what": "NCCL grouped send/recv of the plan's slices into local staging, then the same fused "
+                    "commit kernel from local HBM (not overlapped)"}
+
+
 def e2e_multi(cfg: dict, rank: int, world: int, local: int, ctrl, steps: int) -> dict:
     """The metric end to end through the public API on every rank: committed updates of the
     workers homed on a rank move from pinned host memory (phase 1, H2D), the sharded commit
@@ -354,6 +429,8 @@ def run_bench_multi(a):
         flush_w.zero_()
         flush_r.sum()
 
+    digests = {}
+
     def run(mode, steps, warmup, clocks=False):
         cfg = cfgs.config(cid, G=world, tau=a.tau, dtype=a.dtype)
         sw = ShardedWorkload(cfg, rank, world, local, ctrl, mode=mode)
@@ -377,6 +454,7 @@ def run_bench_multi(a):
         if clocks:
             ck.__exit__()
         kl = sw.wl.ctx.stats()[0] - kl0
+        digests[mode] = w_checksum(sw.wl.w)
         sw.close()
         return cfg, recs, ck, kl
 
@@ -387,6 +465,15 @@ def run_bench_multi(a):
     for i, mode in enumerate(modes):
         results[mode] = run(mode, a.steps if i == 0 else max(3, a.steps // 2), a.warmup if i == 0 else 2,
                             clocks=(i == 0))
+    nb = None
+    cfg0 = cfgs.config(cid, G=world, tau=a.tau, dtype=a.dtype)
+    if not a.no_variants and dist.get_backend() == "nccl" and not cfg0["replica"]:
+        nb = nccl_baseline(cfg0, rank, world, local, ctrl, a.steps, a.warmup, flush=l2_flush)
+        # same batches from the same w0: the library-collective path must land on the same bits
+        same = torch.tensor([1.0 if nb["w_digest"] == digests[modes[0]] else 0.0], dtype=torch.float64)
+        dist.all_reduce(same, op=dist.ReduceOp.MIN, group=ctrl)
+        nb["bitwise_equal_to_primary"] = bool(same.item() == 1.0)
+        del nb["w_digest"]
     ar = None
     if not a.no_variants:
         # NEXT-3: AllReduce via push/get vs NCCL all_reduce, ResNet-50-sized buffer per GPU
@@ -443,6 +530,8 @@ def run_bench_multi(a):
             "value": round(sum(r["bytes"] for r in recs2) / T2 / 1e9, 2), "unit": "GB/s",
             "ms_per_step": round(T2 * 1e3 / len(recs2), 4),
             "roofline_frac": round(sum(r["t_roof"] for r in recs2) / T2, 4)}
+    if nb is not None:
+        line.setdefault("variants", {})["nccl_sendrecv_then_fold"] = nb
     if ar is not None:
         line.setdefault("variants", {})["allreduce_push_get_vs_nccl"] = ar
     if e2e is not None:
