@@ -167,6 +167,46 @@ typedef struct {
 mlf_status mlf_plan(const mlf_net *net, const mlf_batch *batch,
                     const mlf_plan_params *params, mlf_plan_out *out);
 
+/* ---------------------------------------------------------------------
+ * Model distribution trees for pulls (NEXT-4, App. B.3): "for a
+ * batch of requests, k° distributors are earmarked.  Mapping of workers to
+ * distributors is done using a variant of alg. 3 ... we first transfer the model
+ * from the server to the k°-th distributor and then proceed backwards.  The
+ * workers in the first group receive the model directly from the server."
+ *
+ * Reading (R23-R25): Alg. 3 on the time-reversed problem — the network
+ * transposed (up <-> down caps, pair (i, j) <-> (j, i)), every request an "update"
+ * of model_bytes from its node available at 0, ordered by Alg. 1's SJF (no
+ * deadlines); the plan's schedule mirrored by t -> T - t is a feasible real
+ * schedule (capacities are constant within a batch, R9). */
+typedef struct {
+  int32_t n_servers;
+  const int32_t *server;           /* [n_servers] shard nodes */
+  const int64_t *shard_weight;     /* [n_servers] component weights (App. B.2); NULL = equal */
+  int32_t k;                       /* distributors k° */
+  const int32_t *distributor;      /* [k] group i -> distributor[i-1] (pre-assigned, as R13) */
+  int64_t model_bytes;             /* bytes of one full model (>= 0) */
+} mlf_dist_params;
+
+typedef struct {
+  int32_t capacity;                /* in: length of the [n] arrays (>= n_requests) */
+  int32_t *order;                  /* [n] request indices in SJF order O (R24) */
+  int32_t *group;                  /* [n] 0 = direct from the servers, i = via distributor i */
+  int32_t n_direct;                /* |group 0| = the chosen n* */
+  int32_t n_groups;
+  int32_t *group_node;             /* [k] distributor node of group i at [i-1] */
+  int64_t t_total_ns;              /* T: every request holds the model by T (model time) */
+  int64_t *t_recv_ns;              /* [n] model arrival per request (real time, R25) */
+  int64_t *t_start_ns;             /* [n] start of the request's last hop (real time) */
+  int64_t *t_dist_ns;              /* [k] model arrival at distributor i (real time) */
+} mlf_dist_out;
+
+/* Pure; may run concurrently.  request_node[i] = node of the i-th pull request.
+ * Errors: MLF_E_INVALID (null / out-of-range ids, bad weights), MLF_E_CAPACITY
+ * (outputs too small), MLF_E_UNSCHEDULABLE (a request's path is down). */
+mlf_status mlf_plan_distribution(const mlf_net *net, int32_t n_requests, const int32_t *request_node,
+                                 const mlf_dist_params *params, mlf_dist_out *out);
+
 /* ======================================================================
  * Execution (CUDA, one context per process/device; a context is single-threaded)
  * ====================================================================== */
@@ -293,6 +333,23 @@ mlf_status mlf_sync(mlf_ctx *ctx, float *device_ms);
  * committed model to dst + shard_begin (device or host memory, dst_is_host)
  * after the last execute; *version = batch-boundary version (R19). */
 mlf_status mlf_pull_model(mlf_ctx *ctx, void *dst, int32_t dst_is_host, int64_t *version);
+
+/* Execute a distribution plan (NEXT-4, App. B.3) for n pull requests on the box:
+ * request_node[i] is the node of request i (node -> GPU through mlf_config.node_rank),
+ * view[j] a full-length fp32 model view on rank j (16-byte aligned; mapped peer
+ * pointers), shard[j] / shard_begin[j] / shard_elems[j] rank j's PS shard.  Each GPU's
+ * view is written once, by its earliest hop in the plan: a GPU that hosts the
+ * distributor of a non-empty group or a direct request gathers every shard
+ * (MLF_PHASE_AGGREGATE, "the workers in the first group receive the model directly
+ * from the server"); any other requesting GPU copies its distributor's view with TMA
+ * bulk copies (MLF_PHASE_COMMIT), after the peers' phase-1 events — the caller puts a
+ * host barrier between the phases when world > 1.  *source (may be NULL) = -1 filled
+ * from the servers, r >= 0 copied from rank r, -2 not requested.  Call after the
+ * execute whose model is being distributed; mlf_sync times it. */
+mlf_status mlf_distribute_phase(mlf_ctx *ctx, const mlf_dist_out *plan, int32_t n_requests,
+                                const int32_t *request_node, float *const *view, const float *const *shard,
+                                const int64_t *shard_begin, const int64_t *shard_elems, int32_t phase,
+                                int32_t *source);
 
 /* Counters: kernels this context launched, and bytes it moved host<->device. */
 mlf_status mlf_stats(mlf_ctx *ctx, int64_t *kernel_launches, int64_t *h2d_bytes, int64_t *d2h_bytes);

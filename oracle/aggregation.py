@@ -52,6 +52,7 @@ class AggCase:
     total: int | None      # None = infeasible
     commits: list = field(default_factory=list)
     member_arrivals: dict = field(default_factory=dict)   # position -> t_en at its aggregator
+    member_transfers: dict = field(default_factory=dict)  # position -> its Transfer to the aggregator
     net: Net | None = None
 
 
@@ -60,7 +61,7 @@ def det_agg(n: int, items: list, net0: Net, servers, weights, aggs) -> AggCase:
     k = len(aggs)
     nw = net0.fork()
     t_max, have = 0, n > 0
-    commits, arrivals = [], {}
+    commits, arrivals, transfers = [], {}, {}
     for i in range(n):                                       # lines 3-7
         it = items[i]
         s, nw = send(nw, it.node, servers, component_bytes(it.size, weights), it.t_avail)
@@ -96,12 +97,13 @@ def det_agg(n: int, items: list, net0: Net, servers, weights, aggs) -> AggCase:
             group.append(i)
             group_arr.append(tr.t_en)
             arrivals[i] = tr.t_en
+            transfers[i] = tr
             i += 1
         if group:
             flush()
     except Unschedulable:
         return AggCase(n, None)
-    return AggCase(n, t_max, commits, arrivals, nw)
+    return AggCase(n, t_max, commits, arrivals, transfers, nw)
 
 
 def plan_aggregation(items: list, net0: Net, servers, weights, aggs) -> AggCase:

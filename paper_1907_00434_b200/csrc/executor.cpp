@@ -954,14 +954,11 @@ extern "C" mlf_status mlf_copy_kernel(int32_t device, void *dst, const void *src
   });
 }
 
-extern "C" mlf_status mlf_gather(int32_t device, float *dst, int32_t n, const float *const *shard,
-                                 const int64_t *begin, const int64_t *elems, int32_t copy_engine, void *stream) {
-  return guard([&] {
-    if (!dst || n < 0 || (n > 0 && (!shard || !begin || !elems))) throw Fail{MLF_E_INVALID, "gather arguments"};
-    CK(cudaSetDevice(device));
-    int sm = 148;
-    CK(cudaDeviceGetAttribute(&sm, cudaDevAttrMultiProcessorCount, device));
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
+// The whole model from its shards into dst (one gather launch over every 16-byte-aligned
+// body; ragged tails and overflow shards on the copy engine).
+static void gather_into(float *dst, int32_t n, const float *const *shard, const int64_t *begin, const int64_t *elems,
+                        int32_t copy_engine, cudaStream_t s, int sm) {
+  {
     GatherArgs g{};
     for (int i = 0; i < n; ++i) {
       if (elems[i] < 0 || begin[i] < 0 || (elems[i] > 0 && !shard[i])) throw Fail{MLF_E_INVALID, "gather shard"};
@@ -983,7 +980,84 @@ extern "C" mlf_status mlf_gather(int32_t device, float *dst, int32_t n, const fl
                            (size_t)(bytes - body), cudaMemcpyDeviceToDevice, s));
     }
     CK(launch_gather(g, s, sm));
+  }
+}
+
+extern "C" mlf_status mlf_gather(int32_t device, float *dst, int32_t n, const float *const *shard,
+                                 const int64_t *begin, const int64_t *elems, int32_t copy_engine, void *stream) {
+  return guard([&] {
+    if (!dst || n < 0 || (n > 0 && (!shard || !begin || !elems))) throw Fail{MLF_E_INVALID, "gather arguments"};
+    CK(cudaSetDevice(device));
+    int sm = 148;
+    CK(cudaDeviceGetAttribute(&sm, cudaDevAttrMultiProcessorCount, device));
+    gather_into(dst, n, shard, begin, elems, copy_engine, static_cast<cudaStream_t>(stream), sm);
   });
+}
+
+// NEXT-4: a distribution plan executed on the box (header: mlf_distribute_phase).
+extern "C" mlf_status mlf_distribute_phase(mlf_ctx *c, const mlf_dist_out *p, int32_t n, const int32_t *req,
+                                           float *const *view, const float *const *shard, const int64_t *begin,
+                                           const int64_t *elems, int32_t phase, int32_t *source) {
+  mlf_status st = guard([&] {
+    check_ctx(c);
+    const int world = c->cfg.world, r = c->cfg.rank;
+    if (!p || n < 0 || (n > 0 && (!req || !p->order || !p->group)) || !view || !shard || !begin || !elems)
+      throw Fail{MLF_E_INVALID, "distribute arguments"};
+    if (p->n_groups < 0 || (p->n_groups > 0 && !p->group_node)) throw Fail{MLF_E_INVALID, "distribution groups"};
+    const int nn = (int)c->node_rank.size();
+    for (int i = 0; i < n; ++i)
+      if (req[i] < 0 || req[i] >= nn || p->group[i] < 0 || p->group[i] > p->n_groups)
+        throw Fail{MLF_E_INVALID, "request node or group out of range"};
+    for (int g = 0; g < p->n_groups; ++g)
+      if (p->group_node[g] < 0 || p->group_node[g] >= nn) throw Fail{MLF_E_INVALID, "distributor node unknown"};
+    for (int j = 0; j < world; ++j)
+      if (!view[j] || (reinterpret_cast<uintptr_t>(view[j]) & 15) || (elems[j] > 0 && !shard[j]))
+        throw Fail{MLF_E_INVALID, "null or misaligned view, or null shard"};
+    // this GPU's view is written once, by its earliest hop: from the servers if it hosts a
+    // distributor of a non-empty group or a direct request (phase 1), else from the
+    // distributor of its first request in O (phase 2)
+    bool from_servers = false;
+    int src = -1;
+    std::vector<uint8_t> used(p->n_groups + 1, 0);
+    for (int i = 0; i < n; ++i) used[p->group[i]] = 1;
+    for (int g = 1; g <= p->n_groups; ++g)
+      if (used[g] && c->node_rank[p->group_node[g - 1]] == r) from_servers = true;
+    for (int q = 0; q < n; ++q) {
+      const int i = p->order[q];
+      if (i < 0 || i >= n) throw Fail{MLF_E_INVALID, "distribution order"};
+      if (c->node_rank[req[i]] != r) continue;
+      if (p->group[i] == 0) from_servers = true;
+      else if (src < 0) src = c->node_rank[p->group_node[p->group[i] - 1]];
+    }
+    if (from_servers || src == r) src = -1, from_servers = true;
+    if (source) *source = from_servers ? -1 : (src >= 0 ? src : -2);
+    CK(cudaSetDevice(c->cfg.device));
+    if (phase & MLF_PHASE_AGGREGATE) {
+      record_start(c);
+      if (from_servers) {
+        gather_into(view[r], world, shard, begin, elems, 0, c->stream, c->sm_count);
+        ++c->launches;
+      }
+      if (c->ev_phase) CK(cudaEventRecord(c->ev_phase, c->stream));
+    }
+    if (phase & MLF_PHASE_COMMIT) {
+      for (auto e : c->peer_events) CK(cudaStreamWaitEvent(c->stream, e, 0));
+      record_start(c);
+      if (src >= 0) {                             // TMA bulk copy of the distributor's view
+        const int64_t bytes = c->cfg.model_elems * 4, body = bytes & ~int64_t(15);
+        CK(launch_bulk_copy(view[r], view[src], body, c->stream, c->sm_count));
+        ++c->launches;
+        if (bytes > body)
+          CK(cudaMemcpyAsync(reinterpret_cast<char *>(view[r]) + body, reinterpret_cast<const char *>(view[src]) + body,
+                             (size_t)(bytes - body), cudaMemcpyDeviceToDevice, c->stream));
+      }
+      CK(cudaEventRecord(c->ev_stop, c->stream));
+      c->started = false;
+      c->pending = true;
+    }
+  });
+  if (st == MLF_E_CUDA && c) c->sticky = true;
+  return st;
 }
 
 extern "C" mlf_status mlf_copy_bulk(int32_t device, void *dst, const void *src, int64_t bytes, void *stream) {

@@ -520,8 +520,10 @@ struct CommitRec {
 struct AggCase {
   int n = 0;
   bool feasible = false;
+  bool record = false;              // keep the member transfers' times (distribution plans)
   i64 total = 0;
   std::vector<CommitRec> commits;
+  std::vector<i64> m_st, m_en;      // [position - n]: member -> aggregator transfer times
 };
 
 // Alg. 3 DetAgg(n), continued from the state after its n direct sends (R10-R12):
@@ -559,6 +561,10 @@ static void det_agg_tail(AggCase &cs, Net &nw, i64 t_max, const std::vector<Item
     P.clear();                                                // lines 16-18
     add_pending(P, tr);
     apply_pending(nw, P);
+    if (cs.record) {
+      cs.m_st.push_back(tr.t_st);
+      cs.m_en.push_back(tr.t_en);
+    }
     if (gcount == 0) gfirst = i;
     ++gcount;
     gsize = std::max(gsize, items[i].size);
@@ -590,11 +596,13 @@ struct Prefix {
 };
 
 static AggCase det_agg(int n, const std::vector<Item> &items, const Net &net0, const Ctx &c,
-                       const std::vector<int> &dsts, const std::vector<int> &aggs, Net *net_out) {
+                       const std::vector<int> &dsts, const std::vector<int> &aggs, Net *net_out,
+                       bool record = false) {
   Prefix pre(net0);
   for (int i = 0; i < n; ++i) pre.extend(items, i, c, dsts);
   AggCase cs;
   cs.n = n;
+  cs.record = record;
   if (!pre.ok) return cs;
   cs.commits = pre.commits;
   det_agg_tail(cs, pre.nw, pre.t_max, items, c, dsts, aggs);
@@ -604,11 +612,12 @@ static AggCase det_agg(int n, const std::vector<Item> &items, const Net &net0, c
 
 // Alg. 3 lines 21-24: all |U|+1 cases, argmin total, ties -> smallest n (R14).
 static AggCase plan_aggregation(const std::vector<Item> &items, const Net &net0, const Ctx &c,
-                                const std::vector<int> &dsts, const std::vector<int> &aggs, Net *net_out) {
+                                const std::vector<int> &dsts, const std::vector<int> &aggs, Net *net_out,
+                                bool record = false) {
   const int N = (int)items.size();
   // no aggregators: every case n < |U| meets aid = 1 > k at its first tail item (R12), so
   // only the all-direct case is feasible
-  if (aggs.empty()) return det_agg(N, items, net0, c, dsts, aggs, net_out);
+  if (aggs.empty()) return det_agg(N, items, net0, c, dsts, aggs, net_out, record);
   std::vector<i64> totals(N + 1, -1);
   // contiguous ranges of n per task; the prefix states at the range starts are built in
   // one sequential pass, then every task extends its own copy incrementally
@@ -656,7 +665,7 @@ static AggCase plan_aggregation(const std::vector<Item> &items, const Net &net0,
   for (int n = 0; n <= N; ++n)
     if (totals[n] >= 0 && (best < 0 || totals[n] < totals[best])) best = n;
   if (best < 0) throw PlanFail{MLF_E_UNSCHEDULABLE, "no feasible aggregation case"};
-  return det_agg(best, items, net0, c, dsts, aggs, net_out);
+  return det_agg(best, items, net0, c, dsts, aggs, net_out, record);
 }
 
 static std::vector<i64> chained_times(const std::vector<CommitRec> &cm) {
@@ -924,6 +933,135 @@ extern "C" mlf_status mlf_plan(const mlf_net *net, const mlf_batch *batch, const
   try {
     g_plan_err.clear();
     return plan_impl(net, batch, params, out);
+  } catch (const PlanFail &e) {
+    g_plan_err = e.msg;
+    mlf_set_error(e.msg.c_str());
+    return e.code;
+  } catch (const std::exception &e) {
+    g_plan_err = e.what();
+    mlf_set_error(e.what());
+    return MLF_E_INVALID;
+  } catch (...) {
+    mlf_set_error("unknown planner error");
+    return MLF_E_INVALID;
+  }
+}
+
+// ---------------------------------------------------------------- NEXT-4 distribution
+// App. B.3 under readings R23-R25: Alg. 3 on the transposed network
+// (up <-> down, pair (i, j) <-> (j, i)) over the pull requests in Alg. 1's SJF order;
+// the schedule mirrored by t -> T - t is the real one.
+static mlf_status plan_dist_impl(const mlf_net *net, int32_t n, const int32_t *req, const mlf_dist_params *prm,
+                                 mlf_dist_out *out) {
+  if (!net || !prm || !out || (n > 0 && !req)) throw PlanFail{MLF_E_INVALID, "null argument"};
+  if (net->n_nodes < 1 || !net->nic_up || !net->nic_down) throw PlanFail{MLF_E_INVALID, "bad network"};
+  if (n < 0 || prm->model_bytes < 0) throw PlanFail{MLF_E_INVALID, "n_requests / model_bytes"};
+  const int nn = net->n_nodes;
+  auto node_ok = [&](int x) { return x >= 0 && x < nn; };
+  std::vector<int64_t> up(net->nic_down, net->nic_down + nn), down(net->nic_up, net->nic_up + nn), bw;
+  if (net->bw) {
+    bw.resize((size_t)nn * nn);
+    for (int i = 0; i < nn; ++i)
+      for (int j = 0; j < nn; ++j) bw[(size_t)i * nn + j] = net->bw[(size_t)j * nn + i];
+  }
+  Ctx c;
+  c.d.n = nn;
+  c.d.up = up.data();
+  c.d.down = down.data();
+  c.d.bw = net->bw ? bw.data() : nullptr;
+  c.d.site = net->site;
+  if (prm->n_servers < 1 || !prm->server) throw PlanFail{MLF_E_INVALID, "no server"};
+  for (int j = 0; j < prm->n_servers; ++j) {
+    if (!node_ok(prm->server[j])) throw PlanFail{MLF_E_INVALID, "server node out of range"};
+    c.servers.push_back(prm->server[j]);
+    const i64 w = prm->shard_weight ? prm->shard_weight[j] : 1;
+    if (w <= 0) throw PlanFail{MLF_E_INVALID, "shard weights"};
+    c.weights.push_back(w);
+    c.wsum += w;
+  }
+  if (prm->k < 0 || (prm->k > 0 && !prm->distributor)) throw PlanFail{MLF_E_INVALID, "distributors"};
+  for (int i = 0; i < prm->k; ++i) {
+    if (!node_ok(prm->distributor[i])) throw PlanFail{MLF_E_INVALID, "distributor node out of range"};
+    c.aggs.push_back(prm->distributor[i]);
+  }
+  std::vector<Item> items(n);
+  for (int i = 0; i < n; ++i) {
+    if (!node_ok(req[i])) throw PlanFail{MLF_E_INVALID, "request node out of range"};
+    items[i] = {req[i], prm->model_bytes, 0, 0, 0.0};
+  }
+  if (out->capacity < n || (n > 0 && (!out->order || !out->group || !out->t_recv_ns || !out->t_start_ns)) ||
+      (n > 0 && prm->k > 0 && (!out->group_node || !out->t_dist_ns)))
+    throw PlanFail{MLF_E_CAPACITY, "output arrays too small or missing"};
+  std::vector<i64> comp;
+  component_bytes(prm->model_bytes, c.weights, c.wsum, comp);
+  for (auto &it : items)
+    for (size_t j = 0; j < c.servers.size(); ++j)
+      if (comp[j] > 0 && path_dead(c.d, it.node, c.servers[j]))
+        throw PlanFail{MLF_E_UNSCHEDULABLE, "a request's path from a server is down"};
+  // R24: Alg. 1 (SJF, no deadlines) on the transposed network; requests from one node
+  // are interchangeable, so each distinct node is evaluated once per step
+  std::vector<int> order, unproc(n);
+  for (int i = 0; i < n; ++i) unproc[i] = i;
+  Net nw(&c.d);
+  Pending local;
+  while (!unproc.empty()) {
+    std::unordered_map<int, i64> ten;
+    int best = -1;
+    i64 best_t = 0;
+    for (int g : unproc) {
+      auto it = ten.find(items[g].node);
+      if (it == ten.end()) {
+        Send s;
+        if (!send(nw, nullptr, c, c.servers, items[g].node, items[g].size, 0, s, local))
+          throw PlanFail{MLF_E_UNSCHEDULABLE, "a request's path from a server is down"};
+        it = ten.emplace(items[g].node, s.t_en).first;
+      }
+      if (best < 0 || it->second < best_t) {
+        best = g;
+        best_t = it->second;
+      }
+    }
+    Send s;
+    send_apply(nw, c, c.servers, items[best].node, items[best].size, 0, s);
+    order.push_back(best);
+    unproc.erase(std::find(unproc.begin(), unproc.end(), best));
+  }
+  std::vector<Item> ordered(n);
+  for (int p = 0; p < n; ++p) ordered[p] = items[order[p]];
+  const Net net0(&c.d);
+  AggCase cs = plan_aggregation(ordered, net0, c, c.servers, c.aggs, nullptr, true);
+  const i64 T = cs.total;
+  int n_groups = 0;
+  for (auto &cm : cs.commits) {
+    if (cm.group == 0) {
+      const int g = order[cm.first];
+      out->group[g] = 0;
+      out->t_recv_ns[g] = T - cm.send.t_st;
+      out->t_start_ns[g] = T - cm.send.t_en;
+      continue;
+    }
+    out->t_dist_ns[cm.group - 1] = T - cm.send.t_st;
+    out->group_node[cm.group - 1] = c.aggs[cm.group - 1];
+    n_groups = std::max(n_groups, cm.group);
+    for (int p = cm.first; p < cm.first + cm.count; ++p) {
+      const int g = order[p];
+      out->group[g] = cm.group;
+      out->t_recv_ns[g] = T - cs.m_st[p - cs.n];
+      out->t_start_ns[g] = T - cs.m_en[p - cs.n];
+    }
+  }
+  for (int p = 0; p < n; ++p) out->order[p] = order[p];
+  out->n_direct = cs.n;
+  out->n_groups = n_groups;
+  out->t_total_ns = T;
+  return MLF_OK;
+}
+
+extern "C" mlf_status mlf_plan_distribution(const mlf_net *net, int32_t n_requests, const int32_t *request_node,
+                                            const mlf_dist_params *params, mlf_dist_out *out) {
+  try {
+    g_plan_err.clear();
+    return plan_dist_impl(net, n_requests, request_node, params, out);
   } catch (const PlanFail &e) {
     g_plan_err = e.msg;
     mlf_set_error(e.msg.c_str());

@@ -26,7 +26,7 @@ EXPORTS = (
     "mlf_execute", "mlf_execute_phase", "mlf_sync", "mlf_pull_model", "mlf_stats", "mlf_destroy",
     "mlf_last_error", "mlf_ipc_export", "mlf_ipc_open", "mlf_ipc_close", "mlf_phase_event_export",
     "mlf_phase_events_open", "mlf_gather", "mlf_synth_fill", "mlf_copy_kernel", "mlf_copy_engine",
-    "mlf_copy_bulk",
+    "mlf_copy_bulk", "mlf_plan_distribution", "mlf_distribute_phase",
 )
 
 
@@ -94,12 +94,27 @@ class MlfIpcHandle(C.Structure):
     _fields_ = [("handle", C.c_uint8 * 64), ("offset", C.c_int64)]
 
 
+class MlfDistParams(C.Structure):
+    _fields_ = [("n_servers", C.c_int32), ("server", _i32p), ("shard_weight", _i64p), ("k", C.c_int32),
+                ("distributor", _i32p), ("model_bytes", C.c_int64)]
+
+
+class MlfDistOut(C.Structure):
+    _fields_ = [("capacity", C.c_int32), ("order", _i32p), ("group", _i32p), ("n_direct", C.c_int32),
+                ("n_groups", C.c_int32), ("group_node", _i32p), ("t_total_ns", C.c_int64),
+                ("t_recv_ns", _i64p), ("t_start_ns", _i64p), ("t_dist_ns", _i64p)]
+
+
 class MlfIpcEvent(C.Structure):
     _fields_ = [("handle", C.c_uint8 * 64)]
 
 
 _lib.mlf_last_error.restype = C.c_char_p
 _lib.mlf_plan.argtypes = [C.POINTER(MlfNet), C.POINTER(MlfBatch), C.POINTER(MlfPlanParams), C.POINTER(MlfPlanOut)]
+_lib.mlf_plan_distribution.argtypes = [C.POINTER(MlfNet), C.c_int32, _i32p, C.POINTER(MlfDistParams),
+                                       C.POINTER(MlfDistOut)]
+_lib.mlf_distribute_phase.argtypes = [_p, C.POINTER(MlfDistOut), C.c_int32, _i32p, C.POINTER(_p), C.POINTER(_p),
+                                      _i64p, _i64p, C.c_int32, _i32p]
 _lib.mlf_init.argtypes = [C.POINTER(MlfConfig), C.c_int64, C.POINTER(_p)]
 _lib.mlf_submit_update.argtypes = [_p, C.c_int32, C.c_int64, C.c_int64, C.c_double, _i32p]
 _lib.mlf_set_update_host.argtypes = [_p, C.c_int32, _p]
@@ -183,6 +198,38 @@ def plan(n_nodes, nic_up, nic_down, batch, servers, *, bw=None, site=None, aggs=
                         float(div_max), float(gamma), float(hist_norm), len(cn), _ptr(cn, C.c_int32),
                         _ptr(cb, C.c_int64), _ptr(cm, C.c_double), int(replica_mode), int(sync_mode))
     return plan_raw(net, b, prm, n + len(cn), keep)
+
+
+def plan_distribution(n_nodes, nic_up, nic_down, request_nodes, servers, model_bytes: int, *, bw=None, site=None,
+                      distributors=(), shard_weights=None) -> dict:
+    """mlf_plan_distribution (NEXT-4, App. B.3): distribution tree for a batch of pulls."""
+    keep = []
+
+    def A(x, dt):
+        a = _arr(x, dt)
+        keep.append(a)
+        return a
+
+    up, down = A(nic_up, np.int64), A(nic_down, np.int64)
+    bw_a = A(bw, np.int64) if bw is not None else None
+    site_a = A(site, np.int32) if site is not None else None
+    net = MlfNet(int(n_nodes), _ptr(up, C.c_int64), _ptr(down, C.c_int64), _ptr(bw_a, C.c_int64),
+                 _ptr(site_a, C.c_int32))
+    rq, sv, ds = A(list(request_nodes), np.int32), A(list(servers), np.int32), A(list(distributors), np.int32)
+    sw = A(shard_weights, np.int64) if shard_weights is not None else None
+    prm = MlfDistParams(len(sv), _ptr(sv, C.c_int32), _ptr(sw, C.c_int64), len(ds), _ptr(ds, C.c_int32),
+                        int(model_bytes))
+    n, k = len(rq), max(len(ds), 1)
+    order, group = np.zeros(max(n, 1), np.int32), np.zeros(max(n, 1), np.int32)
+    t_recv, t_start = np.zeros(max(n, 1), np.int64), np.zeros(max(n, 1), np.int64)
+    gnode, t_dist = np.zeros(k, np.int32), np.zeros(k, np.int64)
+    out = MlfDistOut(max(n, 1), _ptr(order, C.c_int32), _ptr(group, C.c_int32), 0, 0, _ptr(gnode, C.c_int32), 0,
+                     _ptr(t_recv, C.c_int64), _ptr(t_start, C.c_int64), _ptr(t_dist, C.c_int64))
+    _check(_lib.mlf_plan_distribution(C.byref(net), n, _ptr(rq, C.c_int32), C.byref(prm), C.byref(out)))
+    ng = out.n_groups
+    return {"order": order[:n].tolist(), "group": group[:n].tolist(), "n_direct": out.n_direct, "n_groups": ng,
+            "group_node": gnode[:ng].tolist(), "t_total_ns": out.t_total_ns, "t_recv_ns": t_recv[:n].tolist(),
+            "t_start_ns": t_start[:n].tolist(), "t_dist_ns": t_dist[:ng].tolist()}
 
 
 class PlanBuffers:
@@ -366,6 +413,24 @@ class Context:
         d = dst if isinstance(dst, int) else dst.data_ptr()
         _check(_lib.mlf_pull_model(self._h, d, int(dst_is_host), C.byref(v)))
         return v.value
+
+    def distribute(self, dplan: dict, request_nodes, views, shards, begins, elems,
+                   phase: int = MLF_PHASE_AGGREGATE | MLF_PHASE_COMMIT) -> int:
+        """mlf_distribute_phase (NEXT-4): execute a plan_distribution() plan into the per-rank
+        model views.  Returns this rank's source (-1 servers, r >= 0 rank r's view, -2 none)."""
+        n = len(request_nodes)
+        rq = _arr(request_nodes, np.int32)
+        order, group = _arr(dplan["order"], np.int32), _arr(dplan["group"], np.int32)
+        gnode = _arr(dplan["group_node"] or [0], np.int32)
+        out = MlfDistOut(max(n, 1), _ptr(order, C.c_int32), _ptr(group, C.c_int32), int(dplan["n_direct"]),
+                         int(dplan["n_groups"]), _ptr(gnode, C.c_int32), int(dplan["t_total_ns"]), None, None, None)
+        vw = (_p * len(views))(*[v if isinstance(v, int) else v.data_ptr() for v in views])
+        sh = (_p * len(shards))(*[x if isinstance(x, int) else x.data_ptr() for x in shards])
+        b, e = _arr(begins, np.int64), _arr(elems, np.int64)
+        src = C.c_int32()
+        _check(_lib.mlf_distribute_phase(self._h, C.byref(out), n, _ptr(rq, C.c_int32), vw, sh, _ptr(b, C.c_int64),
+                                         _ptr(e, C.c_int64), int(phase), C.byref(src)))
+        return src.value
 
     def phase_event(self) -> bytes:
         e = MlfIpcEvent()

@@ -292,6 +292,68 @@ def measure_nvlink(device: int, rank: int, world: int, ctrl, nbytes: int = 1 << 
     return out
 
 
+class DistributionRun:
+    """NEXT-4 (App. B.3) on the box: rank j holds PS shard j of a model of S fp32 elements
+    (w0 here) and a full-length model view; pull requests from virtual workers on every GPU
+    are served along an mlf_plan_distribution tree by mlf_distribute_phase."""
+
+    def __init__(self, S: int, rank: int, world: int, device: int, ctrl, seed: int = 0x4D4C46):
+        from synthgen.configs import shard_bounds
+        self.S, self.rank, self.world, self.ctrl = S, rank, world, ctrl
+        dev = torch.device("cuda", device)
+        self.shards = shard_bounds(S, world)
+        b, n = self.shards[rank]
+        self.shard = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
+        if n:
+            m.synth_fill(device, self.shard.data_ptr(), n, elem_offset=b, dtype=m.MLF_F32, seed=seed, kind=2,
+                         stream=torch.cuda.current_stream(dev).cuda_stream)
+        self.view = torch.empty(-(-S // 64) * 64, dtype=torch.float32, device=dev)
+        torch.cuda.synchronize(dev)
+        mine = (rank, m.ipc_export(device, self.shard.data_ptr()), m.ipc_export(device, self.view.data_ptr()))
+        allinfo = [None] * world
+        dist.all_gather_object(allinfo, mine, group=ctrl)
+        allinfo.sort()
+        self.mapper = IpcMapper(device)
+        self.shard_ptrs = [self.shard.data_ptr() if r == rank else self.mapper.open(sb) for (r, sb, _) in allinfo]
+        self.view_ptrs = [self.view.data_ptr() if r == rank else self.mapper.open(vb) for (r, _, vb) in allinfo]
+        self.ctx = m.Context(device=device, model_shard=self.shard[:n] if n else self.shard, update_slots=[], lr=0.0,
+                             model_elems=S, shard_begin=b, rank=rank, world=world, node_rank=list(range(world)),
+                             n_nodes=world, stream=torch.cuda.current_stream(dev).cuda_stream)
+        ev = self.ctx.phase_event()
+        evs = [None] * world
+        dist.all_gather_object(evs, (rank, ev), group=ctrl)
+        self.ctx.open_phase_events([e for (r, e) in sorted(evs) if r != rank])
+        dist.barrier(group=ctrl)
+
+    def plan(self, nic_up, nic_down, request_nodes, distributors) -> dict:
+        """Box network: node j = GPU j (site j), PS shard j on GPU j weighted by its length."""
+        G = self.world
+        return m.plan_distribution(G, nic_up, nic_down, request_nodes, list(range(G)), self.S * 4,
+                                   site=list(range(G)), distributors=distributors,
+                                   shard_weights=[max(x, 1) for (_, x) in self.shards])
+
+    def run(self, dplan: dict, request_nodes, flush=None):
+        """Phase 1, host barrier, phase 2; returns (this rank's source, device ms max over ranks)."""
+        if flush is not None:
+            flush()
+        torch.cuda.current_stream().synchronize()
+        dist.barrier(group=self.ctrl)
+        args = (dplan, request_nodes, self.view_ptrs, self.shard_ptrs, [b for (b, _) in self.shards],
+                [x for (_, x) in self.shards])
+        src = self.ctx.distribute(*args, phase=m.MLF_PHASE_AGGREGATE)
+        dist.barrier(group=self.ctrl)
+        self.ctx.distribute(*args, phase=m.MLF_PHASE_COMMIT)
+        ms = self.ctx.sync()
+        ms = max_over_ranks(ms, self.ctrl)
+        dist.barrier(group=self.ctrl)
+        return src, ms
+
+    def close(self):
+        self.ctx.close()
+        dist.barrier(group=self.ctrl)
+        self.mapper.close()
+
+
 def w_checksum(w: torch.Tensor) -> int:
     """Exact integer digest of an fp32 tensor's bits (for bitwise comparisons across runs)."""
     return int(w.view(torch.int32).to(torch.int64).sum().item())

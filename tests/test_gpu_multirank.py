@@ -62,9 +62,24 @@ def test_two_ranks_allreduce_push_get():
     assert r.returncode == 0 and "ALLREDUCE_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
 
 
+def test_two_ranks_distribution_trees():
+    # NEXT-4: model distribution along mlf_plan_distribution trees into every rank's view
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", "--nnodes=1", "--nproc-per-node=2",
+           os.path.join(HERE, "distribute_check.py"), "--S", "1000003"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, MASTER_ADDR="127.0.0.1", OMP_NUM_THREADS="1"))
+    assert r.returncode == 0 and "DISTRIBUTE_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "case degraded0: groups=1" in r.stdout
+
+
 def test_all_gpus_if_several():
     n = torch.cuda.device_count()
     if n < 4:
         pytest.skip("needs >= 4 GPUs")
     out = _run(4, "--cid", "5", "--S", "2000011")
     assert "MULTIGPU_OK fold" in out and "MULTIGPU_OK tree" in out and "MULTIGPU_OK staged" in out
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", "--nnodes=1", "--nproc-per-node=4",
+           os.path.join(HERE, "distribute_check.py"), "--S", "2000011"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, MASTER_ADDR="127.0.0.1", OMP_NUM_THREADS="1"))
+    assert r.returncode == 0 and "DISTRIBUTE_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
