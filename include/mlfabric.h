@@ -386,8 +386,10 @@ mlf_status mlf_phase_events_open(mlf_ctx *ctx, int32_t n, const mlf_ipc_event *p
 
 /* get(server, model) of the whole model on one GPU (Table 1): copy n shards (local
  * or mapped peer fp32 buffers) into dst[begin_i .. begin_i + elems_i).  copy_engine = 0:
- * SM peer loads through the library's copy kernel (bulk of each shard) — the NVLink
- * all-gather; 1: one cudaMemcpyAsync per shard on a copy engine.  Completes on `stream`. */
+ * TMA bulk copies (16 KB chunks through shared memory, all shards in one launch) — the
+ * NVLink all-gather; 1: one cudaMemcpyAsync per shard on a copy engine; 2: 128-bit SM
+ * peer loads (gather_kernel).  Ragged (non-16-byte) tails go to the copy engine.
+ * Completes on `stream`. */
 mlf_status mlf_gather(int32_t device, float *dst, int32_t n, const float *const *shard, const int64_t *begin,
                       const int64_t *elems, int32_t copy_engine, void *stream);
 

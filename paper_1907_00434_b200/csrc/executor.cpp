@@ -95,6 +95,7 @@ struct mlf_ctx {
   std::vector<std::pair<int, int>> to_free;       // slots released at the next batch
   int64_t retained_bytes = 0;
   bool started = false, pending = false, sticky = false, phase1_done = false;
+  bool dist_p1 = false;                           // distribution phase 1 recorded ev_stop
   int64_t launches = 0, h2d = 0, d2h = 0;
   CommitImpl impl = CommitImpl::kLdg;
 };
@@ -958,29 +959,38 @@ extern "C" mlf_status mlf_copy_kernel(int32_t device, void *dst, const void *src
 // body; ragged tails and overflow shards on the copy engine).
 static void gather_into(float *dst, int32_t n, const float *const *shard, const int64_t *begin, const int64_t *elems,
                         int32_t copy_engine, cudaStream_t s, int sm) {
-  {
-    GatherArgs g{};
-    for (int i = 0; i < n; ++i) {
-      if (elems[i] < 0 || begin[i] < 0 || (elems[i] > 0 && !shard[i])) throw Fail{MLF_E_INVALID, "gather shard"};
-      float *d = dst + begin[i];
-      const int64_t bytes = elems[i] * 4;
-      const bool aligned = ((reinterpret_cast<uintptr_t>(d) | reinterpret_cast<uintptr_t>(shard[i])) & 15) == 0;
-      if (copy_engine || !aligned || g.n == kMaxShards) {
-        if (bytes) CK(cudaMemcpyAsync(d, shard[i], (size_t)bytes, cudaMemcpyDeviceToDevice, s));
-        continue;
-      }
-      const int64_t body = bytes & ~int64_t(15);
+  GatherArgs g{};
+  BulkSegs t{};
+  for (int i = 0; i < n; ++i) {
+    if (elems[i] < 0 || begin[i] < 0 || (elems[i] > 0 && !shard[i])) throw Fail{MLF_E_INVALID, "gather shard"};
+    float *d = dst + begin[i];
+    const int64_t bytes = elems[i] * 4;
+    const bool aligned = ((reinterpret_cast<uintptr_t>(d) | reinterpret_cast<uintptr_t>(shard[i])) & 15) == 0;
+    const int used = copy_engine == 2 ? g.n : t.n;
+    if (copy_engine == 1 || !aligned || used == kMaxShards) {
+      if (bytes) CK(cudaMemcpyAsync(d, shard[i], (size_t)bytes, cudaMemcpyDeviceToDevice, s));
+      continue;
+    }
+    const int64_t body = bytes & ~int64_t(15);
+    if (copy_engine == 2) {
       g.vstart[g.n] = g.total_v;
       g.dst[g.n] = d;
       g.src[g.n] = shard[i];
       g.total_v += body / 16;
       ++g.n;
-      if (bytes > body)
-        CK(cudaMemcpyAsync(reinterpret_cast<char *>(d) + body, reinterpret_cast<const char *>(shard[i]) + body,
-                           (size_t)(bytes - body), cudaMemcpyDeviceToDevice, s));
+    } else if (body > 0) {
+      t.cstart[t.n + 1] = t.cstart[t.n] + (body + kBulkChunk - 1) / kBulkChunk;
+      t.dst[t.n] = reinterpret_cast<char *>(d);
+      t.src[t.n] = reinterpret_cast<const char *>(shard[i]);
+      t.bytes[t.n] = body;
+      ++t.n;
     }
-    CK(launch_gather(g, s, sm));
+    if (bytes > body)
+      CK(cudaMemcpyAsync(reinterpret_cast<char *>(d) + body, reinterpret_cast<const char *>(shard[i]) + body,
+                         (size_t)(bytes - body), cudaMemcpyDeviceToDevice, s));
   }
+  if (copy_engine == 2) CK(launch_gather(g, s, sm));
+  else CK(launch_bulk_segs(t, s, sm));
 }
 
 extern "C" mlf_status mlf_gather(int32_t device, float *dst, int32_t n, const float *const *shard,
@@ -1039,19 +1049,27 @@ extern "C" mlf_status mlf_distribute_phase(mlf_ctx *c, const mlf_dist_out *p, in
         ++c->launches;
       }
       if (c->ev_phase) CK(cudaEventRecord(c->ev_phase, c->stream));
+      // a GPU without a phase-2 hop is done here (its window must not include the host
+      // barrier between the phases)
+      CK(cudaEventRecord(c->ev_stop, c->stream));
+      c->pending = true;
+      c->dist_p1 = true;
     }
     if (phase & MLF_PHASE_COMMIT) {
-      for (auto e : c->peer_events) CK(cudaStreamWaitEvent(c->stream, e, 0));
       record_start(c);
       if (src >= 0) {                             // TMA bulk copy of the distributor's view
+        for (auto e : c->peer_events) CK(cudaStreamWaitEvent(c->stream, e, 0));
         const int64_t bytes = c->cfg.model_elems * 4, body = bytes & ~int64_t(15);
         CK(launch_bulk_copy(view[r], view[src], body, c->stream, c->sm_count));
         ++c->launches;
         if (bytes > body)
           CK(cudaMemcpyAsync(reinterpret_cast<char *>(view[r]) + body, reinterpret_cast<const char *>(view[src]) + body,
                              (size_t)(bytes - body), cudaMemcpyDeviceToDevice, c->stream));
+        CK(cudaEventRecord(c->ev_stop, c->stream));
+      } else if (!c->dist_p1) {
+        CK(cudaEventRecord(c->ev_stop, c->stream));
       }
-      CK(cudaEventRecord(c->ev_stop, c->stream));
+      c->dist_p1 = false;
       c->started = false;
       c->pending = true;
     }

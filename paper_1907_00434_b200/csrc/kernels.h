@@ -84,6 +84,18 @@ struct GatherArgs {
 };
 cudaError_t launch_gather(const GatherArgs &a, cudaStream_t s, int sm_count);
 
+// TMA bulk copies of up to kMaxShards (dst, src, bytes) segments in one launch: 16 KB chunks
+// global -> shared -> global, 12 in flight per SM.  Pointers and sizes 16-byte aligned.
+constexpr int kBulkChunk = 16384;
+struct BulkSegs {
+  int32_t n;
+  int64_t cstart[kMaxShards + 1];  // prefix sums of the segments' chunk counts
+  char *dst[kMaxShards];
+  const char *src[kMaxShards];
+  int64_t bytes[kMaxShards];
+};
+cudaError_t launch_bulk_segs(const BulkSegs &a, cudaStream_t s, int sm_count);
+
 // host-side splitmix64 key derivation (same definition as synthgen.stream_key)
 uint64_t synth_stream_key(uint64_t seed, uint64_t kind, uint64_t a, uint64_t b);
 

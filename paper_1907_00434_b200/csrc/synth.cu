@@ -94,58 +94,81 @@ __global__ void __launch_bounds__(256) gather_kernel(const __grid_constant__ Gat
 // chunks global -> shared (cp.async.bulk ... mbarrier::complete_tx) -> global (bulk store),
 // kStages chunks in flight per SM.  Used to measure what TMA-driven peer reads can reach.
 namespace bulkcopy {
-constexpr int kChunk = 16384, kStages = 12;
+constexpr int kChunk = kBulkChunk, kStages = 12;
 __device__ __forceinline__ uint32_t saddr(const void *p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 }  // namespace bulkcopy
 
-__global__ void __launch_bounds__(32, 1) bulk_copy_kernel(char *dst, const char *src, int64_t bytes) {
+__global__ void __launch_bounds__(32, 1) bulk_copy_kernel(const __grid_constant__ BulkSegs a) {
   using namespace bulkcopy;
   extern __shared__ __align__(128) uint8_t sm[];
   uint64_t *full = reinterpret_cast<uint64_t *>(sm + (size_t)kStages * kChunk);
   if (threadIdx.x != 0) return;
   for (int s = 0; s < kStages; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(saddr(&full[s])));
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  const int64_t n_chunks = (bytes + kChunk - 1) / kChunk;
+  // round i of this CTA works on segment i % n, chunk (i / n) * gridDim.x + blockIdx.x of it:
+  // every CTA interleaves the segments (a gather's local shard and its NVLink shards are read
+  // at the same time instead of one after the other)
+  int64_t kmax = 0;
+  for (int j = 0; j < a.n; ++j) kmax = max(kmax, a.cstart[j + 1] - a.cstart[j]);
+  const int64_t rounds = (int64_t)a.n * ((kmax + gridDim.x - 1) / gridDim.x);
+  auto next = [&](int64_t i) -> int64_t {          // first round >= i with a chunk for this CTA
+    for (; i < rounds; ++i) {
+      const int j = (int)(i % a.n);
+      if ((i / a.n) * gridDim.x + blockIdx.x < a.cstart[j + 1] - a.cstart[j]) return i;
+    }
+    return rounds;
+  };
+  auto locate = [&](int64_t i, int &j, int64_t &off, uint32_t &len) {
+    j = (int)(i % a.n);
+    off = ((i / a.n) * gridDim.x + blockIdx.x) * kChunk;
+    const int64_t rest = a.bytes[j] - off;
+    len = (uint32_t)(rest < kChunk ? rest : kChunk);
+  };
   // issue loads for up to kStages chunks, then per chunk: wait load, store it, refill the stage
-  int64_t c_load = blockIdx.x, c_store = blockIdx.x;
+  int64_t i_load = next(0), i_store = i_load;
   uint32_t L = 0, S = 0;
-  auto issue_load = [&](int64_t c, uint32_t stage) {
-    const uint32_t len = (uint32_t)((bytes - c * kChunk) < kChunk ? (bytes - c * kChunk) : kChunk);
+  auto issue_load = [&](int64_t i, uint32_t stage) {
+    int j;
+    int64_t off;
+    uint32_t len;
+    locate(i, j, off, len);
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(&full[stage])), "r"(len)
                  : "memory");
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                      saddr(sm + (size_t)stage * kChunk)),
-                 "l"(src + c * kChunk), "r"(len), "r"(saddr(&full[stage]))
+                 "l"(a.src[j] + off), "r"(len), "r"(saddr(&full[stage]))
                  : "memory");
   };
-  for (; L < (uint32_t)kStages && c_load < n_chunks; ++L, c_load += gridDim.x) issue_load(c_load, L);
-  for (; c_store < n_chunks; c_store += gridDim.x, ++S) {
+  for (; L < (uint32_t)kStages && i_load < rounds; ++L, i_load = next(i_load + 1)) issue_load(i_load, L);
+  for (; i_store < rounds; i_store = next(i_store + 1), ++S) {
     const uint32_t stage = S % kStages, parity = (S / kStages) & 1;
     asm volatile(
         "{\n\t.reg .pred p;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W_%=;\n}" ::"r"(
             saddr(&full[stage])),
         "r"(parity)
         : "memory");
-    const uint32_t len =
-        (uint32_t)((bytes - c_store * kChunk) < kChunk ? (bytes - c_store * kChunk) : kChunk);
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + c_store * kChunk),
+    int j;
+    int64_t off;
+    uint32_t len;
+    locate(i_store, j, off, len);
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(a.dst[j] + off),
                  "r"(saddr(sm + (size_t)stage * kChunk)), "r"(len)
                  : "memory");
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-    if (c_load < n_chunks) {
+    if (i_load < rounds) {
       // the stage is refilled only after its bulk store has read it
       asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-      issue_load(c_load, stage);
-      c_load += gridDim.x;
+      issue_load(i_load, stage);
+      i_load = next(i_load + 1);
       ++L;
     }
   }
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-cudaError_t launch_bulk_copy(void *dst, const void *src, int64_t bytes, cudaStream_t s, int sm_count) {
+cudaError_t launch_bulk_segs(const BulkSegs &a, cudaStream_t s, int sm_count) {
   using namespace bulkcopy;
-  if (bytes <= 0) return cudaSuccess;
+  if (a.n <= 0 || a.cstart[a.n] <= 0) return cudaSuccess;
   const size_t smem = (size_t)kStages * kChunk + kStages * sizeof(uint64_t);
   static bool init = false;
   if (!init) {
@@ -153,8 +176,20 @@ cudaError_t launch_bulk_copy(void *dst, const void *src, int64_t bytes, cudaStre
     if (e != cudaSuccess) return e;
     init = true;
   }
-  bulk_copy_kernel<<<sm_count, 32, smem, s>>>(static_cast<char *>(dst), static_cast<const char *>(src), bytes);
+  bulk_copy_kernel<<<sm_count, 32, smem, s>>>(a);
   return cudaGetLastError();
+}
+
+cudaError_t launch_bulk_copy(void *dst, const void *src, int64_t bytes, cudaStream_t s, int sm_count) {
+  BulkSegs a{};
+  if (bytes <= 0) return cudaSuccess;
+  a.n = 1;
+  a.dst[0] = static_cast<char *>(dst);
+  a.src[0] = static_cast<const char *>(src);
+  a.bytes[0] = bytes;
+  a.cstart[0] = 0;
+  a.cstart[1] = (bytes + bulkcopy::kChunk - 1) / bulkcopy::kChunk;
+  return launch_bulk_segs(a, s, sm_count);
 }
 
 cudaError_t launch_gather(const GatherArgs &a, cudaStream_t s, int sm_count) {

@@ -505,8 +505,9 @@ def copy_kernel(device: int, dst_ptr: int, src_ptr: int, nbytes: int, stream=Non
     _check(_lib.mlf_copy_kernel(device, dst_ptr, src_ptr, int(nbytes), stream))
 
 
-def gather(device: int, dst_ptr: int, shard_ptrs, begins, elems, copy_engine: bool = False, stream=None):
-    """mlf_gather: the whole model from its shards (local or mapped peer pointers)."""
+def gather(device: int, dst_ptr: int, shard_ptrs, begins, elems, copy_engine: int = 0, stream=None):
+    """mlf_gather: the whole model from its shards (local or mapped peer pointers).
+    copy_engine: 0 TMA bulk copies, 1 copy engine, 2 SM 128-bit peer loads."""
     n = len(shard_ptrs)
     sp = (_p * max(n, 1))(*shard_ptrs)
     b, e = _arr(begins, np.int64), _arr(elems, np.int64)

@@ -354,6 +354,53 @@ class DistributionRun:
         self.mapper.close()
 
 
+def bench_distribution(S: int, rank: int, world: int, local: int, ctrl, b_nv: float, steps: int = 5,
+                       flush=None) -> dict:
+    """NEXT-4: every GPU's view receives the whole model (S fp32) along the plan's tree.
+    Device time, max over ranks, best of `steps`; roofline = the busiest GPU's NVLink
+    ingress/egress of the executed hops at b_nv."""
+    G = world
+    run = DistributionRun(S, rank, world, local, ctrl)
+    reqs = [g for g in range(G) for _ in range(64 // G)]
+    B = int(NV_GUIDE_GBPS * 1e9)
+    plans = {
+        "uniform": run.plan([B] * G, [B] * G, reqs, list(range(G))[::-1]),
+        "degraded_gpu0_egress": run.plan([B // 10] + [B] * (G - 1), [B] * G, reqs, [(j + 1) % G for j in range(G)]),
+        "all_via_gpu1": {"order": list(range(len(reqs))), "group": [1] * len(reqs), "n_direct": 0, "n_groups": 1,
+                         "group_node": [1 % G], "t_total_ns": 0},
+    }
+    out = {}
+    for name, dp in plans.items():
+        best = None
+        srcs = None
+        for _ in range(steps):
+            src, ms = run.run(dp, reqs, flush=flush)
+            best = ms if best is None else min(best, ms)
+            allsrc = [None] * world
+            dist.all_gather_object(allsrc, src, group=ctrl)
+            srcs = allsrc
+        # executed hops: gathers pull every remote shard, copies pull a whole view
+        nin, nout = [0] * G, [0] * G
+        for r, sr in enumerate(srcs):
+            if sr == -1:
+                for j, (_, n) in enumerate(run.shards):
+                    if j != r:
+                        nin[r] += n * 4
+                        nout[j] += n * 4
+            elif sr >= 0:
+                nin[r] += S * 4
+                nout[sr] += S * 4
+        t_roof = max(max(nin), max(nout)) / (b_nv * 1e9)
+        out[name] = {"ms": round(best, 4), "groups": dp["n_groups"], "n_direct": dp["n_direct"],
+                     "sources": srcs, "plan_t_total_ms": round(dp["t_total_ns"] / 1e6, 4),
+                     "roofline_frac": round(t_roof * 1e3 / best, 4) if best else None}
+    run.close()
+    out["model_bytes"] = S * 4
+    out["what"] = ("mlf_plan_distribution + mlf_distribute_phase: views filled from the servers (gather) or "
+                   "from a distributor's view (TMA bulk copy); device ms, max over ranks, best of runs")
+    return out
+
+
 def w_checksum(w: torch.Tensor) -> int:
     """Exact integer digest of an fp32 tensor's bits (for bitwise comparisons across runs)."""
     return int(w.view(torch.int32).to(torch.int64).sum().item())
@@ -541,6 +588,9 @@ def run_bench_multi(a):
         # NEXT-3: AllReduce via push/get vs NCCL all_reduce, ResNet-50-sized buffer per GPU
         from .allreduce import bench_allreduce
         ar = bench_allreduce(25_600_000, rank, world, local, ctrl, steps=5, warmup=2, flush=l2_flush)
+    dv = None
+    if not a.no_variants:
+        dv = bench_distribution(cfg0["S"], rank, world, local, ctrl, b_nv, steps=5, flush=l2_flush)
     e2e = None
     if not a.no_e2e:
         e2e = e2e_multi(cfgs.config(cid, G=world, tau=a.tau, dtype=a.dtype), rank, world, local, ctrl,
@@ -596,6 +646,8 @@ def run_bench_multi(a):
         line.setdefault("variants", {})["nccl_sendrecv_then_fold"] = nb
     if ar is not None:
         line.setdefault("variants", {})["allreduce_push_get_vs_nccl"] = ar
+    if dv is not None:
+        line.setdefault("variants", {})["model_distribution"] = dv
     if e2e is not None:
         line["e2e"] = e2e
     print(json.dumps(line), flush=True)

@@ -238,6 +238,25 @@ def test_denominator_copy_kernels(nbytes):
         assert torch.equal(dst, src), fn.__name__
 
 
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_gather_modes_exact(mode):
+    # get of the whole model from shards (TMA bulk / copy engine / SM loads): ragged shards,
+    # an empty one, tails that are not 16-byte multiples, > 1 chunk per shard
+    dev = torch.device("cuda", 0)
+    S = 3 * 16384 + 1237
+    src = torch.randn(S, device=dev)
+    cuts = [0, 64, 64, 20000 + 7, 33333, S]        # shard begins (64-aligned except the ragged ones)
+    begins, elems, ptrs = [], [], []
+    for b, e in zip(cuts[:-1], cuts[1:]):
+        begins.append(b)
+        elems.append(e - b)
+        ptrs.append(src[b:].data_ptr() if e > b else src.data_ptr())
+    dst = torch.full((S,), float("nan"), device=dev)
+    m.gather(0, dst.data_ptr(), ptrs, begins, elems, copy_engine=mode, stream=torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert torch.equal(dst.view(torch.int32), src.view(torch.int32))
+
+
 def test_invalid_plan_rejected_without_device_work():
     dev = torch.device("cuda", 0)
     S = 64
