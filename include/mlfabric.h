@@ -36,7 +36,7 @@
  *     share its NVLink egress, exactly as the paper's co-located workers share a
  *     host NIC.
  *
- * Readings of silent or ambiguous passages (R1-R20) are listed in DESIGN.md §3.
+ * Readings of silent or ambiguous passages (R1-R25) are listed in DESIGN.md §3.
  */
 #ifndef MLFABRIC_H
 #define MLFABRIC_H
