@@ -286,6 +286,20 @@ def measure_nvlink(device: int, rank: int, world: int, ctrl, nbytes: int = 1 << 
             ms = max_over_ranks(s0.elapsed_time(s1), ctrl)
             best = max(best, nbytes / (ms / 1e3) / 1e9)
         out[name] = round(best, 1)
+    # one-way: only rank 0 pulls (from rank 1), every other link idle
+    for name, fn in (("one_way_copy_engine", m.copy_engine), ("one_way_tma_bulk", m.copy_bulk)):
+        best = 0.0
+        for _ in range(3):
+            dist.barrier(group=ctrl)
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record()
+            if rank == 0:
+                fn(device, dst.data_ptr(), peer, nbytes, torch.cuda.current_stream().cuda_stream)
+            s1.record()
+            s1.synchronize()
+            ms = max_over_ranks(s0.elapsed_time(s1), ctrl)
+            best = max(best, nbytes / (ms / 1e3) / 1e9)
+        out[name] = round(best, 1)
     dist.barrier(group=ctrl)
     mp.close()
     del src, dst
@@ -531,6 +545,7 @@ def run_bench_multi(a):
     # denominator: the best of this run's two measurements and the pool's measured peer copy
     # (770 GB/s per direction, B200_PROFILING.md) — never the slower of them
     b_nv = max(NV_GUIDE_GBPS, nv_meas["copy_engine"], nv_meas["sm_peer_loads"], nv_meas["tma_bulk"])
+    b_nv_one_way = max(b_nv, nv_meas["one_way_copy_engine"], nv_meas["one_way_tma_bulk"])
     flush_w = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     flush_r = torch.ones(64 << 20, dtype=torch.float32, device=dev)
 
@@ -629,6 +644,8 @@ def run_bench_multi(a):
                      "peak_source": ("max(770 GB/s pool peer copy [B200_PROFILING.md], this run's copy-engine "
                                      "and SM peer-load ingress)" if nv_bound else peak_src),
                      "plan_relative_t_roof_ms": round(t_roof * 1e3 / len(recs), 4),
+                     "frac_vs_one_way_peak": (round(t_roof / T * b_nv / b_nv_one_way, 4) if nv_bound else None),
+                     "one_way_peak": b_nv_one_way,
                      "kernel": f"fused_commit_{a.kernel}"},
         "nvlink_measured_GBps": nv_meas,
         "planner_ms": round(sum(r["plan_ms"] for r in recs) / len(recs), 3),
