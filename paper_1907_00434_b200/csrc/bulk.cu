@@ -52,6 +52,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Stage reuse is a write-after-read across proxies: the consumers read a stage with generic
+// loads, the producer then overwrites it with an async-proxy bulk copy.  The empty-barrier
+// acquire orders the reads only for the generic proxy; fence.proxy.async extends the order to
+// the bulk copy (without it, stages were measurably overwritten early under concurrent
+// copy-engine traffic: scripts/dbg_concurrent.py).
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_addr(dst)),
@@ -102,7 +108,10 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_bulk(const __grid_co
         const uint32_t cnt = (uint32_t)(n_bulk - e0 < kTile ? n_bulk - e0 : kTile);
         for (int j = -1; j < a.n_ops; ++j, ++L) {
           const uint32_t s = L % kStages;
-          if (L >= (uint32_t)kStages) mbar_wait(&empty[s], ((L / kStages) & 1) ^ 1);
+          if (L >= (uint32_t)kStages) {
+            mbar_wait(&empty[s], ((L / kStages) & 1) ^ 1);
+            fence_proxy_async_smem();
+          }
           const void *src;
           uint32_t bytes;
           if (j < 0) {
@@ -251,7 +260,10 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_momentum(const __gri
         const uint32_t cnt = (uint32_t)(n_bulk - e0 < kTile ? n_bulk - e0 : kTile);
         for (int j = -2; j < a.n_ops; ++j, ++L) {
           const uint32_t s = L % kStages;
-          if (L >= (uint32_t)kStages) mbar_wait(&empty[s], ((L / kStages) & 1) ^ 1);
+          if (L >= (uint32_t)kStages) {
+            mbar_wait(&empty[s], ((L / kStages) & 1) ^ 1);
+            fence_proxy_async_smem();
+          }
           const void *src;
           uint32_t bytes = cnt * 4;
           if (j == -2) {
@@ -415,16 +427,13 @@ static cudaError_t launch_tile(const CommitArgs &a, cudaStream_t s, int sm_count
   return cudaGetLastError();
 }
 
-// Tile size (elements) per bulk copy: MLF_BULK_TILE in {2048, 4096, 8192}; the ring is
+// Tile size (elements) per bulk copy: MLF_BULK_TILE in {1024, 2048, 4096, 8192}; the ring is
 // always 192 KB.  Default 4096 (16 KB per copy): measured best on one B200 (99.7% of the
 // HBM copy roofline at config 2, tau 4, vs 93.5% at 2048 and 8192); NVLink-bound runs
 // are insensitive to the tile size.
 cudaError_t launch_commit_bulk(const CommitArgs &a, cudaStream_t s, int sm_count) {
-  static int forced = -1;
-  if (forced < 0) {
-    const char *e = getenv("MLF_BULK_TILE");
-    forced = e ? atoi(e) : 0;
-  }
+  const char *env = getenv("MLF_BULK_TILE");           // read per launch (tests switch it)
+  const int forced = env ? atoi(env) : 0;
   // adaptive tile: the largest of 4096 / 2048 / 1024 elements that still deals >= 32 tiles to
   // every persistent CTA, so the last wave's imbalance stays small (a shard of 6.4M elements,
   // config 4 at 4 GPUs: 76.8% of the NVLink roofline at 2048 vs 70.8% at 4096)

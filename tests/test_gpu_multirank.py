@@ -29,6 +29,13 @@ def test_two_ranks_bitwise(cid, extra):
     assert "MULTIGPU_OK fold" in out and "MULTIGPU_OK tree" in out and "MULTIGPU_OK staged" in out
 
 
+def test_two_ranks_full_size_config3():
+    # BASELINE config 3 at its stated size (64 workers x 143,667,240 fp32 = VGG-19) in the
+    # bench's launch configuration (2 PS shards, bulk kernel), sampled outputs vs the oracle
+    out = _run(2, "--cid", "3", "--S", "143667240", "--steps", "2", timeout=1200)
+    assert "MULTIGPU_OK fold" in out and "MULTIGPU_OK tree" in out and "MULTIGPU_OK staged" in out
+
+
 def test_two_ranks_staged_minimum_chunk():
     # copy-engine staging with a 2 MiB buffer: 4096-element chunks, many of them, ragged tail
     out = _run(2, "--cid", "3", "--S", "300007", "--modes", "staged", "--stage-mib", "2", "--workers", "32")

@@ -137,6 +137,63 @@ def test_random_plans_bitwise(dtype, impl):
             assert np.all(np.isnan(b))                     # no replica write
 
 
+@pytest.mark.parametrize("tile", [1024, 2048, 4096, 8192])
+@pytest.mark.parametrize("dtype", [sg.DTYPE_F32, sg.DTYPE_BF16])
+def test_bulk_tiles_bitwise(tile, dtype):
+    # every tile instantiation the adaptive choice can pick (1024 / 2048 / 4096) and the
+    # 8192 override, with several tiles per CTA, ragged last tiles and a mirror boundary
+    rng = np.random.default_rng(tile + dtype)
+    os.environ["MLF_BULK_TILE"] = str(tile)
+    try:
+        for S in (tile * 148 * 3 + 4 * 97 + 5, 1_000_003):
+            W = int(rng.integers(3, 20))
+            p = random_plan(rng, W, n_commit=W, boundary=1)
+            w, b, _, _ = gpu_run(S, W, dtype, p, backup=True, impl="bulk")
+            wr, br = oracle_run(S, dtype, p)
+            assert np.array_equal(bits(w), bits(wr)), (tile, S)
+            assert np.array_equal(bits(b), bits(br)), (tile, S)
+    finally:
+        del os.environ["MLF_BULK_TILE"]
+
+
+@pytest.mark.parametrize("tile", [1024, 2048, 4096])
+def test_bulk_commit_under_concurrent_copy_engine_traffic(tile):
+    # regression: without fence.proxy.async between the empty-barrier wait and the bulk copy
+    # that reuses a stage, concurrent copy-engine traffic (unrelated buffers, another stream)
+    # let stages be overwritten before the consumers had read them (scripts/dbg_concurrent.py)
+    dev = torch.device("cuda", 0)
+    S, W = 16_777_216, 32
+    rng = np.random.default_rng(tile)
+    p = random_plan(rng, W, n_commit=W, boundary=-1)
+    big_src = torch.ones(1 << 28, dtype=torch.float32, device=dev)
+    big_dst = torch.empty_like(big_src)
+    side = torch.cuda.Stream()
+    os.environ["MLF_BULK_TILE"] = str(tile)
+    try:
+        os.environ["MLF_COMMIT_IMPL"] = "bulk"
+        slots = [torch.empty(S, dtype=torch.float32, device=dev) for _ in range(W)]
+        for w, t in enumerate(slots):
+            m.synth_fill(0, t.data_ptr(), S, dtype=sg.DTYPE_F32, seed=SEED, kind=1, a=w, b=0)
+        wt = torch.empty(S, dtype=torch.float32, device=dev)
+        m.synth_fill(0, wt.data_ptr(), S, dtype=m.MLF_F32, seed=SEED, kind=2)
+        torch.cuda.synchronize()
+        ctx = m.Context(device=0, model_shard=wt, update_slots=slots, lr=0.01, model_elems=S,
+                        stream=torch.cuda.current_stream().cuda_stream)
+        for w in range(W):
+            ctx.submit(w, 0, 0, 1.0)
+        for _ in range(8):
+            m.copy_engine(0, big_dst.data_ptr(), big_src.data_ptr(), big_src.numel() * 4, side.cuda_stream)
+        ctx.execute(m.plan_from_dict(p))
+        ctx.sync()
+        torch.cuda.synchronize()
+        ctx.close()
+    finally:
+        del os.environ["MLF_BULK_TILE"]
+    idx = np.unique(np.concatenate([rng.integers(0, S, 200_000), np.arange(S - 9, S)]))
+    wr, _ = oracle_run(S, sg.DTYPE_F32, p, idx=idx)
+    assert np.array_equal(bits(wt.cpu().numpy()[idx]), bits(wr))
+
+
 @pytest.mark.parametrize("impl", IMPLS)
 def test_exact_variant_any_order(impl):
     rng = np.random.default_rng(3)
