@@ -6,7 +6,7 @@ import synthgen as sg
 from oracle.bruteforce import best_order_sum, best_order_sum_recursive, order_t_ens
 from oracle.checks import check_plan
 from oracle.netmodel import Net
-from oracle.ordering import DROP_EXPIRED, DROP_LOOKAHEAD, Item, deadline, order_final, order_sjf
+from oracle.ordering import DROP_EXPIRED, DROP_LOOKAHEAD, Item, deadline, order_final, order_sjf, t_en_server
 from oracle.plan import plan
 from tests.instances import random_instance, to_oracle
 
@@ -99,10 +99,35 @@ def test_expired_at_batch_start_and_due_set_argmin():
     assert res2.order[0] == 1 and res2.drop_reason[0] == DROP_EXPIRED
 
 
-def test_lookahead_never_fires_on_sjf_picks():
-    # R5: reservations only delay, so for an SJF pick t_en(g*) <= t_en(g°, NW').
+def test_lookahead_can_fire_on_an_sjf_pick_with_shard_components():
+    # R5's no-op argument needs t_en to be monotone in the residual.  A single transfer is;
+    # an App. B.2 send whose components are reserved one after another is not.  Worked by
+    # hand (units of 1e9 bytes and 1e9 B/s): W0 up 2, pair W0->B 1, A down 2; W1 up 1.
+    # g0 (4, from W0): c->A at 2 on [0,1], then c->B at 1 on [1,3] -> t_en 3.
+    # g1 (2.8, from W1): c->A at 1 on [0,1.4], c->B on [1.4,2.8]      -> t_en 2.8 (SJF pick).
+    # After g1's reservation A's residual is 1 on [0,1.4], so g0's first component no
+    # longer takes all of W0's up-link: c->A ends at 1.7, c->B runs at 1 from 0 and ends at
+    # 2.3 < 2.8 -> Alg. 2's look-ahead drops the SJF pick g1 (listing line 10).
+    G = 10**9
+    n = 4
+    bw = [0] * (n * n)
+    bw[0 * n + 3] = 1 * G
+    net = Net(n, [2 * G, 1 * G, 0, 0], [0, 0, 2 * G, 0], bw)
+    batch = [Item(0, 4 * G, 0), Item(1, 28 * G // 10, 0)]
+    s0, nw0 = t_en_server(net, batch[0], [2, 3], [1, 1])
+    s1, nw1 = t_en_server(net, batch[1], [2, 3], [1, 1])
+    assert (s0.t_en, s1.t_en) == (3 * S, 28 * S // 10)
+    s0_after, _ = t_en_server(nw1, batch[0], [2, 3], [1, 1])
+    assert s0_after.t_en == 23 * S // 10
+    res = order_final(net, batch, [2, 3], [1, 1], 100, 0)
+    assert res.drop_reason == [0, DROP_LOOKAHEAD] and res.order == [0]
+
+
+def test_lookahead_never_fires_on_sjf_picks_single_server():
+    # R5: with one server a send is one transfer, and reservations only delay it, so for an
+    # SJF pick t_en(g*) <= t_en(g°, NW'): the look-ahead never fires.
     for i in range(200):
-        inst = random_instance(21, i, max_n=7, replica=False)
+        inst = random_instance(21, i, max_n=7, max_servers=1, replica=False)
         for b in inst.batch:
             b["version"] = inst.v_init                    # dl = tau for all
         inst.tau_max = 100                                # never due before the end

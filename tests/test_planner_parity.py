@@ -107,3 +107,15 @@ def test_library_exports_every_declared_symbol():
     assert declared == set(m.EXPORTS)
     for s in declared:
         assert hasattr(m.lib(), s)
+
+
+def test_lookahead_fires_on_sjf_pick_through_cpp():
+    # the multi-component instance of tests/test_oracle_ordering.py, through mlf_plan
+    G = 10**9
+    n = 4
+    bw = [0] * (n * n)
+    bw[0 * n + 3] = 1 * G
+    batch = [dict(node=0, size=4 * G, version=0, t_avail=0, norm=0.0),
+             dict(node=1, size=28 * G // 10, version=0, t_avail=0, norm=0.0)]
+    p = m.plan(n, [2 * G, 1 * G, 0, 0], [0, 0, 2 * G, 0], batch, [2, 3], bw=bw, tau_max=100)
+    assert p["drop_reason"] == [0, 2] and p["order"] == [0]
