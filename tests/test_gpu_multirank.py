@@ -83,7 +83,8 @@ def test_all_gpus_if_several():
     n = torch.cuda.device_count()
     if n < 4:
         pytest.skip("needs >= 4 GPUs")
-    out = _run(4, "--cid", "5", "--S", "2000011")
+    # 64 of config 5's 256 workers: the Python oracle plans every batch of every mode
+    out = _run(4, "--cid", "5", "--S", "2000011", "--workers", "64", timeout=900)
     assert "MULTIGPU_OK fold" in out and "MULTIGPU_OK tree" in out and "MULTIGPU_OK staged" in out
     cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", "--nnodes=1", "--nproc-per-node=4",
            os.path.join(HERE, "distribute_check.py"), "--S", "2000011"]
