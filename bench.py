@@ -30,6 +30,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+# BASELINE.json's metric, verbatim (the roofline fraction is the line's `roofline` object)
+METRIC = "aggregated update GB/s committed (device-timed, max over ranks), % HBM/NVLink roofline"
 HBM_FALLBACK = 6650.0
 
 
@@ -159,7 +161,7 @@ def run_reference(a):
     val = tot_bytes / tot_s / 1e9
     sample = (f"oracle plan of {W_s} of {cfg['W']} updates per batch + numpy numerics on the first {S_sample} of "
               f"{cfg['S']} elements per update")
-    line = {"impl": "reference", "metric": "aggregated update GB/s committed (device-timed, max over ranks)",
+    line = {"impl": "reference", "metric": METRIC,
             "value": round(val, 4),
             "unit": "GB/s", "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": round(tot_s / a.steps * 1e3, 3), "higher_is_better": True,
@@ -334,7 +336,7 @@ def run_single(a):
         key = f"config{cid}_tau{cfg['tau']}_{a.dtype}_{a.kernel}"
         traffic = tj.get(key)
     line = {
-        "metric": "aggregated update GB/s committed (device-timed, max over ranks)",
+        "metric": METRIC,
         "value": round(value, 2), "unit": "GB/s", "n_gpus": 1, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": round(T / a.steps, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": a.dtype, "data": "synthetic",

@@ -533,7 +533,7 @@ def e2e_multi(cfg: dict, rank: int, world: int, local: int, ctrl, steps: int) ->
 
 def run_bench_multi(a):
     """bench.py at N > 1: config 3 (64 workers, VGG-19-sized updates) over N PS shards."""
-    from bench import Clocks, cpu_baseline_oracle, hbm_peak  # noqa: F401  (same process)
+    from bench import METRIC, Clocks, cpu_baseline_oracle, hbm_peak  # noqa: F401  (same process)
 
     rank, world, local, ctrl = init_dist()
     torch.cuda.set_device(local)
@@ -624,7 +624,7 @@ def run_bench_multi(a):
     hbm_bytes = sum(max(r["tr"]["hbm"]) for r in recs)
     nv_bound = nv_bytes / b_nv > hbm_bytes / peak_hbm
     line = {
-        "metric": "aggregated update GB/s committed (device-timed, max over ranks)",
+        "metric": METRIC,
         "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": round(T * 1e3 / len(recs), 4), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": a.dtype, "data": "synthetic",
