@@ -393,7 +393,116 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_momentum(const __gri
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// Tree reduce: the fp32 aggregate of a group on its
+// aggregator's GPU, acc = ((x1 + x2) + x3) + ... in O(U) order, bf16 widened exactly.
+// The same TMA ring as the commit, without w: the producer streams every member's tile,
+// the consumers fold it from shared memory and store the aggregate tile.
+template <int kTile, int kStages>
+__global__ void __launch_bounds__(kThreads, 1) tree_reduce_bulk(const __grid_constant__ ReduceArgs a) {
+  constexpr int kStageBytes = kTile * 4;
+  constexpr int kChunks = kTile / 4 / kConsumers;
+  static_assert(kChunks >= 1 && kTile % (4 * kConsumers) == 0, "tile must be a multiple of 4 * consumers");
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)kStages * kStageBytes);
+  uint64_t *empty = full + kStages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t n_bulk = a.n & ~int64_t(7);
+  const int64_t n_tiles = (n_bulk + kTile - 1) / kTile;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kConsumerWarps) {
+    if (lane == 0) {
+      uint32_t L = 0;
+      for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        const int64_t e0 = t * kTile;
+        const uint32_t cnt = (uint32_t)(n_bulk - e0 < kTile ? n_bulk - e0 : kTile);
+        for (int j = 0; j < a.n_ops; ++j, ++L) {
+          const uint32_t s = L % kStages;
+          if (L >= (uint32_t)kStages) {
+            mbar_wait(&empty[s], ((L / kStages) & 1) ^ 1);
+            fence_proxy_async_smem();
+          }
+          const bool bf = a.flag[j] & kOpBf16;
+          const void *src = bf ? (const void *)(static_cast<const uint16_t *>(a.op[j]) + a.src_off + e0)
+                               : (const void *)(static_cast<const float *>(a.op[j]) + a.src_off + e0);
+          const uint32_t bytes = cnt * (bf ? 2 : 4);
+          mbar_expect_tx(&full[s], bytes);
+          bulk_g2s(smem + (size_t)s * kStageBytes, src, bytes, &full[s]);
+        }
+      }
+    }
+  } else {
+    const int tid = threadIdx.x;
+    uint32_t L = 0;
+    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      const int64_t e0 = t * kTile;
+      const int cnt = (int)(n_bulk - e0 < kTile ? n_bulk - e0 : kTile);
+      float4 x[kChunks];
+      for (int j = 0; j < a.n_ops; ++j, ++L) {
+        const uint32_t s = L % kStages;
+        const bool bf = a.flag[j] & kOpBf16;
+        mbar_wait(&full[s], (L / kStages) & 1);
+        const uint8_t *st = smem + (size_t)s * kStageBytes;
+#pragma unroll
+        for (int k = 0; k < kChunks; ++k) {
+          const int c = tid + k * kConsumers;
+          if (c * 4 < cnt) {
+            const float4 u = bf ? widen_bf16x4(reinterpret_cast<const uint2 *>(st)[c])
+                                : reinterpret_cast<const float4 *>(st)[c];
+            x[k] = j == 0 ? u : add4(x[k], u);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+      }
+#pragma unroll
+      for (int k = 0; k < kChunks; ++k) {
+        const int c = tid + k * kConsumers;
+        if (c * 4 < cnt) __stcs(reinterpret_cast<float4 *>(a.out + e0) + c, x[k]);
+      }
+    }
+    const int64_t tail = a.n - n_bulk;                // ragged tail (< 8 elements) on CTA 0
+    if (blockIdx.x == 0 && tid < tail) {
+      const int64_t e = n_bulk + tid;
+      float xv = 0.f;
+      for (int j = 0; j < a.n_ops; ++j) {
+        const float u = (a.flag[j] & kOpBf16)
+                            ? __uint_as_float(uint32_t(static_cast<const uint16_t *>(a.op[j])[a.src_off + e]) << 16)
+                            : static_cast<const float *>(a.op[j])[a.src_off + e];
+        xv = j == 0 ? u : __fadd_rn(xv, u);
+      }
+      a.out[e] = xv;
+    }
+  }
+}
+
 }  // namespace bulk
+
+cudaError_t launch_reduce_bulk(const ReduceArgs &a, cudaStream_t s, int sm_count) {
+  constexpr int kTile = 4096, kStages = 12;
+  constexpr size_t smem = bulk::smem_bytes(kTile, kStages);
+  static bool init = false;
+  if (!init) {
+    cudaError_t e = cudaFuncSetAttribute(bulk::tree_reduce_bulk<kTile, kStages>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    init = true;
+  }
+  if (a.n_ops < 1 || a.n < 1) return cudaSuccess;
+  const int64_t n_tiles = ((a.n & ~int64_t(7)) + kTile - 1) / kTile;
+  int grid = (int)(n_tiles < sm_count ? (n_tiles > 0 ? n_tiles : 1) : sm_count);
+  bulk::tree_reduce_bulk<kTile, kStages><<<grid, bulk::kThreads, smem, s>>>(a);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_commit_momentum(const MomentumArgs &a, cudaStream_t s, int sm_count) {
   constexpr int kTile = 4096, kStages = 12;

@@ -152,7 +152,8 @@ cudaError_t launch_commit(const CommitArgs &a, cudaStream_t s, int sm_count, Com
   return cudaGetLastError();
 }
 
-cudaError_t launch_reduce(const ReduceArgs &a, cudaStream_t s, int sm_count) {
+cudaError_t launch_reduce(const ReduceArgs &a, cudaStream_t s, int sm_count, CommitImpl impl) {
+  if (impl == CommitImpl::kBulk) return launch_reduce_bulk(a, s, sm_count);
   constexpr int kThreads = 256;
   constexpr int kU = 8;
   static int grid = 0;

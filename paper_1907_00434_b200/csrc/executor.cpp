@@ -420,7 +420,7 @@ static void reduce_local_groups(mlf_ctx *c, const mlf_plan_out *p) {
       a.flag[q] = c->cfg.update_dtype == MLF_BF16 ? kOpBf16 : 0;
     }
     record_start(c);
-    CK(launch_reduce(a, c->stream, c->sm_count));
+    CK(launch_reduce(a, c->stream, c->sm_count, c->impl));
     ++c->launches;
   }
 }

@@ -67,7 +67,9 @@ cudaError_t launch_commit_momentum(const MomentumArgs &a, cudaStream_t s, int sm
 
 cudaError_t launch_commit(const CommitArgs &a, cudaStream_t s, int sm_count, CommitImpl impl);
 cudaError_t launch_commit_bulk(const CommitArgs &a, cudaStream_t s, int sm_count);
-cudaError_t launch_reduce(const ReduceArgs &a, cudaStream_t s, int sm_count);
+// tree reduce: TMA ring (kBulk, default) or 128-bit LDG streaming (kLdg)
+cudaError_t launch_reduce(const ReduceArgs &a, cudaStream_t s, int sm_count, CommitImpl impl);
+cudaError_t launch_reduce_bulk(const ReduceArgs &a, cudaStream_t s, int sm_count);
 cudaError_t launch_synth(void *dst, int64_t n, int64_t elem_offset, int dtype, uint64_t key, int kind,
                          int variant, cudaStream_t s);
 cudaError_t launch_copy(void *dst, const void *src, int64_t bytes, cudaStream_t s, int sm_count);

@@ -23,7 +23,8 @@ def _run(nproc, *args, timeout=600):
 
 
 @pytest.mark.parametrize("cid,extra", [(3, []), (4, ["--steps", "3"]), (5, ["--S", "300007", "--workers", "64"]),
-                                        (3, ["--dtype", "bf16", "--kernel", "bulk"])])
+                                        (3, ["--dtype", "bf16", "--kernel", "bulk"]),
+                                        (3, ["--dtype", "bf16", "--kernel", "ldg", "--steps", "1"])])
 def test_two_ranks_bitwise(cid, extra):
     out = _run(2, "--cid", str(cid), *extra)
     assert "MULTIGPU_OK fold" in out and "MULTIGPU_OK tree" in out and "MULTIGPU_OK staged" in out
