@@ -71,13 +71,17 @@ class Pool {
       job_ = &f;
       n_ = n;
       next_.store(0);
-      pending_ = (int)th_.size();
-      ++gen_;
+      pending_.store((int)th_.size());
+      gen_.fetch_add(1, std::memory_order_release);
     }
     cv_.notify_all();
     work();
-    std::unique_lock<std::mutex> g(m_);
-    done_.wait(g, [&] { return pending_ == 0; });
+    // the scans of one ordering step are tens of microseconds: spin before sleeping
+    for (int spin = 0; pending_.load(std::memory_order_acquire) != 0 && spin < kSpin; ++spin) relax();
+    if (pending_.load(std::memory_order_acquire) != 0) {
+      std::unique_lock<std::mutex> g(m_);
+      done_.wait(g, [&] { return pending_.load() == 0; });
+    }
     job_ = nullptr;
     busy_.unlock();
   }
@@ -104,29 +108,38 @@ class Pool {
       (*job_)(i);
     }
   }
+  static void relax() {
+#if defined(__x86_64__)
+    __builtin_ia32_pause();
+#endif
+  }
   void loop() {
     uint64_t seen = 0;
     for (;;) {
+      // spin for the next job (a plan's scans come back to back), then sleep
+      for (int spin = 0; gen_.load(std::memory_order_acquire) == seen && spin < kSpin; ++spin) relax();
       {
         std::unique_lock<std::mutex> g(m_);
-        cv_.wait(g, [&] { return stop_ || gen_ != seen; });
+        cv_.wait(g, [&] { return stop_ || gen_.load() != seen; });
         if (stop_) return;
-        seen = gen_;
+        seen = gen_.load();
       }
       work();
-      {
+      if (pending_.fetch_sub(1, std::memory_order_acq_rel) == 1) {
         std::lock_guard<std::mutex> g(m_);
-        if (--pending_ == 0) done_.notify_one();
+        done_.notify_one();
       }
     }
   }
+  static constexpr int kSpin = 20000;              // ~50-100 us of pause instructions
   std::vector<std::thread> th_;
   std::mutex m_, busy_;
   std::condition_variable cv_, done_;
   const std::function<void(int)> *job_ = nullptr;
-  int n_ = 0, pending_ = 0;
+  int n_ = 0;
+  std::atomic<int> pending_{0};
   std::atomic<int> next_{0};
-  uint64_t gen_ = 0;
+  std::atomic<uint64_t> gen_{0};
   bool stop_ = false;
 };
 
@@ -414,7 +427,7 @@ struct OrderRes {
   std::vector<uint8_t> reason;
 };
 
-static constexpr int kMinParallelEvals = 128;   // component transfers per scan worth a pool dispatch
+static constexpr int kMinParallelEvals = 32;   // component transfers per scan worth a pool dispatch
 
 static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 tau, i64 v_init) {
   const int n = (int)batch.size();
