@@ -491,6 +491,11 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
   };
 
   Pending star;
+  // When g* is kept, the next step's pick at p+1 runs over exactly the look-ahead's
+  // candidates (the unprocessed updates with dl >= p+1) on exactly the look-ahead's
+  // network (NW with g* reserved), so its result is the look-ahead's g° (and t_en):
+  // reusing it halves the scans without changing any decision.
+  int cached = -1;
   for (;;) {
     std::vector<int> keep;
     for (int g : unproc) {
@@ -501,16 +506,18 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
     }
     unproc.swap(keep);
     if (unproc.empty()) break;
-    const int g_star = pick(p, unproc, nullptr);
+    const int g_star = cached >= 0 ? cached : pick(p, unproc, nullptr);
     const i64 t_star = ten[g_star];
+    cached = -1;
     Send s_star;
     send(nw, nullptr, c, c.servers, batch[g_star].node, batch[g_star].size, batch[g_star].t_avail, s_star, star);
     std::vector<int> cands;
     for (int g : unproc)
       if (g != g_star && dl[g] >= p + 1) cands.push_back(g);
     bool drop = false;
+    int g_next = -1;
     if (!cands.empty()) {
-      const int g_next = pick(p + 1, cands, &star);    // on NetUp(NW, g*)
+      g_next = pick(p + 1, cands, &star);              // on NetUp(NW, g*)
       if (t_star > ten[g_next]) drop = true;           // Alg. 2 line 10
     }
     unproc.erase(std::find(unproc.begin(), unproc.end(), g_star));
@@ -521,6 +528,7 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
     res.order.push_back(g_star);
     apply_pending(nw, star);
     ++p;
+    cached = g_next;
   }
   return res;
 }
