@@ -649,6 +649,8 @@ def run_bench_multi(a):
                      "kernel": f"fused_commit_{a.kernel}"},
         "nvlink_measured_GBps": nv_meas,
         "planner_ms": round(sum(r["plan_ms"] for r in recs) / len(recs), 3),
+        "step_ms_p10_p50_p90": [round(float(x), 4) for x in
+                                __import__("numpy").percentile([r["ms"] for r in recs], [10, 50, 90])],
         "gpu_launches": int(kl),
         "clocks": ck.summary(),
     }
