@@ -27,6 +27,7 @@ import json
 import os
 import time
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -649,8 +650,7 @@ def run_bench_multi(a):
                      "kernel": f"fused_commit_{a.kernel}"},
         "nvlink_measured_GBps": nv_meas,
         "planner_ms": round(sum(r["plan_ms"] for r in recs) / len(recs), 3),
-        "step_ms_p10_p50_p90": [round(float(x), 4) for x in
-                                __import__("numpy").percentile([r["ms"] for r in recs], [10, 50, 90])],
+        "step_ms_p10_p50_p90": [round(float(x), 4) for x in np.percentile([r["ms"] for r in recs], [10, 50, 90])],
         "gpu_launches": int(kl),
         "clocks": ck.summary(),
     }
