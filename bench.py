@@ -370,6 +370,11 @@ def run_single(a):
             var["momentum0.9_bulk"] = summarize(r4, T4)
             _, r5, T5, _, _ = measure(32, a.dtype, nv, 3, "bulk", gamma=0.9)
             var["momentum0.9_tau32_bulk"] = summarize(r5, T5)
+            if a.dtype == "f32":
+                # SURVEY §8(d) config 2's bf16 variant: 2-byte updates widened exactly in the kernel
+                for t in (4, 32):
+                    _, r6, T6, _, _ = measure(t, "bf16", nv, 3, "bulk")
+                    var[f"bf16_tau{t}_bulk"] = summarize(r6, T6)
         line["variants"] = var
         os.environ["MLF_COMMIT_IMPL"] = a.kernel
     # e2e through the public API with host buffers
