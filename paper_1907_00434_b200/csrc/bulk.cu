@@ -394,6 +394,150 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_momentum(const __gri
 }
 
 // ---------------------------------------------------------------------------------------
+// The same commit for bf16 operands with 16 KB bulk copies: a tile is kTile = 8192
+// elements, so every bf16 operand tile fills one 16 KB stage and the fp32 w tile spans two.
+// With the fp32 layout (4096-element tiles) bf16 copies are 8 KB and the per-stage hand-off
+// costs show (config 2, tau 32: 86% of the HBM roofline).  Same fold order and roundings.
+template <int kTile, int kStages>
+__global__ void __launch_bounds__(kThreads, 1) fused_commit_bulk_h(const __grid_constant__ CommitArgs a) {
+  constexpr int kStageBytes = kTile * 2;
+  constexpr int kHalf = kTile / 2;                  // fp32 elements per stage
+  constexpr int kChunks = kTile / 4 / kConsumers;   // float4 chunks per consumer thread per tile
+  static_assert(kChunks % 2 == 0 && kTile % (8 * kConsumers) == 0, "tile must split evenly");
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)kStages * kStageBytes);
+  uint64_t *empty = full + kStages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t n_bulk = a.n & ~int64_t(7);
+  const int64_t n_tiles = (n_bulk + kTile - 1) / kTile;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kConsumerWarps) {
+    if (lane == 0) {
+      uint32_t L = 0;
+      for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        const int64_t e0 = t * kTile;
+        const uint32_t cnt = (uint32_t)(n_bulk - e0 < kTile ? n_bulk - e0 : kTile);
+        for (int j = -2; j < a.n_ops; ++j, ++L) {       // j = -2, -1: the two halves of w
+          const uint32_t s = L % kStages;
+          if (L >= (uint32_t)kStages) {
+            mbar_wait(&empty[s], ((L / kStages) & 1) ^ 1);
+            fence_proxy_async_smem();
+          }
+          const void *src;
+          uint32_t bytes;
+          if (j < 0) {
+            const uint32_t h0 = j == -2 ? 0u : (uint32_t)kHalf;
+            const uint32_t h = cnt > h0 ? (cnt - h0 < (uint32_t)kHalf ? cnt - h0 : (uint32_t)kHalf) : 0u;
+            src = a.w + e0 + h0;
+            bytes = h * 4;
+          } else {
+            src = static_cast<const uint16_t *>(a.op[j]) + a.src_off + e0;
+            bytes = cnt * 2;
+          }
+          mbar_expect_tx(&full[s], bytes);
+          if (bytes) bulk_g2s(smem + (size_t)s * kStageBytes, src, bytes, &full[s]);
+        }
+      }
+    }
+  } else {
+    const int tid = threadIdx.x;
+    uint32_t L = 0;
+    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      const int64_t e0 = t * kTile;
+      const int cnt = (int)(n_bulk - e0 < kTile ? n_bulk - e0 : kTile);
+      float4 w[kChunks], x[kChunks];
+      for (int half = 0; half < 2; ++half, ++L) {       // chunks [half*kChunks/2, ...) of w
+        const uint32_t s = L % kStages;
+        mbar_wait(&full[s], (L / kStages) & 1);
+        const float4 *sw = reinterpret_cast<const float4 *>(smem + (size_t)s * kStageBytes);
+#pragma unroll
+        for (int k = 0; k < kChunks / 2; ++k) {
+          const int kk = half * (kChunks / 2) + k;
+          const int c = tid + kk * kConsumers;
+          if (c * 4 < cnt) w[kk] = sw[c - half * (kHalf / 4)];
+          x[kk] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+      }
+      if (a.backup_after == -1) {
+#pragma unroll
+        for (int k = 0; k < kChunks; ++k) {
+          const int c = tid + k * kConsumers;
+          if (c * 4 < cnt) __stcs(reinterpret_cast<float4 *>(a.backup + e0) + c, w[k]);
+        }
+      }
+      for (int j = 0; j < a.n_ops; ++j, ++L) {
+        const uint32_t s = L % kStages;
+        const uint8_t f = a.flag[j];
+        mbar_wait(&full[s], (L / kStages) & 1);
+        const uint2 *st = reinterpret_cast<const uint2 *>(smem + (size_t)s * kStageBytes);
+#pragma unroll
+        for (int k = 0; k < kChunks; ++k) {
+          const int c = tid + k * kConsumers;
+          if (c * 4 < cnt) {
+            const float4 u = widen_bf16x4(st[c]);
+            x[k] = (f & kOpFirst) ? u : add4(x[k], u);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (f & kOpLast) {
+#pragma unroll
+          for (int k = 0; k < kChunks; ++k) w[k] = apply4(w[k], a.lr, x[k]);
+          if (j == a.backup_after) {
+#pragma unroll
+            for (int k = 0; k < kChunks; ++k) {
+              const int c = tid + k * kConsumers;
+              if (c * 4 < cnt) __stcs(reinterpret_cast<float4 *>(a.backup + e0) + c, w[k]);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kChunks; ++k) {
+        const int c = tid + k * kConsumers;
+        if (c * 4 < cnt) __stcs(reinterpret_cast<float4 *>(a.w + e0) + c, w[k]);
+      }
+      for (int b = 0; b < a.n_bcast; ++b) {
+#pragma unroll
+        for (int k = 0; k < kChunks; ++k) {
+          const int c = tid + k * kConsumers;
+          if (c * 4 < cnt) __stcs(reinterpret_cast<float4 *>(a.bcast[b] + e0) + c, w[k]);
+        }
+      }
+    }
+    const int64_t tail = a.n - n_bulk;                // ragged tail (< 8 elements) on CTA 0
+    if (blockIdx.x == 0 && tid < tail) {
+      const int64_t e = n_bulk + tid;
+      float wv = a.w[e];
+      if (a.backup_after == -1) a.backup[e] = wv;
+      float xv = 0.f;
+      for (int j = 0; j < a.n_ops; ++j) {
+        const uint8_t f = a.flag[j];
+        const float u = __uint_as_float(uint32_t(static_cast<const uint16_t *>(a.op[j])[a.src_off + e]) << 16);
+        xv = (f & kOpFirst) ? u : __fadd_rn(xv, u);
+        if (f & kOpLast) {
+          wv = __fsub_rn(wv, __fmul_rn(a.lr, xv));
+          if (j == a.backup_after) a.backup[e] = wv;
+        }
+      }
+      a.w[e] = wv;
+      for (int b = 0; b < a.n_bcast; ++b) a.bcast[b][e] = wv;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
 // Tree reduce: the fp32 aggregate of a group on its
 // aggregator's GPU, acc = ((x1 + x2) + x3) + ... in O(U) order, bf16 widened exactly.
 // The same TMA ring as the commit, without w: the producer streams every member's tile,
@@ -547,9 +691,32 @@ cudaError_t launch_commit_bulk(const CommitArgs &a, cudaStream_t s, int sm_count
   // every persistent CTA, so the last wave's imbalance stays small (a shard of 6.4M elements,
   // config 4 at 4 GPUs: 76.8% of the NVLink roofline at 2048 vs 70.8% at 4096)
   int tile = forced;
+  const int sms = sm_count > 0 ? sm_count : 148;
   if (tile == 0) {
-    const int64_t per_cta = (a.n / 4096) / (sm_count > 0 ? sm_count : 148);
-    tile = per_cta >= 32 ? 4096 : ((a.n / 2048) / (sm_count > 0 ? sm_count : 148) >= 32 ? 2048 : 1024);
+    // all operands bf16 (one context's update dtype; tree-mode aggregates are fp32) and enough
+    // of them that the stage hand-offs matter: 16 KB bf16 copies through the 8192-element
+    // layout while it still deals >= 16 tiles per CTA (config 2 bf16: tau 32 98.3% vs 86.5%;
+    // at tau 4 the 4096 layout's finer tiles win, 103.9% vs 96.2%)
+    bool all_bf16 = a.n_ops >= 8;
+    for (int j = 0; j < a.n_ops && all_bf16; ++j) all_bf16 = (a.flag[j] & kOpBf16) != 0;
+    const char *hb = getenv("MLF_BULK_BF16");
+    if (all_bf16 && !(hb && atoi(hb) == 0) && (a.n / 8192) / sms >= 16) {
+      constexpr int kT = 8192, kS = 12;
+      constexpr size_t smem = (size_t)kS * kT * 2 + 2 * kS * sizeof(uint64_t);
+      static bool init = false;
+      if (!init) {
+        cudaError_t e = cudaFuncSetAttribute(bulk::fused_commit_bulk_h<kT, kS>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        init = true;
+      }
+      const int64_t n_tiles = ((a.n & ~int64_t(7)) + kT - 1) / kT;
+      const int grid = (int)(n_tiles < sms ? (n_tiles > 0 ? n_tiles : 1) : sms);
+      bulk::fused_commit_bulk_h<kT, kS><<<grid, bulk::kThreads, smem, s>>>(a);
+      return cudaGetLastError();
+    }
+    const int64_t per_cta = (a.n / 4096) / sms;
+    tile = per_cta >= 32 ? 4096 : ((a.n / 2048) / sms >= 32 ? 2048 : 1024);
   }
   if (tile == 8192) return launch_tile<8192, 6>(a, s, sm_count);
   if (tile == 2048) return launch_tile<2048, 24>(a, s, sm_count);

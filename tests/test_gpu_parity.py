@@ -156,6 +156,29 @@ def test_bulk_tiles_bitwise(tile, dtype):
         del os.environ["MLF_BULK_TILE"]
 
 
+@pytest.mark.parametrize("boundary", [0, 2, -1])
+def test_bf16_16kb_layout_bitwise(boundary):
+    # all-bf16 operand lists large enough for the 8192-element layout (16 KB bf16 copies, w
+    # over two stages): bitwise equal to the 4096-element kernel on every element and to the
+    # oracle on a sample, ragged tail and mirror boundary included
+    rng = np.random.default_rng(77 + boundary)
+    S, W = 8192 * 148 * 16 + 4 * 1237 + 5, 9
+    p = random_plan(rng, W, n_commit=W, boundary=boundary)
+    w_h, b_h, _, _ = gpu_run(S, W, sg.DTYPE_BF16, p, backup=True, impl="bulk")
+    os.environ["MLF_BULK_BF16"] = "0"
+    try:
+        w_s, b_s, _, _ = gpu_run(S, W, sg.DTYPE_BF16, p, backup=True, impl="bulk")
+    finally:
+        del os.environ["MLF_BULK_BF16"]
+    assert np.array_equal(bits(w_h), bits(w_s))
+    assert np.array_equal(bits(b_h), bits(b_s)) if boundary >= 0 else np.all(np.isnan(b_h))
+    idx = np.unique(np.concatenate([rng.integers(0, S, 100_000), np.arange(S - 13, S), np.arange(0, 9)]))
+    wr, br = oracle_run(S, sg.DTYPE_BF16, p, idx=idx)
+    assert np.array_equal(bits(w_h[idx]), bits(wr))
+    if boundary >= 0:
+        assert np.array_equal(bits(b_h[idx]), bits(br))
+
+
 @pytest.mark.parametrize("tile", [1024, 2048, 4096])
 def test_bulk_commit_under_concurrent_copy_engine_traffic(tile):
     # regression: without fence.proxy.async between the empty-barrier wait and the bulk copy
