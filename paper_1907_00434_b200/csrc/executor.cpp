@@ -583,8 +583,10 @@ static void pipeline_commit(mlf_ctx *c, const mlf_plan_out *p, const std::vector
     if (c->host_src[w]) host_w.push_back(w);
   }
   const int64_t n = c->cfg.shard_elems, e = (int64_t)c->elem_bytes;
-  for (int64_t off = 0; off < n || (off == 0 && n == 0); off += kPipeChunk) {
-    const int64_t len = std::min(kPipeChunk, n - off);
+  const char *ce = getenv("MLF_PIPE_CHUNK");          // elements per chunk (tuning experiments)
+  const int64_t chunk = ce && atoll(ce) >= 4096 ? atoll(ce) / 4096 * 4096 : kPipeChunk;
+  for (int64_t off = 0; off < n || (off == 0 && n == 0); off += chunk) {
+    const int64_t len = std::min(chunk, n - off);
     for (int w : host_w) {
       const int64_t src = c->cfg.shard_begin + off;
       CK(cudaMemcpyAsync(static_cast<char *>(c->slot[w]) + src * e, static_cast<const char *>(c->host_src[w]) + src * e,
