@@ -37,6 +37,21 @@ def test_two_ranks_full_size_config3():
     assert "MULTIGPU_OK fold" in out and "MULTIGPU_OK tree" in out and "MULTIGPU_OK staged" in out
 
 
+def test_two_ranks_full_size_config4():
+    # config 4 as stated (128 workers, 25.6M fp32, N2 shares, C2 stragglers, re-planned every
+    # batch) on 2 PS shards, sampled outputs vs the oracle planning the same batches
+    out = _run(2, "--cid", "4", "--S", "25600000", "--steps", "2", timeout=1200)
+    assert "MULTIGPU_OK fold" in out and "MULTIGPU_OK tree" in out and "MULTIGPU_OK staged" in out
+
+
+def test_two_ranks_full_size_config5_updates():
+    # config 5's 100M-element updates and replica mirror on the neighbour GPU, 64 of its 256
+    # workers (the Python oracle plans 256 in ~2 minutes per batch)
+    out = _run(2, "--cid", "5", "--S", "100000000", "--steps", "1", "--workers", "64", "--modes", "fold,tree",
+               timeout=1200)
+    assert "MULTIGPU_OK fold" in out and "MULTIGPU_OK tree" in out
+
+
 def test_two_ranks_staged_minimum_chunk():
     # copy-engine staging with a 2 MiB buffer: 4096-element chunks, many of them, ragged tail
     out = _run(2, "--cid", "3", "--S", "300007", "--modes", "staged", "--stage-mib", "2", "--workers", "32")
