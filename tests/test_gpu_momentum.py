@@ -96,3 +96,23 @@ def test_momentum_rejects_tree_mode_and_bad_gamma():
     with pytest.raises(m.MlfError) as e:
         m.Context(device=0, model_shard=w, update_slots=[w], lr=0.1, model_elems=64, gamma=0.9)
     assert e.value.code == m.MLF_E_INVALID                 # no history buffer
+
+
+def test_momentum_under_concurrent_copy_engine_traffic():
+    # the momentum ring reuses stages like the commit ring (fence.proxy.async regression)
+    S, W, gamma = 16_777_216, 24, 0.9
+    rng = np.random.default_rng(5)
+    p = random_plan(rng, W, n_commit=W, boundary=-1)
+    dev = torch.device("cuda", 0)
+    big_src = torch.ones(1 << 28, dtype=torch.float32, device=dev)
+    big_dst = torch.empty_like(big_src)
+    side = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    for _ in range(40):                        # ~40 GiB: still running when the commit launches
+        m.copy_engine(0, big_dst.data_ptr(), big_src.data_ptr(), big_src.numel() * 4, side.cuda_stream)
+    (w, h, _, _), h0 = run_momentum(S, W, sg.DTYPE_F32, p, gamma)
+    torch.cuda.synchronize()
+    idx = np.unique(np.concatenate([rng.integers(0, S, 200_000), np.arange(S - 9, S)]))
+    commits = commits_from_plan(p, lambda g: sg.update_values(SEED, g, 0, idx, sg.DTYPE_F32))
+    wr, hr, _ = weighted_f32(sg.w0_values(SEED, idx), h0[idx], commits, 0.01, gamma, -1)
+    assert np.array_equal(bits(w[idx]), bits(wr)) and np.array_equal(bits(h[idx]), bits(hr))
