@@ -27,6 +27,7 @@
 #include <atomic>
 #include <cmath>
 #include <condition_variable>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <limits>
@@ -88,8 +89,13 @@ class Pool {
 
  private:
   Pool() {
+    // one process per GPU plans on every rank at once: share the host's cores between the
+    // local ranks (torchrun's LOCAL_WORLD_SIZE), or take MLF_PLAN_THREADS as given
     unsigned hw = std::thread::hardware_concurrency();
-    int t = (int)std::min<unsigned>(hw ? hw : 1, 32) - 1;
+    int total = (int)std::min<unsigned>(hw ? hw : 1, 32);
+    if (const char *lw = getenv("LOCAL_WORLD_SIZE")) total = std::max(1, total / std::max(1, atoi(lw)));
+    if (const char *pt = getenv("MLF_PLAN_THREADS")) total = std::max(1, std::min(32, atoi(pt)));
+    int t = total - 1;
     for (int i = 0; i < t; ++i) th_.emplace_back([this] { loop(); });
   }
   ~Pool() {
@@ -131,7 +137,7 @@ class Pool {
       }
     }
   }
-  static constexpr int kSpin = 20000;              // ~50-100 us of pause instructions
+  static constexpr int kSpin = 4000;               // tens of microseconds of pause instructions
   std::vector<std::thread> th_;
   std::mutex m_, busy_;
   std::condition_variable cv_, done_;
