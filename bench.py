@@ -278,7 +278,7 @@ def run_single(a):
 
     def measure(tau, dtype, steps, warmup, kernel, clocks=False, gamma=0.0):
         os.environ["MLF_COMMIT_IMPL"] = kernel
-        cfg = configs.config(cid, tau=tau, dtype=dtype, gamma=gamma)
+        cfg = configs.config(cid, G=1 if cid >= 3 else None, tau=tau, dtype=dtype, gamma=gamma)
         wl = Workload(cfg, device=0)
         wl.fill_updates(0)
         torch.cuda.synchronize()
@@ -382,7 +382,7 @@ def run_single(a):
         line["e2e"] = e2e_single(cid, a)
     if not a.no_cpu_baseline:
         import synthgen as sg
-        line["cpu_baseline"] = cpu_baseline_oracle(configs.config(cid, tau=a.tau, dtype=a.dtype),
+        line["cpu_baseline"] = cpu_baseline_oracle(configs.config(cid, G=1 if cid >= 3 else None, tau=a.tau, dtype=a.dtype),
                                                    sg.DTYPE_BF16 if a.dtype == "bf16" else sg.DTYPE_F32)
     print(json.dumps(line), flush=True)
 
@@ -395,7 +395,7 @@ def e2e_single(cid, a):
     from paper_1907_00434_b200.harness import Workload, committed_bytes
     from synthgen import configs
 
-    cfg = configs.config(cid, tau=a.tau, dtype=a.dtype)
+    cfg = configs.config(cid, G=1 if cid >= 3 else None, tau=a.tau, dtype=a.dtype)
     wl = Workload(cfg, device=0)
     wl.fill_updates(0)
     hosts = {}
