@@ -52,6 +52,14 @@ def test_two_ranks_full_size_config5_updates():
     assert "MULTIGPU_OK fold" in out and "MULTIGPU_OK tree" in out
 
 
+def test_two_ranks_bf16_16kb_layout():
+    # bf16 shards large enough for the 8192-element bf16 kernel (>= 16 tiles per CTA), operands
+    # read over peer mappings (fold) and from the staging buffer (staged)
+    out = _run(2, "--cid", "3", "--S", "40000000", "--steps", "1", "--dtype", "bf16", "--modes", "fold,staged",
+               timeout=900)
+    assert "MULTIGPU_OK fold" in out and "MULTIGPU_OK staged" in out
+
+
 def test_two_ranks_staged_minimum_chunk():
     # copy-engine staging with a 2 MiB buffer: 4096-element chunks, many of them, ragged tail
     out = _run(2, "--cid", "3", "--S", "300007", "--modes", "staged", "--stage-mib", "2", "--workers", "32")
