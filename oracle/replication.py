@@ -29,9 +29,9 @@ keeps its duration and starts at max(its start, commit time of a_e).
 
 Parity: pinned by Eq. 9's coefficients and the 4.61 example, soundness
 ||w_s - w_r|| <= bound on true vectors, Div_max = inf -> no delay, Div_max = 0 &
-gamma = 0 -> lead 0 at T_last (tests/test_oracle_replication.py).  The
-delay-last timing beyond these invariants is PARITY UNPINNED (the paper gives no
-formula for the re-reserved schedule).
+gamma = 0 -> lead 0 at T_last, and a hand-worked delay-last instance at three
+Div_max values (tests/test_oracle_replication.py).  The delay-last *reading* (R15b)
+is ours: the paper gives no formula for the re-reserved schedule.
 """
 from __future__ import annotations
 

@@ -121,3 +121,34 @@ def test_divmax_limits_and_mirror_consistency():
         else:
             assert p["replica_frozen"] == nc + sum(p["commit_count"][:b])
             assert b <= p["n_server_commits"]
+
+
+def test_delayed_last_commit_hand_worked():
+    # §5.3's delay of the last server commit (reading R15b), worked by hand.
+    # Nodes: W0, W1 (up 10 MB/s), server S (down 10 MB/s), replica R (down 5 MB/s); two
+    # fresh 10 MB updates, no aggregators, gamma 0, unit norms (count-style Div_max).
+    # Server plan: g0 on [0,1] s, g1 on [1,2] s -> T_last = 2 s.  Replica plan on the network
+    # after the server's reservations: g0 -> R waits for W0's up-link, runs at 5 MB/s on
+    # [1,3]; g1 -> R gets 5 MB by 1 s, is blocked by g0 on R's down-link until 3, then
+    # finishes on [3,4] -> replica commit times 3 s, 4 s; nothing is frozen by T_last.
+    from oracle.plan import Item, Params, make_net
+    from paper_1907_00434_b200 import mlfabric as m
+    MB, S = 10**6, 10**9
+    up, down = [10 * MB, 10 * MB, 0, 0], [0, 0, 10 * MB, 5 * MB]
+    batch = [Item(0, 10 * MB, 7, 0, 1.0), Item(1, 10 * MB, 7, 0, 1.0)]
+    cases = {
+        # Div_max: (replica_frozen, boundary, punted, delayed_last, commit_t_ns)
+        0.0: (2, 2, [], 1, [1 * S, 5 * S]),   # a_e = replica commit 2 (at 4 s): g1 starts at 4, ends 5
+        1.0: (1, 1, [1], 1, [1 * S, 4 * S]),  # a_e = replica commit 1 (at 3 s): g1 starts at 3, ends 4
+        2.0: (0, -1, [0, 1], 0, [1 * S, 2 * S]),  # the lead of 2 is within Div_max: no delay
+    }
+    for div_max, (frozen, boundary, punted, delayed, times) in cases.items():
+        prm = Params(servers=[2], replicas=[3], v_init=7, tau_max=10, div_max=div_max)
+        p = plan(make_net(4, up, down), batch, prm)
+        assert p["order"] == [0, 1] and p["commit_t_ns"] == times, (div_max, p["commit_t_ns"])
+        assert (p["replica_frozen"], p["replica_boundary_commit"], p["punted"], p["delayed_last"]) == \
+            (frozen, boundary, punted, delayed), div_max
+        assert p["t_total_ns"] == times[-1]
+        c = m.plan(4, up, down, [dict(node=it.node, size=it.size, version=7, t_avail=0, norm=1.0) for it in batch],
+                   [2], replicas=[3], v_init=7, tau_max=10, div_max=div_max)
+        assert {k: c[k] for k in p} == p
