@@ -28,7 +28,7 @@ constexpr int kConsumerWarps = 8;
 constexpr int kConsumers = kConsumerWarps * 32;
 constexpr int kThreads = kConsumers + 32;       // + 1 producer warp
 constexpr size_t smem_bytes(int tile, int stages) {
-  return (size_t)stages * tile * 4 + 2 * stages * sizeof(uint64_t);
+  return (size_t)stages * tile * 4 + 3 * stages * sizeof(uint64_t);   // stages, full, empty, tile ids
 }
 
 __device__ __forceinline__ uint32_t smem_addr(const void *p) {
@@ -86,6 +86,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_bulk(const __grid_co
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)kStages * kStageBytes);
   uint64_t *empty = full + kStages;
+  int64_t *tile_of = reinterpret_cast<int64_t *>(empty + kStages);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t n_bulk = a.n & ~int64_t(7);       // bulk region: whole 8-element groups (16 B for bf16)
   const int64_t n_tiles = (n_bulk + kTile - 1) / kTile;
@@ -101,11 +102,15 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_bulk(const __grid_co
 
   if (warp == kConsumerWarps) {
     // ------------------------------------------------------------ producer
+    // Tiles come round-robin (static) or from a global counter (a.sched: a CTA slowed by a
+    // hot peer link takes fewer tiles).  The w stage of each tile carries its index to the
+    // consumers; index -1 (no stage data) ends them.
     if (lane == 0) {
       uint32_t L = 0;
-      for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      int64_t t = a.sched ? (int64_t)atomicAdd(&a.sched[0], 1ull) : (int64_t)blockIdx.x;
+      for (;;) {
         const int64_t e0 = t * kTile;
-        const uint32_t cnt = (uint32_t)(n_bulk - e0 < kTile ? n_bulk - e0 : kTile);
+        const uint32_t cnt = t < n_tiles ? (uint32_t)(n_bulk - e0 < kTile ? n_bulk - e0 : kTile) : 0u;
         for (int j = -1; j < a.n_ops; ++j, ++L) {
           const uint32_t s = L % kStages;
           if (L >= (uint32_t)kStages) {
@@ -115,6 +120,11 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_bulk(const __grid_co
           const void *src;
           uint32_t bytes;
           if (j < 0) {
+            tile_of[s] = t < n_tiles ? t : -1;
+            if (t >= n_tiles) {
+              mbar_arrive(&full[s]);                  // release: the consumers read -1
+              break;
+            }
             src = a.w + e0;
             bytes = cnt * 4;
           } else if (a.flag[j] & kOpBf16) {
@@ -127,19 +137,34 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_bulk(const __grid_co
           mbar_expect_tx(&full[s], bytes);
           bulk_g2s(smem + (size_t)s * kStageBytes, src, bytes, &full[s]);
         }
+        if (t >= n_tiles) break;
+        t = a.sched ? (int64_t)atomicAdd(&a.sched[0], 1ull) : t + gridDim.x;
+      }
+      if (a.sched) {
+        // every CTA has made its last fetch: the last one resets the counters for the next
+        // launch on this stream
+        __threadfence();
+        if (atomicAdd(&a.sched[1], 1ull) == gridDim.x - 1) {
+          a.sched[0] = 0;
+          a.sched[1] = 0;
+          __threadfence();
+        }
       }
     }
   } else {
     // ------------------------------------------------------------ consumers
     const int tid = threadIdx.x;
     uint32_t L = 0;
-    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    for (;;) {
+      const uint32_t s0 = L % kStages;
+      mbar_wait(&full[s0], (L / kStages) & 1);
+      const int64_t t = tile_of[s0];
+      if (t < 0) break;
       const int64_t e0 = t * kTile;
       const int cnt = (int)(n_bulk - e0 < kTile ? n_bulk - e0 : kTile);
       float4 w[kChunks], x[kChunks];
       {
-        const uint32_t s = L % kStages;
-        mbar_wait(&full[s], (L / kStages) & 1);
+        const uint32_t s = s0;
         const float4 *sw = reinterpret_cast<const float4 *>(smem + (size_t)s * kStageBytes);
 #pragma unroll
         for (int k = 0; k < kChunks; ++k) {

@@ -96,6 +96,8 @@ struct mlf_ctx {
   int64_t retained_bytes = 0;
   bool started = false, pending = false, sticky = false, phase1_done = false;
   bool dist_p1 = false;                           // distribution phase 1 recorded ev_stop
+  unsigned long long *tile_sched = nullptr;       // dynamic tile counters of the bulk commit
+  bool dyn_sched = false;
   int64_t launches = 0, h2d = 0, d2h = 0;
   CommitImpl impl = CommitImpl::kLdg;
 };
@@ -210,6 +212,11 @@ extern "C" mlf_status mlf_init(const mlf_config *cfg, int64_t v0, mlf_ctx **out)
       if (k.world > 1) CK(cudaEventCreateWithFlags(&c->ev_phase, cudaEventInterprocess | cudaEventDisableTiming));
       CK(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
       CK(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
+      // dynamic tile scheduling for the bulk commit (MLF_BULK_SCHED=static turns it off)
+      CK(cudaMalloc(reinterpret_cast<void **>(&c->tile_sched), 2 * sizeof(unsigned long long)));
+      CK(cudaMemset(c->tile_sched, 0, 2 * sizeof(unsigned long long)));
+      const char *sched = getenv("MLF_BULK_SCHED");
+      c->dyn_sched = !(sched && std::string(sched) == "static");
       if (k.stage_buf && k.stage_bytes > 0 && k.world > 1)
         for (int i = 0; i < kCopyStreams; ++i) {
           cudaStream_t s;
@@ -217,7 +224,7 @@ extern "C" mlf_status mlf_init(const mlf_config *cfg, int64_t v0, mlf_ctx **out)
           c->s_copy.push_back(s);
         }
     } catch (...) {
-      delete c;
+      mlf_destroy(c);                              // releases whatever was created
       throw;
     }
     *out = c;
@@ -234,6 +241,7 @@ extern "C" void mlf_destroy(mlf_ctx *c) {
   if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
   if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
   for (auto s : c->s_copy) cudaStreamDestroy(s);
+  if (c->tile_sched) cudaFree(c->tile_sched);
   delete c;
 }
 
@@ -512,6 +520,7 @@ static void launch_ops(mlf_ctx *c, float *w, float *backup, const std::vector<Co
     a.backup_after = -2;
     if (first_launch && boundary == 0) a.backup_after = -1;
     a.n_bcast = 0;
+    a.sched = c->dyn_sched ? c->tile_sched : nullptr;
     if (bcast && i1 == ops.size())                  // only the pass that finishes w broadcasts it
       for (float *d : c->bcast) a.bcast[a.n_bcast++] = d + c->cfg.shard_begin + off;
     for (size_t q = i0; q < i1; ++q) {

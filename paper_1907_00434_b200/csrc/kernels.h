@@ -32,6 +32,9 @@ struct CommitArgs {
   // new model happens tile by tile inside the commit pass
   int32_t n_bcast;
   float *bcast[kMaxBcast];
+  // dynamic tile scheduling (bulk kernel): [0] next tile, [1] CTAs done; zero between launches
+  // (the last CTA resets both).  nullptr = static round-robin tiles.
+  unsigned long long *sched;
 };
 
 // tree_reduce: out[i] = left fold of members, fp32 (an aggregator's sum).
