@@ -111,6 +111,9 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_bulk(const __grid_co
       for (;;) {
         const int64_t e0 = t * kTile;
         const uint32_t cnt = t < n_tiles ? (uint32_t)(n_bulk - e0 < kTile ? n_bulk - e0 : kTile) : 0u;
+        // fetch the next tile now: the atomic's latency hides behind this tile's issues
+        int64_t t_next = 0;
+        if (t < n_tiles) t_next = a.sched ? (int64_t)atomicAdd(&a.sched[0], 1ull) : t + gridDim.x;
         for (int j = -1; j < a.n_ops; ++j, ++L) {
           const uint32_t s = L % kStages;
           if (L >= (uint32_t)kStages) {
@@ -138,7 +141,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_bulk(const __grid_co
           bulk_g2s(smem + (size_t)s * kStageBytes, src, bytes, &full[s]);
         }
         if (t >= n_tiles) break;
-        t = a.sched ? (int64_t)atomicAdd(&a.sched[0], 1ull) : t + gridDim.x;
+        t = t_next;
       }
       if (a.sched) {
         // every CTA has made its last fetch: the last one resets the counters for the next
@@ -266,6 +269,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_momentum(const __gri
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)kStages * kStageBytes);
   uint64_t *empty = full + kStages;
+  int64_t *tile_of = reinterpret_cast<int64_t *>(empty + kStages);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t n_bulk = a.n & ~int64_t(7);
   const int64_t n_tiles = (n_bulk + kTile - 1) / kTile;
@@ -280,9 +284,13 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_momentum(const __gri
   if (warp == kConsumerWarps) {
     if (lane == 0) {
       uint32_t L = 0;
-      for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      int64_t t = a.sched ? (int64_t)atomicAdd(&a.sched[0], 1ull) : (int64_t)blockIdx.x;
+      for (;;) {
         const int64_t e0 = t * kTile;
-        const uint32_t cnt = (uint32_t)(n_bulk - e0 < kTile ? n_bulk - e0 : kTile);
+        const uint32_t cnt = t < n_tiles ? (uint32_t)(n_bulk - e0 < kTile ? n_bulk - e0 : kTile) : 0u;
+        // fetch the next tile now: the atomic's latency hides behind this tile's issues
+        int64_t t_next = 0;
+        if (t < n_tiles) t_next = a.sched ? (int64_t)atomicAdd(&a.sched[0], 1ull) : t + gridDim.x;
         for (int j = -2; j < a.n_ops; ++j, ++L) {
           const uint32_t s = L % kStages;
           if (L >= (uint32_t)kStages) {
@@ -292,6 +300,11 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_momentum(const __gri
           const void *src;
           uint32_t bytes = cnt * 4;
           if (j == -2) {
+            tile_of[s] = t < n_tiles ? t : -1;       // the w stage carries the tile index
+            if (t >= n_tiles) {
+              mbar_arrive(&full[s]);
+              break;
+            }
             src = a.w + e0;
           } else if (j == -1) {
             src = a.h + e0;
@@ -304,13 +317,26 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_momentum(const __gri
           mbar_expect_tx(&full[s], bytes);
           bulk_g2s(smem + (size_t)s * kStageBytes, src, bytes, &full[s]);
         }
+        if (t >= n_tiles) break;
+        t = t_next;
+      }
+      if (a.sched) {                                  // the last CTA resets the counters
+        __threadfence();
+        if (atomicAdd(&a.sched[1], 1ull) == gridDim.x - 1) {
+          a.sched[0] = 0;
+          a.sched[1] = 0;
+          __threadfence();
+        }
       }
     }
     return;
   }
   const int tid = threadIdx.x;
   uint32_t L = 0;
-  for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+  for (;;) {
+    mbar_wait(&full[L % kStages], (L / kStages) & 1);
+    const int64_t t = tile_of[L % kStages];
+    if (t < 0) break;
     const int64_t e0 = t * kTile;
     const int cnt = (int)(n_bulk - e0 < kTile ? n_bulk - e0 : kTile);
     float4 w[kChunks], h[kChunks], A[kChunks], B[kChunks];
@@ -432,6 +458,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_bulk_h(const __grid_
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)kStages * kStageBytes);
   uint64_t *empty = full + kStages;
+  int64_t *tile_of = reinterpret_cast<int64_t *>(empty + kStages);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t n_bulk = a.n & ~int64_t(7);
   const int64_t n_tiles = (n_bulk + kTile - 1) / kTile;
@@ -448,14 +475,25 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_bulk_h(const __grid_
   if (warp == kConsumerWarps) {
     if (lane == 0) {
       uint32_t L = 0;
-      for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      int64_t t = a.sched ? (int64_t)atomicAdd(&a.sched[0], 1ull) : (int64_t)blockIdx.x;
+      for (;;) {
         const int64_t e0 = t * kTile;
-        const uint32_t cnt = (uint32_t)(n_bulk - e0 < kTile ? n_bulk - e0 : kTile);
+        const uint32_t cnt = t < n_tiles ? (uint32_t)(n_bulk - e0 < kTile ? n_bulk - e0 : kTile) : 0u;
+        // fetch the next tile now: the atomic's latency hides behind this tile's issues
+        int64_t t_next = 0;
+        if (t < n_tiles) t_next = a.sched ? (int64_t)atomicAdd(&a.sched[0], 1ull) : t + gridDim.x;
         for (int j = -2; j < a.n_ops; ++j, ++L) {       // j = -2, -1: the two halves of w
           const uint32_t s = L % kStages;
           if (L >= (uint32_t)kStages) {
             mbar_wait(&empty[s], ((L / kStages) & 1) ^ 1);
             fence_proxy_async_smem();
+          }
+          if (j == -2) {
+            tile_of[s] = t < n_tiles ? t : -1;       // the first w stage carries the tile index
+            if (t >= n_tiles) {
+              mbar_arrive(&full[s]);
+              break;
+            }
           }
           const void *src;
           uint32_t bytes;
@@ -471,12 +509,25 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_bulk_h(const __grid_
           mbar_expect_tx(&full[s], bytes);
           if (bytes) bulk_g2s(smem + (size_t)s * kStageBytes, src, bytes, &full[s]);
         }
+        if (t >= n_tiles) break;
+        t = t_next;
+      }
+      if (a.sched) {                                  // the last CTA resets the counters
+        __threadfence();
+        if (atomicAdd(&a.sched[1], 1ull) == gridDim.x - 1) {
+          a.sched[0] = 0;
+          a.sched[1] = 0;
+          __threadfence();
+        }
       }
     }
   } else {
     const int tid = threadIdx.x;
     uint32_t L = 0;
-    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    for (;;) {
+      mbar_wait(&full[L % kStages], (L / kStages) & 1);
+      const int64_t t = tile_of[L % kStages];
+      if (t < 0) break;
       const int64_t e0 = t * kTile;
       const int cnt = (int)(n_bulk - e0 < kTile ? n_bulk - e0 : kTile);
       float4 w[kChunks], x[kChunks];
@@ -727,7 +778,7 @@ cudaError_t launch_commit_bulk(const CommitArgs &a, cudaStream_t s, int sm_count
     const char *hb = getenv("MLF_BULK_BF16");
     if (all_bf16 && !(hb && atoi(hb) == 0) && (a.n / 8192) / sms >= 16) {
       constexpr int kT = 8192, kS = 12;
-      constexpr size_t smem = (size_t)kS * kT * 2 + 2 * kS * sizeof(uint64_t);
+      constexpr size_t smem = (size_t)kS * kT * 2 + 3 * kS * sizeof(uint64_t);
       static bool init = false;
       if (!init) {
         cudaError_t e = cudaFuncSetAttribute(bulk::fused_commit_bulk_h<kT, kS>,

@@ -452,6 +452,7 @@ static void launch_momentum(mlf_ctx *c, const mlf_plan_out *p, const std::vector
       while (i1 > i0 && !(ops[i1 - 1].flag & kOpLast)) --i1;
     if (i1 == i0 && i0 < ops.size()) throw Fail{MLF_E_CAPACITY, "a single commit has more than kMaxOpsM members"};
     MomentumArgs a;
+    a.sched = c->dyn_sched ? c->tile_sched : nullptr;
     a.w = c->cfg.model_shard;
     a.h = c->cfg.history_shard;
     a.backup = c->cfg.backup_shard;

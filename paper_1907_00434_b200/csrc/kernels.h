@@ -62,6 +62,7 @@ struct MomentumArgs {
   float cB[kMaxOpsM];        // g^(m-i)              (h's weight of member i)
   float sh[kMaxOpsM];        // sum_{j=1..m} g^j     (at the commit's last operand)
   float gm[kMaxOpsM];        // g^m                  (at the commit's last operand)
+  unsigned long long *sched; // dynamic tile counters (as CommitArgs::sched) or nullptr
 };
 
 enum class CommitImpl : int { kLdg = 0, kBulk = 1 };
