@@ -444,6 +444,169 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_momentum(const __gri
   }
 }
 
+// The momentum pass with static round-robin tiles and no tile-index hand-off: measured
+// faster for long operand lists (config 2, tau 32: 104.5% of the HBM roofline vs 93.4% for
+// the dynamic kernel above, whose longer loops cost the compute-heavier momentum consumers),
+// slower for short ones (tau 4: 96.9% vs 104.3%).  launch_commit_momentum picks.
+template <int kTile, int kStages>
+__global__ void __launch_bounds__(kThreads, 1) fused_commit_momentum_rr(const __grid_constant__ MomentumArgs a) {
+  constexpr int kStageBytes = kTile * 4;
+  constexpr int kChunks = kTile / 4 / kConsumers;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)kStages * kStageBytes);
+  uint64_t *empty = full + kStages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t n_bulk = a.n & ~int64_t(7);
+  const int64_t n_tiles = (n_bulk + kTile - 1) / kTile;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == kConsumerWarps) {
+    if (lane == 0) {
+      uint32_t L = 0;
+      for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        const int64_t e0 = t * kTile;
+        const uint32_t cnt = (uint32_t)(n_bulk - e0 < kTile ? n_bulk - e0 : kTile);
+        for (int j = -2; j < a.n_ops; ++j, ++L) {
+          const uint32_t s = L % kStages;
+          if (L >= (uint32_t)kStages) {
+            mbar_wait(&empty[s], ((L / kStages) & 1) ^ 1);
+            fence_proxy_async_smem();
+          }
+          const void *src;
+          uint32_t bytes = cnt * 4;
+          if (j == -2) {
+            src = a.w + e0;
+          } else if (j == -1) {
+            src = a.h + e0;
+          } else if (a.flag[j] & kOpBf16) {
+            src = static_cast<const uint16_t *>(a.op[j]) + a.src_off + e0;
+            bytes = cnt * 2;
+          } else {
+            src = static_cast<const float *>(a.op[j]) + a.src_off + e0;
+          }
+          mbar_expect_tx(&full[s], bytes);
+          bulk_g2s(smem + (size_t)s * kStageBytes, src, bytes, &full[s]);
+        }
+      }
+    }
+    return;
+  }
+  const int tid = threadIdx.x;
+  uint32_t L = 0;
+  for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    const int64_t e0 = t * kTile;
+    const int cnt = (int)(n_bulk - e0 < kTile ? n_bulk - e0 : kTile);
+    float4 w[kChunks], h[kChunks], A[kChunks], B[kChunks];
+#pragma unroll
+    for (int which = 0; which < 2; ++which) {
+      const uint32_t s = L % kStages;
+      mbar_wait(&full[s], (L / kStages) & 1);
+      const float4 *sp = reinterpret_cast<const float4 *>(smem + (size_t)s * kStageBytes);
+#pragma unroll
+      for (int k = 0; k < kChunks; ++k) {
+        const int c = tid + k * kConsumers;
+        if (c * 4 < cnt) (which == 0 ? w[k] : h[k]) = sp[c];
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      ++L;
+    }
+    if (a.backup_after == -1) {
+#pragma unroll
+      for (int k = 0; k < kChunks; ++k) {
+        const int c = tid + k * kConsumers;
+        if (c * 4 < cnt) {
+          __stcs(reinterpret_cast<float4 *>(a.backup + e0) + c, w[k]);
+          __stcs(reinterpret_cast<float4 *>(a.backup_h + e0) + c, h[k]);
+        }
+      }
+    }
+    for (int j = 0; j < a.n_ops; ++j, ++L) {
+      const uint32_t s = L % kStages;
+      const uint8_t f = a.flag[j];
+      const float ca = a.cA[j], cb = a.cB[j];
+      mbar_wait(&full[s], (L / kStages) & 1);
+      const uint8_t *st = smem + (size_t)s * kStageBytes;
+#pragma unroll
+      for (int k = 0; k < kChunks; ++k) {
+        const int c = tid + k * kConsumers;
+        if (c * 4 < cnt) {
+          const float4 g = (f & kOpBf16) ? widen_bf16x4(reinterpret_cast<const uint2 *>(st)[c])
+                                         : reinterpret_cast<const float4 *>(st)[c];
+          const float4 u = neg4(mul4(a.lr, g));
+          const float4 pa = mul4(ca, u), pb = mul4(cb, u);
+          A[k] = (f & kOpFirst) ? pa : add4(A[k], pa);
+          B[k] = (f & kOpFirst) ? pb : add4(B[k], pb);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (f & kOpLast) {
+        const float sh = a.sh[j], gm = a.gm[j];
+#pragma unroll
+        for (int k = 0; k < kChunks; ++k) {
+          w[k] = add4(w[k], add4(mul4(sh, h[k]), A[k]));
+          h[k] = add4(mul4(gm, h[k]), B[k]);
+        }
+        if (j == a.backup_after) {
+#pragma unroll
+          for (int k = 0; k < kChunks; ++k) {
+            const int c = tid + k * kConsumers;
+            if (c * 4 < cnt) {
+              __stcs(reinterpret_cast<float4 *>(a.backup + e0) + c, w[k]);
+              __stcs(reinterpret_cast<float4 *>(a.backup_h + e0) + c, h[k]);
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kChunks; ++k) {
+      const int c = tid + k * kConsumers;
+      if (c * 4 < cnt) {
+        __stcs(reinterpret_cast<float4 *>(a.w + e0) + c, w[k]);
+        __stcs(reinterpret_cast<float4 *>(a.h + e0) + c, h[k]);
+      }
+    }
+  }
+  // ragged tail (< 8 elements) on CTA 0
+  const int64_t tail = a.n - n_bulk;
+  if (blockIdx.x == 0 && tid < tail) {
+    const int64_t e = n_bulk + tid;
+    float wv = a.w[e], hv = a.h[e], Av = 0.f, Bv = 0.f;
+    if (a.backup_after == -1) {
+      a.backup[e] = wv;
+      a.backup_h[e] = hv;
+    }
+    for (int j = 0; j < a.n_ops; ++j) {
+      const uint8_t f = a.flag[j];
+      const float g = (f & kOpBf16)
+                          ? __uint_as_float(uint32_t(static_cast<const uint16_t *>(a.op[j])[a.src_off + e]) << 16)
+                          : static_cast<const float *>(a.op[j])[a.src_off + e];
+      const float u = -__fmul_rn(a.lr, g);
+      const float pa = __fmul_rn(a.cA[j], u), pb = __fmul_rn(a.cB[j], u);
+      Av = (f & kOpFirst) ? pa : __fadd_rn(Av, pa);
+      Bv = (f & kOpFirst) ? pb : __fadd_rn(Bv, pb);
+      if (f & kOpLast) {
+        wv = __fadd_rn(wv, __fadd_rn(__fmul_rn(a.sh[j], hv), Av));
+        hv = __fadd_rn(__fmul_rn(a.gm[j], hv), Bv);
+        if (j == a.backup_after) {
+          a.backup[e] = wv;
+          a.backup_h[e] = hv;
+        }
+      }
+    }
+    a.w[e] = wv;
+    a.h[e] = hv;
+  }
+}
+
 // ---------------------------------------------------------------------------------------
 // The same commit for bf16 operands with 16 KB bulk copies: a tile is kTile = 8192
 // elements, so every bf16 operand tile fills one 16 KB stage and the fp32 w tile spans two.
@@ -736,7 +899,18 @@ cudaError_t launch_commit_momentum(const MomentumArgs &a, cudaStream_t s, int sm
   }
   const int64_t n_tiles = ((a.n & ~int64_t(7)) + kTile - 1) / kTile;
   int grid = (int)(n_tiles < sm_count ? (n_tiles > 0 ? n_tiles : 1) : sm_count);
-  bulk::fused_commit_momentum<kTile, kStages><<<grid, bulk::kThreads, smem, s>>>(a);
+  if (a.sched && a.n_ops <= 8) {
+    bulk::fused_commit_momentum<kTile, kStages><<<grid, bulk::kThreads, smem, s>>>(a);
+  } else {
+    static bool init_rr = false;
+    if (!init_rr) {
+      cudaError_t e = cudaFuncSetAttribute(bulk::fused_commit_momentum_rr<kTile, kStages>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      init_rr = true;
+    }
+    bulk::fused_commit_momentum_rr<kTile, kStages><<<grid, bulk::kThreads, smem, s>>>(a);
+  }
   return cudaGetLastError();
 }
 
