@@ -10,13 +10,13 @@ for N in 2 4 8; do
 done
 if [ $NG -ge 8 ]; then
   timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 8 --master-addr 127.0.0.1 --master-port 29599 \
-     bench.py --gpus 8 --config 5 --steps 6 --warmup 2 --no-e2e > $OUT/bench_n8_cfg5.log 2>&1; echo rc=$? >> $OUT/bench_n8_cfg5.log
+     bench.py --gpus 8 --config 5 --steps 6 --warmup 3 --no-e2e > $OUT/bench_n8_cfg5.log 2>&1; echo rc=$? >> $OUT/bench_n8_cfg5.log
 fi
 # configs 4 (re-planned every batch, N2 NVLink shares, C2 stragglers) and 5 (replica, Div_max 0) at the largest N
 NB=$([ $NG -ge 8 ] && echo 8 || echo $NG)
 if [ $NB -ge 2 ]; then
   for C in 4 5; do
     timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $NB --master-addr 127.0.0.1 --master-port 2957$C \
-       bench.py --gpus $NB --config $C --steps 6 --warmup 2 --no-e2e --no-variants > $OUT/bench_n${NB}_cfg$C.log 2>&1; echo rc=$? >> $OUT/bench_n${NB}_cfg$C.log
+       bench.py --gpus $NB --config $C --steps 6 --warmup 3 --no-e2e --no-variants > $OUT/bench_n${NB}_cfg$C.log 2>&1; echo rc=$? >> $OUT/bench_n${NB}_cfg$C.log
   done
 fi
