@@ -259,7 +259,7 @@ def run_single(a):
     import numpy as np
     import torch
 
-    from paper_1907_00434_b200 import mlfabric as m
+    from paper_1907_00434_b200 import mlfabric as m  # noqa: F401  (loads libmlfabric.so: fails loudly if absent)
     from paper_1907_00434_b200.harness import Workload, committed_bytes
     from synthgen import configs
 
@@ -391,7 +391,7 @@ def e2e_single(cid, a):
     """Same metric end to end: pinned host updates -> (H2D of committed ones) -> commit -> D2H pull."""
     import torch
 
-    from paper_1907_00434_b200 import mlfabric as m
+    from paper_1907_00434_b200 import mlfabric as m  # noqa: F401  (loads libmlfabric.so: fails loudly if absent)
     from paper_1907_00434_b200.harness import Workload, committed_bytes
     from synthgen import configs
 
