@@ -329,6 +329,14 @@ mlf_status mlf_execute_phase(mlf_ctx *ctx, const mlf_plan_out *plan, int32_t pha
  * first to its last kernel on this device.  Releases the batch's slots. */
 mlf_status mlf_sync(mlf_ctx *ctx, float *device_ms);
 
+/* Slots are released per executed batch as soon as that batch's device work has finished
+ * (checked by mlf_submit_update).  mlf_release waits until at most max_batches executed
+ * batches are still running and releases the finished ones' slots: a producer with two
+ * slot sets calls mlf_release(ctx, 1) before submitting into the set batch b-1 used, so
+ * batch b+1 is submitted, planned and (host-resident updates) copied in while batch b
+ * still commits.  MLF_E_INVALID if max_batches < 0. */
+mlf_status mlf_release(mlf_ctx *ctx, int32_t max_batches);
+
 /* get(server, model) (Table 1): copy this rank's shard of the latest
  * committed model to dst + shard_begin (device or host memory, dst_is_host)
  * after the last execute; *version = batch-boundary version (R19). */

@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <deque>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -98,6 +99,8 @@ struct mlf_ctx {
   bool dist_p1 = false;                           // distribution phase 1 recorded ev_stop
   unsigned long long *tile_sched = nullptr;       // dynamic tile counters of the bulk commit
   bool dyn_sched = false;
+  std::deque<std::pair<cudaEvent_t, std::vector<int>>> flights;   // executed batches not yet released
+  std::vector<cudaEvent_t> ev_free;                                // their recycled events
   int64_t launches = 0, h2d = 0, d2h = 0;
   CommitImpl impl = CommitImpl::kLdg;
 };
@@ -240,21 +243,29 @@ extern "C" void mlf_destroy(mlf_ctx *c) {
   for (auto e : c->pipe_ev) cudaEventDestroy(e);
   if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
   if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
+  for (auto &f : c->flights) cudaEventDestroy(f.first);
+  for (auto e : c->ev_free) cudaEventDestroy(e);
   for (auto s : c->s_copy) cudaStreamDestroy(s);
   if (c->tile_sched) cudaFree(c->tile_sched);
   delete c;
 }
 
+// Slots are released per executed batch, oldest first, as soon as that batch's device work
+// has finished: with two slot sets a producer can submit (and the pipeline stage) batch b+1
+// while batch b still commits.
 static void release_if_done(mlf_ctx *c) {
-  if (!c->pending) return;
-  cudaError_t q = cudaEventQuery(c->ev_stop);
-  if (q == cudaSuccess) {
-    c->pending = false;
-    std::fill(c->in_flight.begin(), c->in_flight.end(), 0);
-  } else if (q != cudaErrorNotReady) {
-    c->sticky = true;
-    throw Fail{MLF_E_CUDA, std::string("cudaEventQuery: ") + cudaGetErrorString(q)};
+  while (!c->flights.empty()) {
+    cudaError_t q = cudaEventQuery(c->flights.front().first);
+    if (q == cudaErrorNotReady) return;
+    if (q != cudaSuccess) {
+      c->sticky = true;
+      throw Fail{MLF_E_CUDA, std::string("cudaEventQuery: ") + cudaGetErrorString(q)};
+    }
+    for (int w : c->flights.front().second) c->in_flight[w] = 0;
+    c->ev_free.push_back(c->flights.front().first);
+    c->flights.pop_front();
   }
+  if (c->pending && cudaEventQuery(c->ev_stop) == cudaSuccess) c->pending = false;
 }
 
 extern "C" mlf_status mlf_submit_update(mlf_ctx *c, int32_t worker, int64_t version, int64_t t_avail_ns, double norm,
@@ -584,8 +595,9 @@ static void pipeline_commit(mlf_ctx *c, const mlf_plan_out *p, const std::vector
   record_start(c);
   size_t ev = 0;
   const cudaEvent_t begin = pipe_event(c, ev++);
-  CK(cudaEventRecord(begin, c->stream));            // slots / w are free once earlier work is done
-  CK(cudaStreamWaitEvent(c->s_h2d, begin, 0));
+  CK(cudaEventRecord(begin, c->stream));            // w is final once earlier work is done
+  // no wait for the H2D: a slot is only resubmitted after the batch that last read it has
+  // finished (release_if_done), so this batch's copies may overlap the previous batch's tail
   CK(cudaStreamWaitEvent(c->s_d2h, begin, 0));
   std::vector<int> host_w;
   for (int i = 0; i < p->n_commit; ++i) {
@@ -770,6 +782,16 @@ static void phase_commit(mlf_ctx *c, const mlf_plan_out *p) {
   if (trees) replicate_trees(c, p);
   record_start(c);
   CK(cudaEventRecord(c->ev_stop, c->stream));
+  // this batch's slots are released when its own work is done (release_if_done)
+  cudaEvent_t done;
+  if (c->ev_free.empty()) {
+    CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+  } else {
+    done = c->ev_free.back();
+    c->ev_free.pop_back();
+  }
+  CK(cudaEventRecord(done, c->stream));
+  c->flights.emplace_back(done, c->b_worker);
   c->started = false;
   c->pending = true;
   // version accounting (R2): every committed update advances the version
@@ -859,6 +881,24 @@ extern "C" mlf_status mlf_sync(mlf_ctx *c, float *device_ms) {
     if (device_ms) CK(cudaEventElapsedTime(device_ms, c->ev_start, c->ev_stop));
     c->pending = false;
     std::fill(c->in_flight.begin(), c->in_flight.end(), 0);
+    for (auto &f : c->flights) c->ev_free.push_back(f.first);   // all stream-ordered before ev_stop
+    c->flights.clear();
+  });
+  if (st == MLF_E_CUDA && c) c->sticky = true;
+  return st;
+}
+
+extern "C" mlf_status mlf_release(mlf_ctx *c, int32_t max_batches) {
+  mlf_status st = guard([&] {
+    check_ctx(c);
+    if (max_batches < 0) throw Fail{MLF_E_INVALID, "max_batches < 0"};
+    while ((int32_t)c->flights.size() > max_batches) {
+      CK(cudaEventSynchronize(c->flights.front().first));
+      for (int w : c->flights.front().second) c->in_flight[w] = 0;
+      c->ev_free.push_back(c->flights.front().first);
+      c->flights.pop_front();
+    }
+    release_if_done(c);
   });
   if (st == MLF_E_CUDA && c) c->sticky = true;
   return st;

@@ -26,7 +26,7 @@ EXPORTS = (
     "mlf_execute", "mlf_execute_phase", "mlf_sync", "mlf_pull_model", "mlf_stats", "mlf_destroy",
     "mlf_last_error", "mlf_ipc_export", "mlf_ipc_open", "mlf_ipc_close", "mlf_phase_event_export",
     "mlf_phase_events_open", "mlf_gather", "mlf_synth_fill", "mlf_copy_kernel", "mlf_copy_engine",
-    "mlf_copy_bulk", "mlf_plan_distribution", "mlf_distribute_phase",
+    "mlf_copy_bulk", "mlf_plan_distribution", "mlf_distribute_phase", "mlf_release",
 )
 
 
@@ -124,6 +124,7 @@ _lib.mlf_version.argtypes = [_p, _i64p]
 _lib.mlf_execute.argtypes = [_p, C.POINTER(MlfPlanOut)]
 _lib.mlf_execute_phase.argtypes = [_p, C.POINTER(MlfPlanOut), C.c_int32]
 _lib.mlf_sync.argtypes = [_p, C.POINTER(C.c_float)]
+_lib.mlf_release.argtypes = [_p, C.c_int32]
 _lib.mlf_pull_model.argtypes = [_p, _p, C.c_int32, _i64p]
 _lib.mlf_stats.argtypes = [_p, _i64p, _i64p, _i64p]
 _lib.mlf_destroy.argtypes = [_p]
@@ -407,6 +408,10 @@ class Context:
         ms = C.c_float()
         _check(_lib.mlf_sync(self._h, C.byref(ms)))
         return ms.value
+
+    def release(self, max_batches: int):
+        """mlf_release: wait until <= max_batches executed batches run; free the others' slots."""
+        _check(_lib.mlf_release(self._h, int(max_batches)))
 
     def pull(self, dst, dst_is_host: bool) -> int:
         v = C.c_int64()

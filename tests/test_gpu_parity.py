@@ -179,6 +179,51 @@ def test_bf16_16kb_layout_bitwise(boundary):
         assert np.array_equal(bits(b_h[idx]), bits(br))
 
 
+def test_double_buffered_batches_overlap_and_stay_exact():
+    # two slot sets with host-resident updates: batch s+1 is submitted and its H2D starts
+    # (mlf_release(ctx, 1)) while batch s still commits; the model after every batch equals
+    # the oracle's sequential commits, and the pulled host copy matches the device model
+    dev = torch.device("cuda", 0)
+    S, W, B = 1_000_003, 6, 5
+    slots = [torch.empty(S, dtype=torch.float32, device=dev) for _ in range(2 * W)]
+    hosts = [torch.empty(S, dtype=torch.float32).pin_memory() for _ in range(2 * W)]
+    wt = torch.empty(S, dtype=torch.float32, device=dev)
+    m.synth_fill(0, wt.data_ptr(), S, dtype=m.MLF_F32, seed=SEED, kind=2)
+    pulled = torch.empty(S, dtype=torch.float32).pin_memory()
+    os.environ["MLF_COMMIT_IMPL"] = "bulk"
+    ctx = m.Context(device=0, model_shard=wt, update_slots=slots, lr=0.01, model_elems=S,
+                    worker_node=[i % W for i in range(2 * W)], n_nodes=W, node_rank=[0] * W,
+                    stream=torch.cuda.current_stream().cuda_stream)
+    for i in range(2 * W):
+        ctx.set_update_host(i, hosts[i].data_ptr())
+    ctx.set_pull_host(pulled.data_ptr())
+    idx = np.unique(np.concatenate([np.random.default_rng(3).integers(0, S, 50_000), np.arange(S - 7, S)]))
+    w_ref = sg.w0_values(SEED, idx)
+    plan = {"n_commit": W, "order": list(range(W)), "drop_reason": [0] * W, "group": [0] * W, "n_direct": W,
+            "n_groups": 0, "group_node": [], "n_server_commits": W, "commit_first": list(range(W)),
+            "commit_count": [1] * W, "replica_boundary_commit": -1, "n_punted": 0, "punted": []}
+    pbs = []
+    for s in range(B):
+        ctx.release(1)                                   # set s % 2 is free (batch s - 2 done)
+        base = (s % 2) * W
+        for k in range(W):                               # the producer writes its update for batch s
+            t = torch.empty(S, dtype=torch.float32, device=dev)
+            m.synth_fill(0, t.data_ptr(), S, dtype=m.MLF_F32, seed=SEED, kind=1, a=k, b=s)
+            hosts[base + k].copy_(t.cpu())
+            ctx.submit(base + k, 0, 0, 1.0)
+        pbs.append(m.plan_from_dict(plan))
+        ctx.execute(pbs[-1])
+        w_ref, _, _ = execute_plan(w_ref, plan, lambda g: sg.update_values(SEED, g, s, idx, sg.DTYPE_F32), 0.01)
+    ctx.sync()
+    torch.cuda.synchronize()
+    assert np.array_equal(bits(wt.cpu().numpy()[idx]), bits(w_ref))
+    assert np.array_equal(bits(pulled.numpy()[idx]), bits(w_ref))
+    with pytest.raises(m.MlfError) as e:
+        ctx.release(-1)
+    assert e.value.code == m.MLF_E_INVALID
+    ctx.close()
+
+
 @pytest.mark.parametrize("tile", [1024, 2048, 4096])
 def test_bulk_commit_under_concurrent_copy_engine_traffic(tile):
     # regression: without fence.proxy.async between the empty-barrier wait and the bulk copy
