@@ -334,7 +334,9 @@ mlf_status mlf_sync(mlf_ctx *ctx, float *device_ms);
  * batches are still running and releases the finished ones' slots: a producer with two
  * slot sets calls mlf_release(ctx, 1) before submitting into the set batch b-1 used, so
  * batch b+1 is submitted, planned and (host-resident updates) copied in while batch b
- * still commits.  MLF_E_INVALID if max_batches < 0. */
+ * still commits.  MLF_E_INVALID if max_batches < 0.  With world > 1 the release is local:
+ * peers' kernels may still read this rank's slots, so a producer refills a slot only after
+ * every rank has synced the batch that read it (a host barrier, as multigpu.py does). */
 mlf_status mlf_release(mlf_ctx *ctx, int32_t max_batches);
 
 /* get(server, model) (Table 1): copy this rank's shard of the latest
