@@ -789,6 +789,7 @@ __global__ void __launch_bounds__(kThreads, 1) tree_reduce_bulk(const __grid_con
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)kStages * kStageBytes);
   uint64_t *empty = full + kStages;
+  int64_t *tile_of = reinterpret_cast<int64_t *>(empty + kStages);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t n_bulk = a.n & ~int64_t(7);
   const int64_t n_tiles = (n_bulk + kTile - 1) / kTile;
@@ -805,14 +806,24 @@ __global__ void __launch_bounds__(kThreads, 1) tree_reduce_bulk(const __grid_con
   if (warp == kConsumerWarps) {
     if (lane == 0) {
       uint32_t L = 0;
-      for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      int64_t t = a.sched ? (int64_t)atomicAdd(&a.sched[0], 1ull) : (int64_t)blockIdx.x;
+      for (;;) {
         const int64_t e0 = t * kTile;
-        const uint32_t cnt = (uint32_t)(n_bulk - e0 < kTile ? n_bulk - e0 : kTile);
+        const uint32_t cnt = t < n_tiles ? (uint32_t)(n_bulk - e0 < kTile ? n_bulk - e0 : kTile) : 0u;
+        int64_t t_next = 0;
+        if (t < n_tiles) t_next = a.sched ? (int64_t)atomicAdd(&a.sched[0], 1ull) : t + gridDim.x;
         for (int j = 0; j < a.n_ops; ++j, ++L) {
           const uint32_t s = L % kStages;
           if (L >= (uint32_t)kStages) {
             mbar_wait(&empty[s], ((L / kStages) & 1) ^ 1);
             fence_proxy_async_smem();
+          }
+          if (j == 0) {
+            tile_of[s] = t < n_tiles ? t : -1;        // the first member's stage carries the tile index
+            if (t >= n_tiles) {
+              mbar_arrive(&full[s]);
+              break;
+            }
           }
           const bool bf = a.flag[j] & kOpBf16;
           const void *src = bf ? (const void *)(static_cast<const uint16_t *>(a.op[j]) + a.src_off + e0)
@@ -821,12 +832,25 @@ __global__ void __launch_bounds__(kThreads, 1) tree_reduce_bulk(const __grid_con
           mbar_expect_tx(&full[s], bytes);
           bulk_g2s(smem + (size_t)s * kStageBytes, src, bytes, &full[s]);
         }
+        if (t >= n_tiles) break;
+        t = t_next;
+      }
+      if (a.sched) {                                  // the last CTA resets the counters
+        __threadfence();
+        if (atomicAdd(&a.sched[1], 1ull) == gridDim.x - 1) {
+          a.sched[0] = 0;
+          a.sched[1] = 0;
+          __threadfence();
+        }
       }
     }
   } else {
     const int tid = threadIdx.x;
     uint32_t L = 0;
-    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    for (;;) {
+      mbar_wait(&full[L % kStages], (L / kStages) & 1);
+      const int64_t t = tile_of[L % kStages];
+      if (t < 0) break;
       const int64_t e0 = t * kTile;
       const int cnt = (int)(n_bulk - e0 < kTile ? n_bulk - e0 : kTile);
       float4 x[kChunks];
@@ -883,7 +907,15 @@ cudaError_t launch_reduce_bulk(const ReduceArgs &a, cudaStream_t s, int sm_count
   if (a.n_ops < 1 || a.n < 1) return cudaSuccess;
   const int64_t n_tiles = ((a.n & ~int64_t(7)) + kTile - 1) / kTile;
   int grid = (int)(n_tiles < sm_count ? (n_tiles > 0 ? n_tiles : 1) : sm_count);
-  bulk::tree_reduce_bulk<kTile, kStages><<<grid, bulk::kThreads, smem, s>>>(a);
+  int64_t tile_bytes = 0;                          // dynamic tiles only when a tile loads >= 64 KB
+  for (int j = 0; j < a.n_ops; ++j) tile_bytes += (int64_t)kTile * ((a.flag[j] & kOpBf16) ? 2 : 4);
+  if (a.sched && tile_bytes < (64 << 10)) {
+    ReduceArgs b = a;
+    b.sched = nullptr;
+    bulk::tree_reduce_bulk<kTile, kStages><<<grid, bulk::kThreads, smem, s>>>(b);
+  } else {
+    bulk::tree_reduce_bulk<kTile, kStages><<<grid, bulk::kThreads, smem, s>>>(a);
+  }
   return cudaGetLastError();
 }
 

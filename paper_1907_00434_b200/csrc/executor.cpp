@@ -430,6 +430,7 @@ static void reduce_local_groups(mlf_ctx *c, const mlf_plan_out *p) {
     if (r != c->cfg.rank) continue;
     if (cnt > kMaxOps) throw Fail{MLF_E_CAPACITY, "group larger than kMaxOps"};
     ReduceArgs a;
+    a.sched = c->dyn_sched ? c->tile_sched : nullptr;
     a.out = c->agg_scratch[(size_t)r * c->cfg.agg_slots + s];
     a.n = c->cfg.model_elems;
     a.src_off = 0;

@@ -45,6 +45,7 @@ struct ReduceArgs {
   int32_t n_ops;
   const void *op[kMaxOps];
   uint8_t flag[kMaxOps];
+  unsigned long long *sched;  // dynamic tile counters (bulk reduce; as CommitArgs::sched) or nullptr
 };
 
 // Momentum commit (Eq. 2 with gamma > 0, aggregate form): per operand the weights of the two
