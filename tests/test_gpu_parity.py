@@ -179,6 +179,36 @@ def test_bf16_16kb_layout_bitwise(boundary):
         assert np.array_equal(bits(b_h[idx]), bits(br))
 
 
+def test_many_batches_dynamic_tile_counters():
+    # 300 launches on one context with operand counts that switch between dynamic and
+    # round-robin tiles (and between tile sizes): the tile counters must be back at zero before
+    # every launch, or some tiles would be skipped or done twice
+    dev = torch.device("cuda", 0)
+    S, W, B = 20_000_003, 8, 300                      # 4096-element tiles: n >= 3 operands -> dynamic
+    rng = np.random.default_rng(300)
+    slots = [torch.empty(S, dtype=torch.float32, device=dev) for _ in range(W)]
+    for k, t in enumerate(slots):
+        m.synth_fill(0, t.data_ptr(), S, dtype=m.MLF_F32, seed=SEED, kind=1, a=k, b=0)
+    wt = torch.empty(S, dtype=torch.float32, device=dev)
+    m.synth_fill(0, wt.data_ptr(), S, dtype=m.MLF_F32, seed=SEED, kind=2)
+    os.environ["MLF_COMMIT_IMPL"] = "bulk"
+    ctx = m.Context(device=0, model_shard=wt, update_slots=slots, lr=0.01, model_elems=S,
+                    stream=torch.cuda.current_stream().cuda_stream)
+    idx = np.unique(np.concatenate([rng.integers(0, S, 20_000), np.arange(S - 9, S), np.arange(0, 9)]))
+    ops = {k: sg.update_values(SEED, k, 0, idx, sg.DTYPE_F32) for k in range(W)}
+    w_ref = sg.w0_values(SEED, idx)
+    for b in range(B):
+        n = int(rng.integers(1, W + 1))
+        p = random_plan(rng, W, n_commit=n, boundary=-1)
+        for k in range(W):
+            ctx.submit(k, 0, 0, 1.0)
+        ctx.execute(m.plan_from_dict(p))
+        ctx.sync()
+        w_ref, _, _ = execute_plan(w_ref, p, lambda g: ops[g], 0.01)
+    assert np.array_equal(bits(wt.cpu().numpy()[idx]), bits(w_ref))
+    ctx.close()
+
+
 def test_double_buffered_batches_overlap_and_stay_exact():
     # two slot sets with host-resident updates: batch s+1 is submitted and its H2D starts
     # (mlf_release(ctx, 1)) while batch s still commits; the model after every batch equals
