@@ -179,6 +179,23 @@ def test_bf16_16kb_layout_bitwise(boundary):
         assert np.array_equal(bits(b_h[idx]), bits(br))
 
 
+def test_distribution_on_one_gpu():
+    # NEXT-4 with world = 1: the single view is filled from the single shard (ragged length)
+    dev = torch.device("cuda", 0)
+    S = 3_000_017
+    w = torch.empty(S, dtype=torch.float32, device=dev)
+    m.synth_fill(0, w.data_ptr(), S, dtype=m.MLF_F32, seed=SEED, kind=2)
+    view = torch.full((-(-S // 64) * 64,), float("nan"), device=dev)
+    ctx = m.Context(device=0, model_shard=w, update_slots=[], lr=0.0, model_elems=S, node_rank=[0], n_nodes=1,
+                    stream=torch.cuda.current_stream().cuda_stream)
+    dp = m.plan_distribution(1, [10**9], [10**9], [0, 0, 0], [0], S * 4)
+    assert dp["n_direct"] == 3 and dp["t_total_ns"] == 0        # same node: zero-time pulls
+    src = ctx.distribute(dp, [0, 0, 0], [view.data_ptr()], [w.data_ptr()], [0], [S])
+    ctx.sync()
+    assert src == -1 and torch.equal(view[:S].view(torch.int32), w.view(torch.int32))
+    ctx.close()
+
+
 def test_many_batches_dynamic_tile_counters():
     # 300 launches on one context with operand counts that switch between dynamic and
     # round-robin tiles (and between tile sizes): the tile counters must be back at zero before
