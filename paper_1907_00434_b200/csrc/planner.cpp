@@ -448,7 +448,32 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
   const int G = (int)c.servers.size();
   std::vector<i64> ten(n);
   std::vector<uint8_t> ok(n);
-  std::vector<int> pool, uniq, rep;
+  std::vector<int> pool, uniq, rep(n, -1);
+  // t_en is a pure function of (network, node, size, t_avail): updates sharing the triple
+  // (virtual workers on one GPU usually share all three) form one class, evaluated once per scan
+  std::vector<int> cls(n), cls_rep, cls_stamp;
+  {
+    std::vector<int> byk(n);
+    for (int g = 0; g < n; ++g) byk[g] = g;
+    std::sort(byk.begin(), byk.end(), [&](int a, int b) {
+      const Item &x = batch[a], &y = batch[b];
+      if (x.node != y.node) return x.node < y.node;
+      if (x.size != y.size) return x.size < y.size;
+      if (x.t_avail != y.t_avail) return x.t_avail < y.t_avail;
+      return a < b;
+    });
+    int k = -1;
+    for (int i = 0; i < n; ++i) {
+      const Item &x = batch[byk[i]];
+      if (i == 0 || x.node != batch[byk[i - 1]].node || x.size != batch[byk[i - 1]].size ||
+          x.t_avail != batch[byk[i - 1]].t_avail)
+        ++k;
+      cls[byk[i]] = k;
+    }
+    cls_rep.assign(k + 1, -1);
+    cls_stamp.assign(k + 1, -1);
+  }
+  int scan = 0;
 
   // ShrtDline(pos, cands, NW + L0): the due set's argmin if any, else ShrtUp (R4, R6).
   auto pick = [&](i64 pos, const std::vector<int> &cands, const Pending *L0) -> int {
@@ -461,20 +486,17 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
     pool.clear();
     for (int g : cands)
       if (!any_due || dl[g] == pos) pool.push_back(g);
-    // t_en is a pure function of (network, node, size, t_avail): evaluate each distinct
-    // triple once (virtual workers on one GPU usually share all three)
+    // one evaluation per class; its representative is the class's first member in the pool
+    ++scan;
     uniq.clear();
-    rep.assign(n, -1);
     for (int g : pool) {
-      int u = -1;
-      for (int q : uniq)
-        if (batch[q].node == batch[g].node && batch[q].size == batch[g].size &&
-            batch[q].t_avail == batch[g].t_avail) {
-          u = q;
-          break;
-        }
-      if (u < 0) uniq.push_back(g);
-      rep[g] = u < 0 ? g : u;
+      const int k = cls[g];
+      if (cls_stamp[k] != scan) {
+        cls_stamp[k] = scan;
+        cls_rep[k] = g;
+        uniq.push_back(g);
+      }
+      rep[g] = cls_rep[k];
     }
     Pool::get().run(
         (int)uniq.size(),
