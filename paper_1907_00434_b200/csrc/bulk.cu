@@ -13,7 +13,10 @@
 //   * 8 consumer warps wait on the stage's full mbarrier, fold the tile from
 //     shared memory in the pinned order, release the stage (empty mbarrier),
 //     and write w (and the mirror) back with 128-bit streaming stores.
-// Tiles are dealt round-robin to the persistent CTAs (tile = cta + k * grid).
+// Tiles come from a global counter when a tile loads >= 64 KB (one atomic per tile, fetched a
+// tile ahead, the last CTA resets the counter; the tile index rides with the first stage of
+// the tile), else round-robin (tile = cta + k * grid).  A stage is refilled only after
+// fence.proxy.async: its reuse is a write-after-read across proxies.
 #include <cuda_runtime.h>
 
 #include <cstdint>
