@@ -103,6 +103,18 @@ def test_two_ranks_distribution_trees():
     assert "case degraded0: groups=1" in r.stdout
 
 
+def test_eight_ranks_sharing_the_visible_gpus():
+    # world = 8 (the box size the north star names) on whatever GPUs are visible: 8 shards, 8
+    # fused-get destinations, the 8-way plan — bitwise vs the oracle
+    out = _run(8, "--cid", "3", "--S", "2000011", "--steps", "1", "--workers", "64", timeout=900)
+    assert "MULTIGPU_OK fold" in out and "MULTIGPU_OK tree" in out and "MULTIGPU_OK staged" in out
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", "--nnodes=1", "--nproc-per-node=8",
+           os.path.join(HERE, "allreduce_check.py"), "--S", "500009", "--workers", "8"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, MASTER_ADDR="127.0.0.1", OMP_NUM_THREADS="1"))
+    assert r.returncode == 0 and "ALLREDUCE_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
 def test_all_gpus_if_several():
     n = torch.cuda.device_count()
     if n < 4:
