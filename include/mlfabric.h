@@ -269,6 +269,10 @@ typedef struct {
    * (copy engines reach a higher NVLink rate than SM peer reads).  NULL / 0 = SM peer reads. */
   void *stage_buf;
   int64_t stage_bytes;
+  /* 1: bcast[0] (n_bcast == 1) is an NVLS multicast address bound to every GPU's view (e.g.
+   * PyTorch symmetric memory's multicast_ptr): the fused get stores each final tile once
+   * with multimem.st and NVSwitch replicates it, instead of one store per peer view. */
+  int32_t bcast_multicast;
 } mlf_config;
 
 typedef struct mlf_ctx mlf_ctx;

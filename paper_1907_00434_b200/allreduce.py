@@ -39,10 +39,13 @@ class MlfAllReduce:
     GPU's result view (push and get in ONE kernel per GPU, NVLink stores overlapped with the
     reduce); fused = False: push, barrier, then get with mlf_gather (peer loads)."""
 
-    def __init__(self, cfg: dict, rank: int, world: int, device: int, ctrl, fused: bool = True):
+    def __init__(self, cfg: dict, rank: int, world: int, device: int, ctrl, fused: bool = True,
+                 multicast: bool = False):
+        """multicast = True (with fused): the get stores through an NVLS multicast address."""
         self.cfg, self.rank, self.world, self.device, self.ctrl = cfg, rank, world, device, ctrl
         self.fused = fused
-        self.sw = ShardedWorkload(cfg, rank, world, device, ctrl, mode="fold", fused_get=fused)
+        self.sw = ShardedWorkload(cfg, rank, world, device, ctrl, mode="fold", fused_get=fused,
+                                  multicast=multicast and fused)
         dev = torch.device("cuda", device)
         self.out = self.sw.view[:cfg["S"]] if fused else torch.empty(cfg["S"], dtype=torch.float32, device=dev)
         blobs = [None] * world
@@ -82,8 +85,14 @@ def bench_allreduce(S: int, rank: int, world: int, device: int, ctrl, steps: int
     """MLfabric AllReduce vs NCCL all_reduce on the same per-GPU buffer of S fp32 values."""
     cfg = allreduce_config(S, world)
     res = {}
-    for fused in (True, False):
-        ar = MlfAllReduce(cfg, rank, world, device, ctrl, fused=fused)
+    variants = [(True, False), (False, False)]
+    if dist.get_backend() == "nccl":
+        variants.append((True, True))             # NVLS multicast get (one GPU per rank)
+    for fused, mc in variants:
+        try:
+            ar = MlfAllReduce(cfg, rank, world, device, ctrl, fused=fused, multicast=mc)
+        except RuntimeError:                      # no multicast on this box
+            continue
         ar.sw.fill(0)
         push = get = wall = 0.0
         for s in range(warmup + steps):
@@ -91,7 +100,7 @@ def bench_allreduce(S: int, rank: int, world: int, device: int, ctrl, steps: int
             if s >= warmup:
                 push, get, wall = push + mp, get + mg, wall + mw
         ar.close()
-        res[fused] = (push / steps, get / steps, wall / steps)
+        res[(fused, mc)] = (push / steps, get / steps, wall / steps)
     # NCCL on the default (NCCL) process group, same bytes per GPU
     t = torch.ones(S, dtype=torch.float32, device=torch.device("cuda", device))
     nccl_ms = None
@@ -116,11 +125,14 @@ def bench_allreduce(S: int, rank: int, world: int, device: int, ctrl, steps: int
     def busbw(ms):
         return round(2 * (world - 1) / world * nbytes / (ms / 1e3) / 1e9, 1) if ms else None
 
-    fp, _, fw = res[True]
-    gp, gg, gw = res[False]
+    fp, _, fw = res[(True, False)]
+    gp, gg, gw = res[(False, False)]
+    mcp = res[(True, True)][0] if (True, True) in res else None
     return {"bytes_per_gpu": nbytes,
             "mlfabric_fused_ms": round(fp, 4), "mlfabric_fused_busbw_GBps": busbw(fp),
             "mlfabric_fused_wall_ms": round(fw, 3),
+            "mlfabric_fused_multicast_ms": round(mcp, 4) if mcp else None,
+            "mlfabric_fused_multicast_busbw_GBps": busbw(mcp) if mcp else None,
             "mlfabric_push_then_gather_ms": round(gp + gg, 4), "push_ms": round(gp, 4), "gather_ms": round(gg, 4),
             "mlfabric_push_then_gather_busbw_GBps": busbw(gp + gg),
             "nccl_ms": round(nccl_ms, 4) if nccl_ms else None, "nccl_busbw_GBps": busbw(nccl_ms),

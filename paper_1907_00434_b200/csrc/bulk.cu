@@ -68,6 +68,23 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       : "memory");
 }
 
+// fused-get store of one float4: a plain streaming store to a peer view, or one multimem
+// store to an NVLS multicast address that NVSwitch replicates into every GPU's view
+__device__ __forceinline__ void store_get(float *dst, float4 v, bool mc) {
+  if (mc)
+    asm volatile("multimem.st.weak.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(v.x), "f"(v.y), "f"(v.z),
+                 "f"(v.w)
+                 : "memory");
+  else
+    __stcs(reinterpret_cast<float4 *>(dst), v);
+}
+__device__ __forceinline__ void store_get1(float *dst, float v, bool mc) {
+  if (mc)
+    asm volatile("multimem.st.weak.global.f32 [%0], %1;" ::"l"(dst), "f"(v) : "memory");
+  else
+    *dst = v;
+}
+
 __device__ __forceinline__ float4 add4(float4 a, float4 b) {
   return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
 }
@@ -227,7 +244,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_bulk(const __grid_co
 #pragma unroll
         for (int k = 0; k < kChunks; ++k) {
           const int c = tid + k * kConsumers;
-          if (c * 4 < cnt) __stcs(reinterpret_cast<float4 *>(a.bcast[b] + e0) + c, w[k]);
+          if (c * 4 < cnt) store_get(a.bcast[b] + e0 + 4 * c, w[k], a.bcast_mc != 0);
         }
       }
     }
@@ -250,8 +267,9 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_bulk(const __grid_co
         }
       }
       a.w[e] = wv;
-      for (int b = 0; b < a.n_bcast; ++b) a.bcast[b][e] = wv;
+      for (int b = 0; b < a.n_bcast; ++b) store_get1(a.bcast[b] + e, wv, a.bcast_mc != 0);
     }
+    if (a.bcast_mc) __threadfence_system();        // multimem stores visible system-wide at exit
   }
 }
 
@@ -754,7 +772,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_bulk_h(const __grid_
 #pragma unroll
         for (int k = 0; k < kChunks; ++k) {
           const int c = tid + k * kConsumers;
-          if (c * 4 < cnt) __stcs(reinterpret_cast<float4 *>(a.bcast[b] + e0) + c, w[k]);
+          if (c * 4 < cnt) store_get(a.bcast[b] + e0 + 4 * c, w[k], a.bcast_mc != 0);
         }
       }
     }
@@ -774,8 +792,9 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_bulk_h(const __grid_
         }
       }
       a.w[e] = wv;
-      for (int b = 0; b < a.n_bcast; ++b) a.bcast[b][e] = wv;
+      for (int b = 0; b < a.n_bcast; ++b) store_get1(a.bcast[b] + e, wv, a.bcast_mc != 0);
     }
+    if (a.bcast_mc) __threadfence_system();        // multimem stores visible system-wide at exit
   }
 }
 

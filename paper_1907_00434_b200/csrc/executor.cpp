@@ -128,6 +128,8 @@ extern "C" mlf_status mlf_init(const mlf_config *cfg, int64_t v0, mlf_ctx **out)
     if (k.n_bcast < 0 || k.n_bcast > kMaxBcast || (k.n_bcast > 0 && !k.bcast))
       throw Fail{MLF_E_INVALID, "fused get: 0..8 destinations"};
     if (k.n_bcast > 0 && k.gamma != 0.f) throw Fail{MLF_E_INVALID, "fused get is implemented for gamma = 0"};
+    if (k.bcast_multicast != 0 && (k.bcast_multicast != 1 || k.n_bcast != 1))
+      throw Fail{MLF_E_INVALID, "bcast_multicast needs exactly one (multicast) destination"};
     for (int i = 0; i < k.n_bcast; ++i)
       if (!k.bcast[i] || (reinterpret_cast<uintptr_t>(k.bcast[i] + k.shard_begin) & 15))
         throw Fail{MLF_E_INVALID, "fused get destination null or misaligned"};
@@ -533,6 +535,7 @@ static void launch_ops(mlf_ctx *c, float *w, float *backup, const std::vector<Co
     a.backup_after = -2;
     if (first_launch && boundary == 0) a.backup_after = -1;
     a.n_bcast = 0;
+    a.bcast_mc = c->cfg.bcast_multicast;
     a.sched = c->dyn_sched ? c->tile_sched : nullptr;
     if (bcast && i1 == ops.size())                  // only the pass that finishes w broadcasts it
       for (float *d : c->bcast) a.bcast[a.n_bcast++] = d + c->cfg.shard_begin + off;

@@ -32,6 +32,7 @@ struct CommitArgs {
   // new model happens tile by tile inside the commit pass
   int32_t n_bcast;
   float *bcast[kMaxBcast];
+  int32_t bcast_mc;     // 1: bcast[0] is an NVLS multicast address (multimem.st, the switch replicates)
   // dynamic tile scheduling (bulk kernel): [0] next tile, [1] CTAs done; zero between launches
   // (the last CTA resets both).  nullptr = static round-robin tiles.
   unsigned long long *sched;

@@ -23,7 +23,7 @@ class Workload:
     def __init__(self, cfg: dict, *, device: int = 0, rank: int = 0, world: int = 1, variant: int = 0,
                  peer_slots=None, backup_ptr=None, agg_slots: int = 0, agg_scratch=None, stream=None,
                  slot_tensors: dict | None = None, backup_h_ptr=None, retain_table=None, bcast=None,
-                 stage=None):
+                 stage=None, bcast_multicast: bool = False):
         self.cfg = cfg
         self.device, self.rank, self.world = device, rank, world
         self.variant = variant
@@ -74,7 +74,7 @@ class Workload:
                              gamma=self.gamma, history=self.h,
                              backup_history=(backup_h_ptr if backup_h_ptr is not None else self.backup_h),
                              replica_mode=self.replica_mode, retain_slots=retain_table, bcast=bcast,
-                             stage=stage)
+                             stage=stage, bcast_multicast=bcast_multicast)
         self.v_init, self.v_prev = 0, 0
         self.iteration = 0
         self.carried = []

@@ -87,7 +87,7 @@ class MlfConfig(C.Structure):
                 ("stream", _p), ("gamma", C.c_float), ("history_shard", _p), ("backup_history", _p),
                 ("replica_mode", C.c_int32), ("n_retain", C.c_int32), ("retain_slot", C.POINTER(_p)),
                 ("n_bcast", C.c_int32), ("bcast", C.POINTER(_p)),
-                ("stage_buf", _p), ("stage_bytes", C.c_int64)]
+                ("stage_buf", _p), ("stage_bytes", C.c_int64), ("bcast_multicast", C.c_int32)]
 
 
 class MlfIpcHandle(C.Structure):
@@ -326,7 +326,7 @@ class Context:
                  backup_shard=None, worker_rank=None, node_rank=None, n_nodes=None, agg_slots: int = 0,
                  agg_scratch=None, stream=None, v0: int = 0, worker_node=None, gamma: float = 0.0,
                  history=None, backup_history=None, replica_mode: int = 0, retain_slots=None, bcast=None,
-                 stage=None):
+                 stage=None, bcast_multicast: bool = False):
         """update_slots: list of int device pointers (or torch tensors); model_shard/backup_shard:
         torch tensors or int pointers; stream: int cudaStream_t (None -> default stream)."""
         def ptr(x):
@@ -357,6 +357,7 @@ class Context:
         if bc:
             self.cfg.n_bcast = len(bc)
             self.cfg.bcast = self._bc
+            self.cfg.bcast_multicast = 1 if bcast_multicast else 0
         if stage is not None:                       # copy-engine staging buffer (torch tensor)
             self.cfg.stage_buf = ptr(stage)
             self.cfg.stage_bytes = stage.numel() * stage.element_size()

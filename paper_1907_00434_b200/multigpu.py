@@ -83,7 +83,7 @@ class ShardedWorkload:
     """Rank `rank`'s part of a config sharded over `world` GPUs."""
 
     def __init__(self, cfg: dict, rank: int, world: int, device: int, ctrl, mode: str = "fold", variant: int = 0,
-                 fused_get: bool = False, stage_mib: int = 0):
+                 fused_get: bool = False, stage_mib: int = 0, multicast: bool = False):
         """mode: "fold" (SM peer loads inside the commit kernel), "tree" (tree_reduce on the
         aggregator GPU first) or "staged" (fold whose remote operand slices are pulled by the
         copy engines into a local staging buffer of stage_mib MiB, default 4096)."""
@@ -116,6 +116,20 @@ class ShardedWorkload:
                       if mode == "staged" else None)
         # fused get: every GPU holds a full-length view of the model, written by all shards' commits
         self.view = torch.empty(-(-S // 64) * 64, dtype=torch.float32, device=dev) if fused_get else None
+        # NVLS: the views are PyTorch symmetric memory bound to one multicast object, so the
+        # fused get stores each tile once (multimem.st) and NVSwitch replicates it
+        self.mc_ptr = 0
+        if fused_get and multicast:
+            import torch.distributed._symmetric_memory as symm_mem
+            self.view = symm_mem.empty(-(-S // 64) * 64, dtype=torch.float32, device=dev)
+            try:
+                self._symm = symm_mem.rendezvous(self.view, dist.group.WORLD)
+            except RuntimeError:                  # older builds: the group must be enabled first
+                symm_mem.enable_symm_mem_for_group(dist.group.WORLD.group_name)
+                self._symm = symm_mem.rendezvous(self.view, dist.group.WORLD)
+            self.mc_ptr = int(self._symm.multicast_ptr)
+            if not self.mc_ptr:
+                raise RuntimeError("multicast requested but this box's GPUs offer no NVLS multicast")
         self.scratch = (torch.empty((self.n_slots, self.row), dtype=torch.float32, device=dev)
                         if self.n_slots else None)
         torch.cuda.synchronize(dev)
@@ -126,7 +140,8 @@ class ShardedWorkload:
                              if self.mirror_h is not None else None),
                 "scratch": m.ipc_export(device, self.scratch.data_ptr()) if self.scratch is not None else None,
                 "retain": m.ipc_export(device, self.retain.data_ptr()) if self.retain is not None else None,
-                "view": m.ipc_export(device, self.view.data_ptr()) if self.view is not None else None}
+                "view": (m.ipc_export(device, self.view.data_ptr())
+                         if self.view is not None and not self.mc_ptr else None)}
         allinfo = [None] * world
         dist.all_gather_object(allinfo, mine, group=ctrl)
         allinfo.sort(key=lambda d: d["rank"])
@@ -158,13 +173,15 @@ class ShardedWorkload:
                 base = self.retain.data_ptr() if info["rank"] == rank else self.mapper.open(info["retain"])
                 retain_tab += [base + s * rowb for s in range(self.n_retain)]
         bcast = None
-        if self.view is not None:
+        if self.mc_ptr:
+            bcast = [self.mc_ptr]
+        elif self.view is not None:
             bcast = [self.view.data_ptr() if info["rank"] == rank else self.mapper.open(info["view"])
                      for info in allinfo]
         self.wl = Workload(cfg, device=device, rank=rank, world=world, variant=variant, peer_slots=peer_slots,
                            backup_ptr=backup_ptr, agg_slots=self.n_slots, agg_scratch=scratch_tab,
                            slot_tensors=slot_tensors, backup_h_ptr=backup_h_ptr, retain_table=retain_tab,
-                           bcast=bcast, stage=self.stage)
+                           bcast=bcast, stage=self.stage, bcast_multicast=bool(self.mc_ptr))
         ev = self.wl.ctx.phase_event()
         evs = [None] * world
         dist.all_gather_object(evs, (rank, ev), group=ctrl)

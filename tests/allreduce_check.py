@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--S", type=int, default=1_000_003)
     ap.add_argument("--workers", type=int, default=None)
     ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--multicast", action="store_true", help="also the NVLS multicast fused get")
     a = ap.parse_args()
     rank, world, local, ctrl = init_dist()
     device = local % torch.cuda.device_count()
@@ -40,14 +41,16 @@ def main():
     idx = np.unique(np.concatenate([rng.integers(0, cfg["S"], 8000), np.arange(cfg["S"] - 11, cfg["S"])]))
     for fused in (True, False):
         check(cfg, rank, world, device, ctrl, idx, a.steps, fused)
+    if a.multicast:
+        check(cfg, rank, world, device, ctrl, idx, a.steps, True, multicast=True)
     if rank == 0:
-        print(f"ALLREDUCE_OK world={world} S={cfg['S']} workers={cfg['W']}", flush=True)
+        print(f"ALLREDUCE_OK world={world} S={cfg['S']} workers={cfg['W']} multicast={a.multicast}", flush=True)
     dist.barrier(group=ctrl)
     dist.destroy_process_group()
 
 
-def check(cfg, rank, world, device, ctrl, idx, steps, fused):
-    ar = MlfAllReduce(cfg, rank, world, device, ctrl, fused=fused)
+def check(cfg, rank, world, device, ctrl, idx, steps, fused, multicast=False):
+    ar = MlfAllReduce(cfg, rank, world, device, ctrl, fused=fused, multicast=multicast)
     v = vp = 0
     for it in range(steps):
         ar.sw.fill(it)
@@ -64,7 +67,7 @@ def check(cfg, rank, world, device, ctrl, idx, steps, fused):
                               commits_from_plan(op, lambda g: sg.update_values(cfg["seed"], g, it, idx)), -1.0)
         got = ar.out.cpu().numpy()[idx]
         assert np.array_equal(got.view(np.uint32), ref.view(np.uint32)), \
-            f"rank {rank}: allreduce mismatch (fused={fused})"
+            f"rank {rank}: allreduce mismatch (fused={fused}, multicast={multicast})"
         vp, v = v, v + 1
     ar.close()
 
