@@ -103,6 +103,17 @@ def test_two_ranks_distribution_trees():
     assert "case degraded0: groups=1" in r.stdout
 
 
+def test_two_gpus_multicast_get():
+    # NVLS multicast fused get: needs one GPU per rank (the multicast object spans devices)
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", "--nnodes=1", "--nproc-per-node=2",
+           os.path.join(HERE, "allreduce_check.py"), "--S", "1000003", "--workers", "4", "--multicast"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, MASTER_ADDR="127.0.0.1", OMP_NUM_THREADS="1"))
+    assert r.returncode == 0 and "multicast=True" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
 def test_eight_ranks_sharing_the_visible_gpus():
     # world = 8 (the box size the north star names) on whatever GPUs are visible: 8 shards, 8
     # fused-get destinations, the 8-way plan — bitwise vs the oracle
