@@ -68,6 +68,21 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       : "memory");
 }
 
+// the same copy with an L2 eviction-priority hint (operands are read exactly once)
+__device__ __forceinline__ void bulk_g2s_hint(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
+                                              uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
 // fused-get store of one float4: a plain streaming store to a peer view, or one multimem
 // store to an NVLS multicast address that NVSwitch replicates into every GPU's view
 __device__ __forceinline__ void store_get(float *dst, float4 v, bool mc) {
@@ -127,6 +142,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_bulk(const __grid_co
     // consumers; index -1 (no stage data) ends them.
     if (lane == 0) {
       uint32_t L = 0;
+      const uint64_t policy = policy_evict_first();
       int64_t t = a.sched ? (int64_t)atomicAdd(&a.sched[0], 1ull) : (int64_t)blockIdx.x;
       for (;;) {
         const int64_t e0 = t * kTile;
@@ -158,7 +174,10 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_bulk(const __grid_co
             bytes = cnt * 4;
           }
           mbar_expect_tx(&full[s], bytes);
-          bulk_g2s(smem + (size_t)s * kStageBytes, src, bytes, &full[s]);
+          if (a.l2_hint && j >= 0)
+            bulk_g2s_hint(smem + (size_t)s * kStageBytes, src, bytes, &full[s], policy);
+          else
+            bulk_g2s(smem + (size_t)s * kStageBytes, src, bytes, &full[s]);
         }
         if (t >= n_tiles) break;
         t = t_next;

@@ -33,6 +33,7 @@ struct CommitArgs {
   int32_t n_bcast;
   float *bcast[kMaxBcast];
   int32_t bcast_mc;     // 1: bcast[0] is an NVLS multicast address (multimem.st, the switch replicates)
+  int32_t l2_hint;      // 1: operand tiles are loaded with an L2 evict-first policy
   // dynamic tile scheduling (bulk kernel): [0] next tile, [1] CTAs done; zero between launches
   // (the last CTA resets both).  nullptr = static round-robin tiles.
   unsigned long long *sched;
