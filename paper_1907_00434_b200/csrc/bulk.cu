@@ -82,6 +82,11 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 
 // fused-get store of one float4: a plain streaming store to a peer view, or one multimem
 // store to an NVLS multicast address that NVSwitch replicates into every GPU's view
@@ -142,7 +147,10 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_bulk(const __grid_co
     // consumers; index -1 (no stage data) ends them.
     if (lane == 0) {
       uint32_t L = 0;
-      const uint64_t policy = policy_evict_first();
+      // operands are read once: evict-first when asked (a.l2_hint), else the normal policy;
+      // one instruction form either way (a branch here costs the producer)
+      const uint64_t pol_w = policy_evict_normal();
+      const uint64_t pol_op = a.l2_hint ? policy_evict_first() : pol_w;
       int64_t t = a.sched ? (int64_t)atomicAdd(&a.sched[0], 1ull) : (int64_t)blockIdx.x;
       for (;;) {
         const int64_t e0 = t * kTile;
@@ -174,10 +182,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_bulk(const __grid_co
             bytes = cnt * 4;
           }
           mbar_expect_tx(&full[s], bytes);
-          if (a.l2_hint && j >= 0)
-            bulk_g2s_hint(smem + (size_t)s * kStageBytes, src, bytes, &full[s], policy);
-          else
-            bulk_g2s(smem + (size_t)s * kStageBytes, src, bytes, &full[s]);
+          bulk_g2s_hint(smem + (size_t)s * kStageBytes, src, bytes, &full[s], j < 0 ? pol_w : pol_op);
         }
         if (t >= n_tiles) break;
         t = t_next;
