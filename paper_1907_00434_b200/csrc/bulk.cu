@@ -117,8 +117,9 @@ __device__ __forceinline__ float4 widen_bf16x4(uint2 u) {
                      __uint_as_float(u.y & 0xffff0000u));
 }
 
-// kTile elements per tile (one fp32 tile per stage; bf16 tiles use half), kStages-deep ring
-template <int kTile, int kStages>
+// kTile elements per tile (one fp32 tile per stage; bf16 tiles use half), kStages-deep ring;
+// kHint: operand copies carry an L2 evict-first policy (a.l2_hint), else the plain copy form
+template <int kTile, int kStages, bool kHint>
 __global__ void __launch_bounds__(kThreads, 1) fused_commit_bulk(const __grid_constant__ CommitArgs a) {
   constexpr int kStageBytes = kTile * 4;
   constexpr int kChunks = kTile / 4 / kConsumers;   // float4 chunks per consumer thread per tile
@@ -147,10 +148,11 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_bulk(const __grid_co
     // consumers; index -1 (no stage data) ends them.
     if (lane == 0) {
       uint32_t L = 0;
-      // operands are read once: evict-first when asked (a.l2_hint), else the normal policy;
-      // one instruction form either way (a branch here costs the producer)
-      const uint64_t pol_w = policy_evict_normal();
-      const uint64_t pol_op = a.l2_hint ? policy_evict_first() : pol_w;
+      // operands are read once: evict-first under kHint.  One instruction form per
+      // instantiation: a per-copy branch costs the producer, and the hinted form
+      // even with the normal policy costs ~4% on peer (NVLink) reads
+      const uint64_t pol_w = kHint ? policy_evict_normal() : 0;
+      const uint64_t pol_op = kHint ? policy_evict_first() : 0;
       int64_t t = a.sched ? (int64_t)atomicAdd(&a.sched[0], 1ull) : (int64_t)blockIdx.x;
       for (;;) {
         const int64_t e0 = t * kTile;
@@ -182,7 +184,10 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_bulk(const __grid_co
             bytes = cnt * 4;
           }
           mbar_expect_tx(&full[s], bytes);
-          bulk_g2s_hint(smem + (size_t)s * kStageBytes, src, bytes, &full[s], j < 0 ? pol_w : pol_op);
+          if constexpr (kHint)
+            bulk_g2s_hint(smem + (size_t)s * kStageBytes, src, bytes, &full[s], j < 0 ? pol_w : pol_op);
+          else
+            bulk_g2s(smem + (size_t)s * kStageBytes, src, bytes, &full[s]);
         }
         if (t >= n_tiles) break;
         t = t_next;
@@ -992,12 +997,12 @@ cudaError_t launch_commit_momentum(const MomentumArgs &a, cudaStream_t s, int sm
   return cudaGetLastError();
 }
 
-template <int kTile, int kStages>
-static cudaError_t launch_tile(const CommitArgs &a, cudaStream_t s, int sm_count) {
+template <int kTile, int kStages, bool kHint>
+static cudaError_t launch_tile_h(const CommitArgs &a, cudaStream_t s, int sm_count) {
   constexpr size_t smem = bulk::smem_bytes(kTile, kStages);
   static bool init = false;
   if (!init) {
-    cudaError_t e = cudaFuncSetAttribute(bulk::fused_commit_bulk<kTile, kStages>,
+    cudaError_t e = cudaFuncSetAttribute(bulk::fused_commit_bulk<kTile, kStages, kHint>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     init = true;
@@ -1012,11 +1017,16 @@ static cudaError_t launch_tile(const CommitArgs &a, cudaStream_t s, int sm_count
   if (a.sched && tile_bytes < (64 << 10)) {
     CommitArgs b = a;
     b.sched = nullptr;
-    bulk::fused_commit_bulk<kTile, kStages><<<grid, bulk::kThreads, smem, s>>>(b);
+    bulk::fused_commit_bulk<kTile, kStages, kHint><<<grid, bulk::kThreads, smem, s>>>(b);
   } else {
-    bulk::fused_commit_bulk<kTile, kStages><<<grid, bulk::kThreads, smem, s>>>(a);
+    bulk::fused_commit_bulk<kTile, kStages, kHint><<<grid, bulk::kThreads, smem, s>>>(a);
   }
   return cudaGetLastError();
+}
+template <int kTile, int kStages>
+static cudaError_t launch_tile(const CommitArgs &a, cudaStream_t s, int sm_count) {
+  return a.l2_hint ? launch_tile_h<kTile, kStages, true>(a, s, sm_count)
+                   : launch_tile_h<kTile, kStages, false>(a, s, sm_count);
 }
 
 // Tile size (elements) per bulk copy: MLF_BULK_TILE in {1024, 2048, 4096, 8192}; the ring is
