@@ -554,6 +554,10 @@ def run_bench_multi(a):
     from bench import METRIC, Clocks, cpu_baseline_oracle, hbm_peak  # noqa: F401  (same process)
 
     rank, world, local, ctrl = init_dist()
+    # one GPU per rank; more ranks than GPUs (a rehearsal of a larger N on a smaller box)
+    # share devices round-robin and say so in the line
+    shared = world > torch.cuda.device_count()
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     cid = a.config or 3
@@ -654,7 +658,9 @@ def run_bench_multi(a):
                    "parallelism": f"ps-shards{world} (one process per GPU, " + {
                        "fold": "NVLink peer loads in the commit kernel)",
                        "staged": "copy-engine NVLink pulls into local staging + commit kernel)",
-                       "tree": "tree_reduce on the aggregator GPU + peer loads)"}[modes[0]]},
+                       "tree": "tree_reduce on the aggregator GPU + peer loads)"}[modes[0]],
+                   **({"shared_gpus": f"{world} ranks on {torch.cuda.device_count()} GPUs: not a valid bench number"}
+                      if shared else {})},
         "roofline": {"bound": "nvlink" if nv_bound else "hbm",
                      "achieved": round((nv_bytes if nv_bound else hbm_bytes) / T / 1e9, 1),
                      "peak": round(b_nv if nv_bound else peak_hbm, 1), "unit": "GB/s",
