@@ -70,10 +70,14 @@ def test_momentum_random_plans(gamma, dtype):
         assert np.max(np.abs(w - w64)) <= 1e-6 * max(np.max(np.abs(w64)), 1e-30)
 
 
-def test_momentum_config2_full_size():
-    cfg = configs.config(2, tau=32, gamma=0.9)
+@pytest.mark.parametrize("dtype,tau", [("f32", 32), ("bf16", 32), ("bf16", 4)])
+def test_momentum_config2_full_size(dtype, tau):
+    # fp32 takes the generic fold, all-bf16 operand lists the branch-free one (both kernels:
+    # dynamic tiles at tau 4, round-robin at tau 32)
+    cfg = configs.config(2, tau=tau, gamma=0.9, dtype=dtype)
     wl = Workload(cfg, device=0)
     S = cfg["S"]
+    sdt = sg.DTYPE_BF16 if dtype == "bf16" else sg.DTYPE_F32
     rng = np.random.default_rng(9)
     idx = np.unique(np.concatenate([rng.integers(0, S, 20_000), np.arange(S - 9, S)]))
     w_ref = sg.w0_values(cfg["seed"], idx)
@@ -81,7 +85,7 @@ def test_momentum_config2_full_size():
     for it in range(3):
         pb, pd, draws = wl.step(it)
         wl.ctx.sync()
-        commits = commits_from_plan(pd, lambda g: sg.update_values(cfg["seed"], g, it, idx))
+        commits = commits_from_plan(pd, lambda g: sg.update_values(cfg["seed"], g, it, idx, sdt))
         w_ref, h_ref, _ = weighted_f32(w_ref, h_ref, commits, cfg["lr"], 0.9)
         assert np.array_equal(bits(wl.w.cpu().numpy()[idx]), bits(w_ref))
         assert np.array_equal(bits(wl.h.cpu().numpy()[idx]), bits(h_ref))
