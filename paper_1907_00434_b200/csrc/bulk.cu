@@ -1007,13 +1007,9 @@ __global__ void __launch_bounds__(kThreads, 1) tree_reduce_bulk(const __grid_con
 cudaError_t launch_reduce_bulk(const ReduceArgs &a, cudaStream_t s, int sm_count) {
   constexpr int kTile = 4096, kStages = 12;
   constexpr size_t smem = bulk::smem_bytes(kTile, kStages);
-  static bool init = false;
-  if (!init) {
-    cudaError_t e = cudaFuncSetAttribute(bulk::tree_reduce_bulk<kTile, kStages>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    init = true;
-  }
+  static std::atomic<uint64_t> init{0};
+  if (cudaError_t e = ensure_smem(bulk::tree_reduce_bulk<kTile, kStages>, smem, init); e != cudaSuccess)
+    return e;
   if (a.n_ops < 1 || a.n < 1) return cudaSuccess;
   const int64_t n_tiles = ((a.n & ~int64_t(7)) + kTile - 1) / kTile;
   int grid = (int)(n_tiles < sm_count ? (n_tiles > 0 ? n_tiles : 1) : sm_count);
@@ -1033,13 +1029,9 @@ template <bool kBf>
 static cudaError_t launch_momentum_t(const MomentumArgs &a, cudaStream_t s, int sm_count) {
   constexpr int kTile = 4096, kStages = 12;
   constexpr size_t smem = bulk::smem_bytes(kTile, kStages);
-  static bool init = false;
-  if (!init) {
-    cudaError_t e = cudaFuncSetAttribute(bulk::fused_commit_momentum<kTile, kStages, kBf>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    init = true;
-  }
+  static std::atomic<uint64_t> init{0};
+  if (cudaError_t e = ensure_smem(bulk::fused_commit_momentum<kTile, kStages, kBf>, smem, init); e != cudaSuccess)
+    return e;
   const int64_t n_tiles = ((a.n & ~int64_t(7)) + kTile - 1) / kTile;
   int grid = (int)(n_tiles < sm_count ? (n_tiles > 0 ? n_tiles : 1) : sm_count);
   // dynamic tiles for short fp32 lists; bf16 lists measured faster round-robin at every
@@ -1047,13 +1039,9 @@ static cudaError_t launch_momentum_t(const MomentumArgs &a, cudaStream_t s, int 
   if (!kBf && a.sched && a.n_ops <= 8) {
     bulk::fused_commit_momentum<kTile, kStages, kBf><<<grid, bulk::kThreads, smem, s>>>(a);
   } else {
-    static bool init_rr = false;
-    if (!init_rr) {
-      cudaError_t e = cudaFuncSetAttribute(bulk::fused_commit_momentum_rr<kTile, kStages, kBf>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      init_rr = true;
-    }
+    static std::atomic<uint64_t> init_rr{0};
+    if (cudaError_t e = ensure_smem(bulk::fused_commit_momentum_rr<kTile, kStages, kBf>, smem, init_rr); e != cudaSuccess)
+      return e;
     bulk::fused_commit_momentum_rr<kTile, kStages, kBf><<<grid, bulk::kThreads, smem, s>>>(a);
   }
   return cudaGetLastError();
@@ -1070,13 +1058,9 @@ cudaError_t launch_commit_momentum(const MomentumArgs &a, cudaStream_t s, int sm
 template <int kTile, int kStages, bool kHint>
 static cudaError_t launch_tile_h(const CommitArgs &a, cudaStream_t s, int sm_count) {
   constexpr size_t smem = bulk::smem_bytes(kTile, kStages);
-  static bool init = false;
-  if (!init) {
-    cudaError_t e = cudaFuncSetAttribute(bulk::fused_commit_bulk<kTile, kStages, kHint>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    init = true;
-  }
+  static std::atomic<uint64_t> init{0};
+  if (cudaError_t e = ensure_smem(bulk::fused_commit_bulk<kTile, kStages, kHint>, smem, init); e != cudaSuccess)
+    return e;
   const int64_t n_tiles = ((a.n & ~int64_t(7)) + kTile - 1) / kTile;
   int grid = (int)(n_tiles < sm_count ? (n_tiles > 0 ? n_tiles : 1) : sm_count);
   // Dynamic tiles pay one global atomic per tile; below ~64 KB of loads per tile its latency
@@ -1128,13 +1112,9 @@ cudaError_t launch_commit_bulk(const CommitArgs &a, cudaStream_t s, int sm_count
     if (all_bf16 && !(hb && atoi(hb) == 0) && (a.n / 8192) / sms >= 16) {
       constexpr int kT = 8192, kS = 12;
       constexpr size_t smem = (size_t)kS * kT * 2 + 3 * kS * sizeof(uint64_t);
-      static bool init = false;
-      if (!init) {
-        cudaError_t e = cudaFuncSetAttribute(bulk::fused_commit_bulk_h<kT, kS>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        init = true;
-      }
+      static std::atomic<uint64_t> init{0};
+      if (cudaError_t e = ensure_smem(bulk::fused_commit_bulk_h<kT, kS>, smem, init); e != cudaSuccess)
+        return e;
       const int64_t n_tiles = ((a.n & ~int64_t(7)) + kT - 1) / kT;
       const int grid = (int)(n_tiles < sms ? (n_tiles > 0 ? n_tiles : 1) : sms);
       bulk::fused_commit_bulk_h<kT, kS><<<grid, bulk::kThreads, smem, s>>>(a);

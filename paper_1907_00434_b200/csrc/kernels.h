@@ -1,5 +1,6 @@
 // kernels.h — launch interface between the executor (host C++) and the sm_100a kernels.
 #pragma once
+#include <atomic>
 #include <cstdint>
 
 #include <cuda_runtime_api.h>
@@ -17,6 +18,20 @@ constexpr uint8_t kOpLast = 2;    // last member of its commit: w <- w - lr*x af
 constexpr uint8_t kOpBf16 = 4;    // operand is bf16 (widened exactly), else fp32
 
 // The fused reduce + scale + apply (+ mirror store) pass over one shard slice.
+// Dynamic shared memory above 48 KB must be opted into per kernel and per device.  One bit
+// per device records that it was; setting it twice (two threads racing) is harmless.
+template <typename K>
+inline cudaError_t ensure_smem(K kernel, size_t smem, std::atomic<uint64_t> &done) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
+
 struct CommitArgs {
   float *w;             // [n] shard slice, read once, written once
   float *backup;        // [n] mirror target (local or peer), or nullptr

@@ -170,12 +170,9 @@ cudaError_t launch_bulk_segs(const BulkSegs &a, cudaStream_t s, int sm_count) {
   using namespace bulkcopy;
   if (a.n <= 0 || a.cstart[a.n] <= 0) return cudaSuccess;
   const size_t smem = (size_t)kStages * kChunk + kStages * sizeof(uint64_t);
-  static bool init = false;
-  if (!init) {
-    cudaError_t e = cudaFuncSetAttribute(bulk_copy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    init = true;
-  }
+  static std::atomic<uint64_t> init{0};
+  if (cudaError_t e = ensure_smem(bulk_copy_kernel, smem, init); e != cudaSuccess)
+    return e;
   bulk_copy_kernel<<<sm_count, 32, smem, s>>>(a);
   return cudaGetLastError();
 }

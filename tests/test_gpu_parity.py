@@ -32,24 +32,29 @@ def bits(a):
 
 
 def gpu_run(S, W, dtype, plan_d, *, lr=0.01, variant=0, iteration=0, backup=False, host_updates=False,
-            impl="ldg"):
-    """Fill W slots + w0 on cuda:0 with the generator, submit every worker, execute plan_d."""
+            impl="ldg", device=0):
+    """Fill W slots + w0 on cuda:<device> with the generator, submit every worker, execute plan_d."""
+    with torch.cuda.device(device):
+        return _gpu_run(S, W, dtype, plan_d, lr, variant, iteration, backup, host_updates, impl, device)
+
+
+def _gpu_run(S, W, dtype, plan_d, lr, variant, iteration, backup, host_updates, impl, device):
     os.environ["MLF_COMMIT_IMPL"] = impl                     # read at mlf_init
-    dev = torch.device("cuda", 0)
+    dev = torch.device("cuda", device)
     tdt = torch.bfloat16 if dtype == sg.DTYPE_BF16 else torch.float32
     slots = [torch.empty(S, dtype=tdt, device=dev) for _ in range(W)]
     for w, t in enumerate(slots):
-        m.synth_fill(0, t.data_ptr(), S, dtype=dtype, seed=SEED, kind=1, a=w, b=iteration, variant=variant)
+        m.synth_fill(device, t.data_ptr(), S, dtype=dtype, seed=SEED, kind=1, a=w, b=iteration, variant=variant)
     wt = torch.empty(S, dtype=torch.float32, device=dev)
-    m.synth_fill(0, wt.data_ptr(), S, dtype=m.MLF_F32, seed=SEED, kind=2, variant=variant)
+    m.synth_fill(device, wt.data_ptr(), S, dtype=m.MLF_F32, seed=SEED, kind=2, variant=variant)
     bk = torch.full((S,), float("nan"), dtype=torch.float32, device=dev) if backup else None
     hosts = []
     if host_updates:
         for t in slots:
             hosts.append(t.cpu().pin_memory())
             t.zero_()
-    ctx = m.Context(device=0, model_shard=wt, update_slots=slots, lr=lr, model_elems=S, dtype=dtype,
-                    backup_shard=bk, stream=torch.cuda.current_stream().cuda_stream)
+    ctx = m.Context(device=device, model_shard=wt, update_slots=slots, lr=lr, model_elems=S, dtype=dtype,
+                    backup_shard=bk, stream=torch.cuda.current_stream(dev).cuda_stream)
     for w in range(W):
         ctx.submit(w, 0, 0, 1.0)
         if host_updates:
@@ -307,6 +312,19 @@ def test_bulk_commit_under_concurrent_copy_engine_traffic(tile):
     idx = np.unique(np.concatenate([rng.integers(0, S, 200_000), np.arange(S - 9, S)]))
     wr, _ = oracle_run(S, sg.DTYPE_F32, p, idx=idx)
     assert np.array_equal(bits(wt.cpu().numpy()[idx]), bits(wr))
+
+
+def test_contexts_on_two_devices_in_one_process():
+    # the large-shared-memory opt-in is per device: a second device's first launch must set it
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    rng = np.random.default_rng(23)
+    S, W = 300_007, 9
+    p = random_plan(rng, W, n_commit=W, boundary=1)
+    ref, bref = oracle_run(S, sg.DTYPE_F32, p)
+    for device in (0, 1, 0):
+        w, b, _, _ = gpu_run(S, W, sg.DTYPE_F32, p, impl="bulk", backup=True, device=device)
+        assert np.array_equal(bits(w), bits(ref)) and np.array_equal(bits(b), bits(bref)), device
 
 
 @pytest.mark.parametrize("impl", IMPLS)
