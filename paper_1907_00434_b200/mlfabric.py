@@ -333,6 +333,12 @@ class Context:
             if x is None:
                 return None
             return x if isinstance(x, int) else x.data_ptr()
+        self._h = _p()
+        # the library borrows every buffer for the context's lifetime (include/mlfabric.h,
+        # ownership): hold the tensors passed in, so none is freed while the context uses it
+        self._refs = [x for x in (model_shard, backup_shard, history, backup_history, stage, *update_slots,
+                                  *(agg_scratch or []), *(retain_slots or []), *(bcast or []))
+                      if x is not None and not isinstance(x, int)]
         self.n_workers = len(update_slots)
         self._slots = (_p * max(self.n_workers, 1))(*[ptr(s) for s in update_slots])
         self._wr = _arr(worker_rank if worker_rank is not None else [0] * self.n_workers, np.int32)
@@ -361,16 +367,24 @@ class Context:
         if stage is not None:                       # copy-engine staging buffer (torch tensor)
             self.cfg.stage_buf = ptr(stage)
             self.cfg.stage_bytes = stage.numel() * stage.element_size()
-        self._h = _p()
         _check(_lib.mlf_init(C.byref(self.cfg), int(v0), C.byref(self._h)))
         self._bufs = None
 
     def close(self):
-        if self._h:
-            _lib.mlf_destroy(self._h)
+        h = getattr(self, "_h", None)
+        if h:
+            _lib.mlf_destroy(h)
             self._h = _p()
+        self._refs = []
 
     __del__ = close
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+        return False
 
     def submit(self, worker: int, version: int, t_avail_ns: int = 0, norm: float = 0.0) -> int:
         idx = C.c_int32()

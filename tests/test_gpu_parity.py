@@ -515,3 +515,26 @@ def test_config2_full_size_sampled(tau, dtype, impl):
         got = wl.w.cpu().numpy()[idx]
         assert np.array_equal(bits(got), bits(w_ref))
         assert pd["n_commit"] == min(tau, 32)
+
+
+def test_context_holds_its_buffers():
+    # the library borrows the buffers for the context's lifetime: the binding keeps them alive
+    import gc
+    import weakref
+    w = torch.zeros(4099, device="cuda")
+    slots = [torch.ones(4099, device="cuda") for _ in range(2)]
+    refs = [weakref.ref(t) for t in (w, *slots)]
+    with m.Context(device=0, model_shard=w, update_slots=slots, lr=0.5, model_elems=4099) as ctx:
+        del w, slots
+        gc.collect()
+        assert all(r() is not None for r in refs)
+        for g in range(2):
+            ctx.submit(g, 0, 0, 1.0)
+        p = {"n_commit": 2, "n_server_commits": 2, "order": [0, 1], "drop_reason": [0, 0], "group": [0, 0],
+             "n_direct": 2, "n_groups": 0,
+             "group_node": [], "commit_first": [0, 1], "commit_count": [1, 1], "replica_boundary_commit": -1}
+        ctx.execute(m.plan_from_dict(p))
+        ctx.sync()
+        assert torch.equal(refs[0](), torch.full((4099,), -1.0, device="cuda"))
+    gc.collect()
+    assert all(r() is None for r in refs)
