@@ -623,11 +623,19 @@ def run_bench_multi(a):
     ar = None
     if not a.no_variants:
         # NEXT-3: AllReduce via push/get vs NCCL all_reduce, ResNet-50-sized buffer per GPU
+        # optional side measurements: a failure here (raised on every rank alike) is reported in
+        # the line instead of costing the primary number
         from .allreduce import bench_allreduce
-        ar = bench_allreduce(25_600_000, rank, world, local, ctrl, steps=5, warmup=2, flush=l2_flush)
+        try:
+            ar = bench_allreduce(25_600_000, rank, world, local, ctrl, steps=5, warmup=2, flush=l2_flush)
+        except Exception as e:                    # noqa: BLE001
+            ar = {"error": f"{type(e).__name__}: {str(e)[:200]}"}
     dv = None
     if not a.no_variants:
-        dv = bench_distribution(cfg0["S"], rank, world, local, ctrl, b_nv, steps=5, flush=l2_flush)
+        try:
+            dv = bench_distribution(cfg0["S"], rank, world, local, ctrl, b_nv, steps=5, flush=l2_flush)
+        except Exception as e:                    # noqa: BLE001
+            dv = {"error": f"{type(e).__name__}: {str(e)[:200]}"}
     e2e = None
     if not a.no_e2e:
         e2e = e2e_multi(cfgs.config(cid, G=world, tau=a.tau, dtype=a.dtype), rank, world, local, ctrl,
