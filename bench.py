@@ -22,25 +22,13 @@ from __future__ import annotations
 import argparse
 import json
 import os
-import subprocess
 import sys
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
-# BASELINE.json's metric, verbatim (the roofline fraction is the line's `roofline` object)
-METRIC = "aggregated update GB/s committed (device-timed, max over ranks), % HBM/NVLink roofline"
-HBM_FALLBACK = 6650.0
-
-
-def hbm_peak():
-    try:
-        d = json.load(open(PEAKS))
-        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
-    except Exception:
-        return HBM_FALLBACK, "fallback (B200_PROFILING.md)"
+from benchkit.common import METRIC, Clocks, hbm_peak  # noqa: E402
 
 
 def parse():
@@ -61,57 +49,6 @@ def parse():
     ap.add_argument("--kernel", default=os.environ.get("MLF_COMMIT_IMPL"), choices=["ldg", "bulk"],
                     help="fused commit kernel (default bulk: TMA bulk copies; ldg: 128-bit load streaming)")
     return ap.parse_args()
-
-
-class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
-
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-
-    def __init__(self, index: int):
-        self.index = index
-        self.p = None
-
-    def __enter__(self):
-        try:
-            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
-                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except Exception:
-            self.p = None
-        return self
-
-    def __exit__(self, *a):
-        self.lines = []
-        if self.p is not None:
-            time.sleep(0.25)
-            self.p.terminate()
-            try:
-                out, _ = self.p.communicate(timeout=5)
-            except Exception:
-                out = ""
-            self.lines = [l for l in out.splitlines() if l.strip()]
-
-    def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for l in getattr(self, "lines", []):
-            f = [x.strip() for x in l.split(",")]
-            if len(f) < 9:
-                continue
-            try:
-                sm.append(float(f[1]))
-                mx = float(f[2])
-            except ValueError:
-                continue
-            for nm, v in zip(names, f[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        sm.sort()
-        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
 
 
 def dist_env():
@@ -190,16 +127,20 @@ def cpu_baseline_oracle(cfg, dt, budget_s=15.0):
     w = sg.w0_values(cfg["seed"], idx)
     v_init = v_prev = 0
     tot_b, tot_s, it = 0, 0.0, 0
+    # sharded configs: the Python planner is O(#U^2 * G), so each batch plans a 16-update sample
+    W_s = cfg["W"] if cfg["G"] == 1 else min(cfg["W"], 16)
+    weights = [n for (_, n) in cfg["shards"]] if cfg["G"] > 1 else None
     t_start = time.perf_counter()
     while time.perf_counter() - t_start < budget_s and it < 50:
         up, down, site = configs.network(cfg, it)
-        draws = configs.batch_draws(cfg, it, v_init, v_prev)
-        ops = {g: sg.update_values(cfg["seed"], g, it, idx, dt) for g in range(cfg["W"])}
+        draws = configs.batch_draws(cfg, it, v_init, v_prev)[:W_s]
+        ops = {g: sg.update_values(cfg["seed"], g, it, idx, dt) for g in range(W_s)}
         t0 = time.perf_counter()
         batch = [Item(cfg["worker_node"][g], cfg["S"] * cfg["e"], d["version"], d["t_avail"], d["norm"])
                  for g, d in enumerate(draws)]
         p = oracle_plan(make_net(cfg["n_nodes"], up, down, None, site), batch,
-                        Params(servers=cfg["servers"], aggs=cfg["aggs"], v_init=v_init, tau_max=cfg["tau"]))
+                        Params(servers=cfg["servers"], aggs=cfg["aggs"], v_init=v_init, tau_max=cfg["tau"],
+                               shard_weights=weights))
         w, _, _ = execute_plan(w, p, lambda g: ops[g], cfg["lr"])
         tot_s += time.perf_counter() - t0
         tot_b += p["n_commit"] * S_sample * cfg["e"]
@@ -207,8 +148,8 @@ def cpu_baseline_oracle(cfg, dt, budget_s=15.0):
         it += 1
     out = {"value": round(tot_b / tot_s / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
            "cpu": cpu_model(), "host_cores": os.cpu_count(),
-           "sample": f"{it} batches of config{cfg['cid']}: full oracle plan + numpy numerics on the first "
-                     f"{S_sample} of {cfg['S']} elements of every update (single-threaded numpy)"}
+           "sample": f"{it} batches of config{cfg['cid']}: oracle plan of {W_s} of {cfg['W']} updates + numpy "
+                     f"numerics on the first {S_sample} of {cfg['S']} elements of every update (single-threaded numpy)"}
     try:
         out["all_cores"] = cpu_oracle_all_cores(cfg, dt, p)
     except Exception as e:  # the single-core figure above is the reported baseline
@@ -508,8 +449,18 @@ def main():
     if a.kernel is None:
         a.kernel = "bulk"
     if multi:
-        from paper_1907_00434_b200.multigpu import run_bench_multi
-        run_bench_multi(a)
+        from benchkit.multi import run_bench_multi
+        line = run_bench_multi(a)
+        if line is None:                      # ranks > 0: rank 0 prints the line
+            return
+        if not a.no_cpu_baseline:
+            # the oracle on rank 0 after every rank's GPU work (same sharded config, bounded sample)
+            import synthgen as sg
+            from synthgen import configs
+            cid = a.config or 3
+            line["cpu_baseline"] = cpu_baseline_oracle(configs.config(cid, G=world, tau=a.tau, dtype=a.dtype),
+                                                       sg.DTYPE_BF16 if a.dtype == "bf16" else sg.DTYPE_F32)
+        print(json.dumps(line), flush=True)
         return
     run_single(a)
 

@@ -241,8 +241,10 @@ typedef struct {
    * aggregation"): w += (sum_{j=1..m} g^j) h + sum_i (sum_{j=0..m-i} g^j) u_i,
    * h = g^m h + sum_i g^(m-i) u_i, two weighted sums in one pass (the aggregators'
    * "weighted sum").  backup_history receives h at the mirror boundary.
-   * Requires fold mode (agg_slots = 0) and the bulk kernel. */
-  float gamma;
+   * Requires fold mode (agg_slots = 0) and the bulk kernel.  gamma is a double, the same
+   * type as mlf_plan_params.gamma (one momentum parameter across the ABI): the weights are
+   * computed from it in float64 and each rounded once to fp32 for the kernel (reading R21). */
+  double gamma;
   float *history_shard;
   float *backup_history;
   /* Replica trees (NEXT-2; plans with replica_mode = 1): backup_shard is the
@@ -273,6 +275,16 @@ typedef struct {
    * PyTorch symmetric memory's multicast_ptr): the fused get stores each final tile once
    * with multimem.st and NVSwitch replicates it, instead of one store per peer view. */
   int32_t bcast_multicast;
+  /* registerAsServer(params tau_max, ...) (Table 1): the delay bound this server
+   * enforces.  enforce_tau = 1: mlf_execute / mlf_execute_phase reject, with MLF_E_INVALID and
+   * before any device work, an asynchronous plan (sync_mode = 0) that commits an update g at
+   * 1-based position p of O(U) with (v + p) - v(g) > tau_max, v = the context's version
+   * (mlf_version) — "no update is applied with a delay greater than tau_max" (P:933-945,
+   * reading R1).  A plan built by mlf_plan with the same tau_max and v_init = v never fails the
+   * check; a hand-built or stale plan can.  enforce_tau = 0 (a zero-initialised config): not
+   * checked.  Synchronous plans have no delay bound. */
+  int32_t enforce_tau;
+  int32_t tau_max;
 } mlf_config;
 
 typedef struct mlf_ctx mlf_ctx;

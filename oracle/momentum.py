@@ -14,13 +14,14 @@ Paper passages:
 
 Two oracles:
 * sequential_f64 — the plain definition: Eq. 2 per update, in float64.
-* weighted_f32 — the aggregate form in fp32 with a pinned evaluation order (what the
-  commit kernel computes): gamma taken as its fp32 value (reading R21: the model, its
-  history and the momentum parameter are fp32); coefficients from float64 powers
-  pw[j] = pw[j-1]*g summed left to right, rounded once to fp32; per member
-  u_i = -(lr*g_i); A = left fold of
-  (cA_i*u_i), B = left fold of (cB_i*u_i); t = s_h*h + A; w' = w + t;
-  h' = g_m*h + B; every product / sum rounded to fp32, never fused.
+* weighted_f32 — the same two weighted sums evaluated in fp32 in a pinned order (reading
+  R21: the model and its history are fp32, the paper fixes no precision): gamma is the
+  float64 value of the ABI (the same double the planner's Eq. 9/12 bound uses); the
+  coefficients are float64 powers pw[j] = pw[j-1]*gamma summed left to right, each rounded
+  once to fp32; per member u_i = -(lr*g_i); A = left fold of (cA_i*u_i), B = left fold of
+  (cB_i*u_i); t = s_h*h + A; w' = w + t; h' = g_m*h + B; every product / sum rounded to
+  fp32, never fused.  The order is a reading, so weighted_f32 is checked against
+  sequential_f64 (the definition) with the tolerance DESIGN.md R21 derives.
 
 Parity: weighted_f32 equals the exact rational value of the sequential definition in
 an exact-arithmetic case (gamma = 1/2, dyadic inputs), and is within 1e-6
@@ -69,7 +70,7 @@ def sequential_f64(w, h, commits: list, lr: float, gamma: float, boundary: int =
 def weighted_f32(w, h, commits: list, lr: float, gamma: float, boundary: int = -1):
     """The aggregate (weighted-sum) form in fp32, pinned order.  Returns (w, h, backup)."""
     f = np.float32
-    gamma = float(np.float32(gamma))      # R21: gamma is an fp32 parameter (the model's dtype)
+    gamma = float(gamma)                  # R21: one float64 gamma; each weight rounded once to fp32
     w = np.asarray(w, dtype=np.float32).copy()
     h = np.asarray(h, dtype=np.float32).copy()
     lr32 = f(lr)

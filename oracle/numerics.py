@@ -27,13 +27,13 @@ from __future__ import annotations
 
 import numpy as np
 
-from synthgen import bf16_bits_to_f32
-
 
 def widen(a: np.ndarray) -> np.ndarray:
-    """fp32 operand as-is; bf16 bit patterns (uint16) widened exactly."""
+    """fp32 operand as-is; bf16 bit patterns (uint16) widened exactly (R17, SURVEY §8(c)
+    O6): a bf16 value is the upper half of the fp32 with the same sign, exponent and leading
+    7 mantissa bits, so the fp32 bit pattern is u32 = u16 << 16 (low half zero)."""
     if a.dtype == np.uint16:
-        return bf16_bits_to_f32(a)
+        return (a.astype(np.uint32) << np.uint32(16)).view(np.float32)
     assert a.dtype == np.float32
     return a
 

@@ -78,64 +78,3 @@ class MlfAllReduce:
     def close(self):
         self.sw.close()
         self.mapper.close()
-
-
-def bench_allreduce(S: int, rank: int, world: int, device: int, ctrl, steps: int = 5, warmup: int = 2,
-                    flush=None) -> dict:
-    """MLfabric AllReduce vs NCCL all_reduce on the same per-GPU buffer of S fp32 values."""
-    cfg = allreduce_config(S, world)
-    res = {}
-    variants = [(True, False), (False, False)]
-    if dist.get_backend() == "nccl":
-        variants.append((True, True))             # NVLS multicast get (one GPU per rank)
-    for fused, mc in variants:
-        try:
-            ar = MlfAllReduce(cfg, rank, world, device, ctrl, fused=fused, multicast=mc)
-        except Exception:                         # no multicast on this box (fails on every rank alike)
-            if not mc:
-                raise
-            continue
-        ar.sw.fill(0)
-        push = get = wall = 0.0
-        for s in range(warmup + steps):
-            _, mp, mg, mw = ar.run(s, flush=flush)
-            if s >= warmup:
-                push, get, wall = push + mp, get + mg, wall + mw
-        ar.close()
-        res[(fused, mc)] = (push / steps, get / steps, wall / steps)
-    # NCCL on the default (NCCL) process group, same bytes per GPU
-    t = torch.ones(S, dtype=torch.float32, device=torch.device("cuda", device))
-    nccl_ms = None
-    if dist.get_backend() == "nccl":
-        for _ in range(warmup):
-            dist.all_reduce(t)
-        torch.cuda.synchronize()
-        acc = 0.0
-        for _ in range(steps):
-            if flush is not None:
-                flush()
-            dist.barrier()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            dist.all_reduce(t)
-            e1.record()
-            e1.synchronize()
-            acc += max_over_ranks(e0.elapsed_time(e1), ctrl)
-        nccl_ms = acc / steps
-    nbytes = S * 4
-
-    def busbw(ms):
-        return round(2 * (world - 1) / world * nbytes / (ms / 1e3) / 1e9, 1) if ms else None
-
-    fp, _, fw = res[(True, False)]
-    gp, gg, gw = res[(False, False)]
-    mcp = res[(True, True)][0] if (True, True) in res else None
-    return {"bytes_per_gpu": nbytes,
-            "mlfabric_fused_ms": round(fp, 4), "mlfabric_fused_busbw_GBps": busbw(fp),
-            "mlfabric_fused_wall_ms": round(fw, 3),
-            "mlfabric_fused_multicast_ms": round(mcp, 4) if mcp else None,
-            "mlfabric_fused_multicast_busbw_GBps": busbw(mcp) if mcp else None,
-            "mlfabric_push_then_gather_ms": round(gp + gg, 4), "push_ms": round(gp, 4), "gather_ms": round(gg, 4),
-            "mlfabric_push_then_gather_busbw_GBps": busbw(gp + gg),
-            "nccl_ms": round(nccl_ms, 4) if nccl_ms else None, "nccl_busbw_GBps": busbw(nccl_ms),
-            "timing": "device time (CUDA events), max over ranks; busbw = 2(N-1)/N * bytes / time"}

@@ -124,11 +124,12 @@ extern "C" mlf_status mlf_init(const mlf_config *cfg, int64_t v0, mlf_ctx **out)
     if (k.update_dtype != MLF_F32 && k.update_dtype != MLF_BF16) throw Fail{MLF_E_INVALID, "update dtype"};
     if (k.shard_elems > 0 && !k.model_shard) throw Fail{MLF_E_INVALID, "model shard"};
     if (k.agg_slots < 0 || (k.agg_slots > 0 && !k.agg_scratch)) throw Fail{MLF_E_INVALID, "aggregate scratch"};
-    if (!(k.gamma >= 0.f && k.gamma < 1.f)) throw Fail{MLF_E_INVALID, "gamma must be in [0, 1)"};
+    if (!(k.gamma >= 0.0 && k.gamma < 1.0)) throw Fail{MLF_E_INVALID, "gamma must be in [0, 1)"};
+    if (k.enforce_tau != 0 && (k.enforce_tau != 1 || k.tau_max < 0)) throw Fail{MLF_E_INVALID, "enforce_tau / tau_max"};
     if (k.replica_mode != 0 && k.replica_mode != 1) throw Fail{MLF_E_INVALID, "replica_mode"};
     if (k.n_bcast < 0 || k.n_bcast > kMaxBcast || (k.n_bcast > 0 && !k.bcast))
       throw Fail{MLF_E_INVALID, "fused get: 0..8 destinations"};
-    if (k.n_bcast > 0 && k.gamma != 0.f) throw Fail{MLF_E_INVALID, "fused get is implemented for gamma = 0"};
+    if (k.n_bcast > 0 && k.gamma != 0.0) throw Fail{MLF_E_INVALID, "fused get is implemented for gamma = 0"};
     if (k.bcast_multicast != 0 && (k.bcast_multicast != 1 || k.n_bcast != 1))
       throw Fail{MLF_E_INVALID, "bcast_multicast needs exactly one (multicast) destination"};
     for (int i = 0; i < k.n_bcast; ++i)
@@ -136,13 +137,13 @@ extern "C" mlf_status mlf_init(const mlf_config *cfg, int64_t v0, mlf_ctx **out)
         throw Fail{MLF_E_INVALID, "fused get destination null or misaligned"};
     if (k.replica_mode == 1) {
       if (k.shard_elems > 0 && !k.backup_shard) throw Fail{MLF_E_INVALID, "replica trees need the replica shard"};
-      if (k.gamma != 0.f) throw Fail{MLF_E_INVALID, "replica trees are implemented for gamma = 0"};
+      if (k.gamma != 0.0) throw Fail{MLF_E_INVALID, "replica trees are implemented for gamma = 0"};
       if (k.n_retain < 0 || (k.n_retain > 0 && !k.retain_slot)) throw Fail{MLF_E_INVALID, "retention pool"};
       for (int i = 0; i < k.world * k.n_retain; ++i)
         if (!k.retain_slot[i] || (reinterpret_cast<uintptr_t>(k.retain_slot[i]) & 15))
           throw Fail{MLF_E_INVALID, "retention slot null or not 16-byte aligned"};
     }
-    if (k.gamma != 0.f) {
+    if (k.gamma != 0.0) {
       if (k.shard_elems > 0 && !k.history_shard) throw Fail{MLF_E_INVALID, "momentum needs history_shard"};
       if (k.backup_shard && !k.backup_history) throw Fail{MLF_E_INVALID, "momentum mirror needs backup_history"};
       if (k.world > 1 && k.agg_slots > 0)
@@ -333,6 +334,9 @@ extern "C" mlf_status mlf_version(mlf_ctx *c, int64_t *v) {
 }
 
 // --------------------------------------------------------------- plan checks
+// Structure first (every index is range-checked before it is dereferenced), then the delay
+// bound the server registered (Table 1 tau_max): no device work is enqueued for a
+// plan that fails either.
 static void validate_plan(const mlf_ctx *c, const mlf_plan_out *p) {
   const int n = (int)c->b_worker.size();
   if (!p) throw Fail{MLF_E_INVALID, "null plan"};
@@ -345,21 +349,23 @@ static void validate_plan(const mlf_ctx *c, const mlf_plan_out *p) {
     if (g < 0 || g >= n || seen[g]) throw Fail{MLF_E_INVALID, "plan order is not a subset of the batch"};
     seen[g] = 1;
   }
+  if (p->n_server_commits < 0 || p->n_server_commits > p->n_commit)
+    throw Fail{MLF_E_INVALID, "n_server_commits out of range"};
+  if (p->n_groups < 0) throw Fail{MLF_E_INVALID, "n_groups < 0"};
   int pos = 0;
-  if (p->n_server_commits < 0) throw Fail{MLF_E_INVALID, "n_server_commits"};
   for (int ci = 0; ci < p->n_server_commits; ++ci) {
-    if (p->commit_first[ci] != pos || p->commit_count[ci] < 1) throw Fail{MLF_E_INVALID, "commit runs not contiguous"};
-    int gid = p->group[p->order[pos]];
-    for (int q = pos; q < pos + p->commit_count[ci]; ++q) {
-      if (q >= p->n_commit) throw Fail{MLF_E_INVALID, "commit runs exceed n_commit"};
+    const int cnt = p->commit_count[ci];
+    if (p->commit_first[ci] != pos || cnt < 1) throw Fail{MLF_E_INVALID, "commit runs not contiguous"};
+    if (pos >= p->n_commit || cnt > p->n_commit - pos) throw Fail{MLF_E_INVALID, "commit runs exceed n_commit"};
+    const int gid = p->group[p->order[pos]];
+    for (int q = pos; q < pos + cnt; ++q)
       if (p->group[p->order[q]] != gid) throw Fail{MLF_E_INVALID, "commit mixes groups"};
-    }
     if (gid < 0 || gid > p->n_groups) throw Fail{MLF_E_INVALID, "group id out of range"};
     if (gid > 0) {
       int node = p->group_node ? p->group_node[gid - 1] : -1;
       if (node < 0 || node >= (int)c->node_rank.size()) throw Fail{MLF_E_INVALID, "aggregator node unknown to the executor"};
     }
-    pos += p->commit_count[ci];
+    pos += cnt;
   }
   if (pos != p->n_commit) throw Fail{MLF_E_INVALID, "commit runs do not cover O(U)"};
   if (p->replica_boundary_commit < -1 || p->replica_boundary_commit > p->n_server_commits)
@@ -368,19 +374,33 @@ static void validate_plan(const mlf_ctx *c, const mlf_plan_out *p) {
     throw Fail{MLF_E_INVALID, "plan writes the replica but the context has no backup shard"};
   if (c->cfg.replica_mode == 1) {
     // the plan must be a replica-trees plan over this context's carried items
+    const int carried = (int)c->carried.size();
+    if (p->n_punted < 0 || p->replica_frozen < 0 || p->replica_frozen > carried + p->n_commit)
+      throw Fail{MLF_E_INVALID, "replica_frozen / n_punted out of range"};
     const int n_c = p->replica_frozen + p->n_punted - p->n_commit;
-    if (p->replica_boundary_commit != -1 || n_c != (int)c->carried.size())
+    if (p->replica_boundary_commit != -1 || n_c != carried)
       throw Fail{MLF_E_INVALID, "plan is not a replica-trees plan over the carried items"};
-    if (p->n_replica_commits < 0 || (p->n_replica_commits > 0 && (!p->replica_commit_first || !p->replica_commit_count)))
+    if (p->n_replica_commits < 0 || p->n_replica_commits > p->replica_frozen ||
+        (p->n_replica_commits > 0 && (!p->replica_commit_first || !p->replica_commit_count)))
       throw Fail{MLF_E_INVALID, "replica commits"};
     int rpos = 0;
     for (int ci = 0; ci < p->n_replica_commits; ++ci) {
-      if (p->replica_commit_first[ci] != rpos || p->replica_commit_count[ci] < 1)
+      if (p->replica_commit_first[ci] != rpos || p->replica_commit_count[ci] < 1 ||
+          p->replica_commit_count[ci] > p->replica_frozen - rpos)
         throw Fail{MLF_E_INVALID, "replica commit runs not contiguous"};
       rpos += p->replica_commit_count[ci];
     }
     if (rpos != p->replica_frozen) throw Fail{MLF_E_INVALID, "replica commits do not cover the frozen prefix"};
   }
+  // delay bound (R1, R2): the update at 1-based position p commits as version v + p
+  if (c->cfg.enforce_tau && !p->sync_mode)
+    for (int i = 0; i < p->n_commit; ++i) {
+      const int64_t delay = c->version + (int64_t)(i + 1) - c->b_version[p->order[i]];
+      if (delay > (int64_t)c->cfg.tau_max)
+        throw Fail{MLF_E_INVALID, "plan commits update " + std::to_string(p->order[i]) + " at position " +
+                                      std::to_string(i + 1) + " with delay " + std::to_string(delay) +
+                                      " > tau_max " + std::to_string(c->cfg.tau_max)};
+    }
 }
 
 static bool tree_mode(const mlf_ctx *c) { return c->cfg.world > 1 && c->cfg.agg_slots > 0; }
@@ -460,7 +480,8 @@ struct CommitOp {
 };
 
 // Momentum commits (NEXT-1, Eq. 2 with gamma > 0): the aggregate form's weights per member
-// and per commit, from float64 powers summed left to right (oracle/momentum.py coefficients).
+// and per commit (the expansion of m sequential Eq. 2 steps), from
+// float64 powers of the double gamma summed left to right, each rounded once to fp32 (R21).
 static void launch_momentum(mlf_ctx *c, const mlf_plan_out *p, const std::vector<CommitOp> &ops, int boundary) {
   const double g = c->cfg.gamma;
   size_t i0 = 0;
@@ -567,7 +588,7 @@ static void launch_ops(mlf_ctx *c, float *w, float *backup, const std::vector<Co
 static constexpr int64_t kPipeChunk = 1 << 22;     // elements per chunk (16 MB of fp32)
 
 static bool pipelined(const mlf_ctx *c, const mlf_plan_out *p) {
-  if (c->cfg.world != 1 || c->cfg.gamma != 0.f || c->cfg.replica_mode != 0 || !c->bcast.empty()) return false;
+  if (c->cfg.world != 1 || c->cfg.gamma != 0.0 || c->cfg.replica_mode != 0 || !c->bcast.empty()) return false;
   if (c->pull_host) return true;
   for (int i = 0; i < p->n_commit; ++i)
     if (c->host_src[c->b_worker[p->order[i]]]) return true;
@@ -781,7 +802,7 @@ static void phase_commit(mlf_ctx *c, const mlf_plan_out *p) {
   }
   const bool trees = c->cfg.replica_mode == 1;
   const int boundary = (c->cfg.backup_shard && !trees) ? p->replica_boundary_commit : -1;
-  if (c->cfg.gamma != 0.f)
+  if (c->cfg.gamma != 0.0)
     launch_momentum(c, p, ops, boundary);
   else if (pipelined(c, p))
     pipeline_commit(c, p, ops, boundary);

@@ -74,7 +74,7 @@ class Workload:
                              gamma=self.gamma, history=self.h,
                              backup_history=(backup_h_ptr if backup_h_ptr is not None else self.backup_h),
                              replica_mode=self.replica_mode, retain_slots=retain_table, bcast=bcast,
-                             stage=stage, bcast_multicast=bcast_multicast)
+                             stage=stage, bcast_multicast=bcast_multicast, tau_max=cfg["tau"])
         self.v_init, self.v_prev = 0, 0
         self.iteration = 0
         self.carried = []

@@ -84,10 +84,11 @@ class MlfConfig(C.Structure):
                 ("model_shard", _p), ("backup_shard", _p), ("update_slot", C.POINTER(_p)),
                 ("worker_rank", _i32p), ("n_nodes", C.c_int32), ("node_rank", _i32p),
                 ("worker_node", _i32p), ("agg_slots", C.c_int32), ("agg_scratch", C.POINTER(_p)),
-                ("stream", _p), ("gamma", C.c_float), ("history_shard", _p), ("backup_history", _p),
+                ("stream", _p), ("gamma", C.c_double), ("history_shard", _p), ("backup_history", _p),
                 ("replica_mode", C.c_int32), ("n_retain", C.c_int32), ("retain_slot", C.POINTER(_p)),
                 ("n_bcast", C.c_int32), ("bcast", C.POINTER(_p)),
-                ("stage_buf", _p), ("stage_bytes", C.c_int64), ("bcast_multicast", C.c_int32)]
+                ("stage_buf", _p), ("stage_bytes", C.c_int64), ("bcast_multicast", C.c_int32),
+                ("enforce_tau", C.c_int32), ("tau_max", C.c_int32)]
 
 
 class MlfIpcHandle(C.Structure):
@@ -326,9 +327,11 @@ class Context:
                  backup_shard=None, worker_rank=None, node_rank=None, n_nodes=None, agg_slots: int = 0,
                  agg_scratch=None, stream=None, v0: int = 0, worker_node=None, gamma: float = 0.0,
                  history=None, backup_history=None, replica_mode: int = 0, retain_slots=None, bcast=None,
-                 stage=None, bcast_multicast: bool = False):
+                 stage=None, bcast_multicast: bool = False, tau_max: int | None = None):
         """update_slots: list of int device pointers (or torch tensors); model_shard/backup_shard:
-        torch tensors or int pointers; stream: int cudaStream_t (None -> default stream)."""
+        torch tensors or int pointers; stream: int cudaStream_t (None -> default stream);
+        tau_max: the server's registered delay bound (Table 1), enforced by mlf_execute on every
+        asynchronous plan (None: not enforced)."""
         def ptr(x):
             if x is None:
                 return None
@@ -364,6 +367,9 @@ class Context:
             self.cfg.n_bcast = len(bc)
             self.cfg.bcast = self._bc
             self.cfg.bcast_multicast = 1 if bcast_multicast else 0
+        if tau_max is not None:
+            self.cfg.enforce_tau = 1
+            self.cfg.tau_max = int(tau_max)
         if stage is not None:                       # copy-engine staging buffer (torch tensor)
             self.cfg.stage_buf = ptr(stage)
             self.cfg.stage_bytes = stage.numel() * stage.element_size()

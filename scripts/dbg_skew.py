@@ -8,7 +8,8 @@ import torch
 import torch.distributed as dist
 
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
-from paper_1907_00434_b200.multigpu import ShardedWorkload, init_dist, plan_traffic  # noqa: E402
+from benchkit.multi import plan_traffic  # noqa: E402
+from paper_1907_00434_b200.multigpu import ShardedWorkload, init_dist  # noqa: E402
 from synthgen import configs  # noqa: E402
 
 

@@ -70,6 +70,49 @@ def test_momentum_random_plans(gamma, dtype):
         assert np.max(np.abs(w - w64)) <= 1e-6 * max(np.max(np.abs(w64)), 1e-30)
 
 
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_momentum_config2_every_element_vs_sequential_eq2(dtype):
+    """The plain definition at full size (R21): config 2, gamma =
+    0.9, tau = 32, two batches; EVERY one of the 25.6M elements of w and h on the GPU lies within
+    the per-element forward error bound of sequential Eq. 2 in float64 (tests/momentum_bound.py),
+    and the norm-relative error max|dw| / max|w64| is <= 1e-6 (the north star's fp32 target)."""
+    from oracle.numerics import widen
+    from tests.momentum_bound import sequential_with_bound
+    cfg = configs.config(2, tau=32, gamma=0.9, dtype=dtype)
+    wl = Workload(cfg, device=0)
+    S, lr = cfg["S"], cfg["lr"]
+    sdt = sg.DTYPE_BF16 if dtype == "bf16" else sg.DTYPE_F32
+    plans = []
+    for it in range(2):
+        pb, pd, draws = wl.step(it)
+        plans.append(pd)
+    wl.ctx.sync()
+    w_gpu = wl.w.cpu().numpy()
+    h_gpu = wl.h.cpu().numpy()
+    wl.ctx.close()
+    assert sum(p["n_commit"] for p in plans) >= 48
+    chunk = 1 << 22
+    worst_w = worst_h = 0.0
+    max_dw = max_w = 0.0
+    for lo in range(0, S, chunk):
+        idx = np.arange(lo, min(S, lo + chunk))
+        w64 = sg.w0_values(cfg["seed"], idx)
+        h64 = np.zeros(len(idx), np.float32)
+        commits = []
+        for it, pd in enumerate(plans):
+            commits += commits_from_plan(pd, lambda g, it=it: sg.update_values(cfg["seed"], g, it, idx, sdt))
+        w64, h64, bw, bh = sequential_with_bound(w64, h64, commits, lr, 0.9, widen)
+        dw = np.abs(w_gpu[idx].astype(np.float64) - w64)
+        dh = np.abs(h_gpu[idx].astype(np.float64) - h64)
+        assert np.all(dw <= bw), (lo, float(np.max(dw / bw)))
+        assert np.all(dh <= bh), (lo, float(np.max(dh / bh)))
+        worst_w, worst_h = max(worst_w, float(np.max(dw / bw))), max(worst_h, float(np.max(dh / bh)))
+        max_dw, max_w = max(max_dw, float(dw.max())), max(max_w, float(np.abs(w64).max()))
+    assert max_dw <= 1e-6 * max_w, (max_dw, max_w)
+    print(f"momentum {dtype}: worst |dw|/bound {worst_w:.3f}, |dh|/bound {worst_h:.3f}, "
+          f"norm-relative {max_dw / max_w:.2e}")
+
+
 @pytest.mark.parametrize("dtype,tau", [("f32", 32), ("bf16", 32), ("bf16", 4)])
 def test_momentum_config2_full_size(dtype, tau):
     # fp32 takes the generic fold, all-bf16 operand lists the branch-free one (both kernels:

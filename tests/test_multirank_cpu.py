@@ -23,7 +23,8 @@ def _worker(rank, world, port, cid, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_1907_00434_b200 import mlfabric as m
-    from paper_1907_00434_b200.multigpu import agg_slots_needed, plan_traffic
+    from benchkit.multi import plan_traffic
+    from paper_1907_00434_b200.multigpu import agg_slots_needed
 
     cfg = configs.config(cid, G=world, scale_S=1_000_003)
     plans = []

@@ -69,3 +69,29 @@ def test_weighted_close_to_sequential_f64():
         single = [[g] for mem in commits for g in mem]
         w1, _, _ = weighted_f32(w0, h0, single, 0.01, gamma)
         assert np.max(np.abs(w1 - w64)) <= 1e-6 * np.max(np.abs(w64))
+
+
+def test_weighted_within_per_element_bound_of_sequential():
+    # DESIGN.md R21: every element of the fp32 aggregate form lies within the first-order forward
+    # error bound of the plain sequential Eq. 2 (tests/momentum_bound.py); a dropped or wrong
+    # weight (e.g. cB with gamma^(m-i+1)) moves elements by ~|u| >> the bound
+    from oracle.numerics import widen
+    from tests.momentum_bound import sequential_with_bound
+    n = 200_000
+    idx = np.arange(n)
+    for seed, gamma, dt in ((4, 0.9, sg.DTYPE_F32), (5, 0.9, sg.DTYPE_BF16), (6, 0.99, sg.DTYPE_F32)):
+        rng = np.random.default_rng(seed)
+        commits, w_id = [], 0
+        for _ in range(12):
+            m = int(rng.integers(1, 9))
+            commits.append([sg.update_values(seed, w_id + j, 0, idx, dt) for j in range(m)])
+            w_id += m
+        w0 = sg.w0_values(seed, idx)
+        h0 = (sg.w0_values(seed + 100, idx) * np.float32(1e-3)).astype(np.float32)
+        w32, h32, _ = weighted_f32(w0, h0, commits, 0.01, gamma)
+        w64, h64, bw, bh = sequential_with_bound(w0, h0, commits, 0.01, gamma, widen)
+        assert np.all(np.abs(w32 - w64) <= bw) and np.all(np.abs(h32 - h64) <= bh)
+        # the bound is tight enough to matter: a plausible slip in the weights breaks it
+        bad = [[g for g in mem] for mem in commits]
+        wb, _, _ = weighted_f32(w0, h0, [mem[::-1] for mem in bad], 0.01, gamma)   # members reversed
+        assert np.any(np.abs(wb - w64) > bw)
