@@ -31,6 +31,7 @@
 #include <cstring>
 #include <functional>
 #include <limits>
+#include <memory>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -224,11 +225,84 @@ static bool path_dead(const NetDef &d, int src, int dst) {
 struct TSeg {
   i64 a, b, r;        // rate r used on [a, b)
 };
-struct Res {
-  i64 key;            // link
-  TSeg s;
+
+// A piecewise-constant function as a canonical step profile: segment i holds value p[i].r on
+// [p[i].t, p[i+1].t), p[0].t == 0, no two adjacent segments with equal values (a fully
+// reserved stretch of a link is ONE zero segment, so a t_en walk skips it in one step).
+// combine() adds sign * (the sum of the segments s) to p in one merge pass over the affected
+// range.  The function is exactly the one of adding the segments one by one, and a canonical
+// profile is unique, so the representation (hence every later t_en) does not depend on the
+// order in which reservations were applied.
+static void combine(Profile &p, const TSeg *s, int m, int sign) {
+  struct Ev {
+    i64 t, d;
+  };
+  thread_local std::vector<Ev> ev;
+  thread_local Profile tmp;
+  ev.clear();
+  for (int i = 0; i < m; ++i)
+    if (s[i].r != 0 && s[i].a < s[i].b) {
+      ev.push_back({s[i].a, sign * s[i].r});
+      ev.push_back({s[i].b, -sign * s[i].r});
+    }
+  if (ev.empty()) return;
+  // one transfer's segments, or a reserved-rate profile, arrive in time order already
+  if (!std::is_sorted(ev.begin(), ev.end(), [](const Ev &x, const Ev &y) { return x.t < y.t; }))
+    std::sort(ev.begin(), ev.end(), [](const Ev &x, const Ev &y) { return x.t < y.t; });
+  const i64 A = ev.front().t, B = ev.back().t;
+  // ia = last segment starting at or before A (p[0].t == 0 <= A)
+  size_t ia = (size_t)(std::upper_bound(p.begin(), p.end(), A, [](i64 v, const Seg &x) { return v < x.t; }) -
+                       p.begin()) - 1;
+  const size_t keep = p[ia].t < A ? ia + 1 : ia;       // p[0, keep) stays as it is
+  i64 base = p[ia].r, delta = 0;
+  size_t pi = ia + 1, ei = 0;
+  tmp.clear();
+  for (i64 t = A;;) {
+    while (pi < p.size() && p[pi].t <= t) base = p[pi++].r;
+    while (ei < ev.size() && ev[ei].t <= t) delta += ev[ei++].d;
+    const i64 r = base + delta;
+    if (r < 0) throw PlanFail{MLF_E_INVALID, "internal: residual went negative"};
+    const i64 prev = tmp.empty() ? (keep > 0 ? p[keep - 1].r : -1) : tmp.back().r;
+    if (r != prev) tmp.push_back({t, r});
+    if (t >= B) break;
+    i64 nt = ev[ei].t;                                 // ei < ev.size() while t < B
+    if (pi < p.size()) nt = std::min(nt, p[pi].t);
+    t = nt;
+  }
+  // p[keep, pi) is replaced by tmp (pi = first segment starting after B)
+  const size_t old_n = pi - keep, new_n = tmp.size();
+  if (new_n > old_n)
+    p.insert(p.begin() + (std::ptrdiff_t)pi, new_n - old_n, Seg{0, 0});
+  else if (new_n < old_n)
+    p.erase(p.begin() + (std::ptrdiff_t)(keep + new_n), p.begin() + (std::ptrdiff_t)pi);
+  std::copy(tmp.begin(), tmp.end(), p.begin() + (std::ptrdiff_t)keep);
+}
+
+// Reservations evaluated but not applied to a Net: per link, the reserved rate as a step
+// profile (0 outside the reservations), so a transfer walks it with a cursor like the
+// link's own residual profile.  clear() keeps every buffer's capacity.
+struct Pending {
+  int nkeys = 0;
+  std::vector<i64> keys;
+  std::vector<Profile> used;
+  void clear() { nkeys = 0; }
+  const Profile *find(i64 key) const {
+    for (int i = 0; i < nkeys; ++i)
+      if (keys[i] == key) return &used[i];
+    return nullptr;
+  }
+  Profile &slot(i64 key) {
+    for (int i = 0; i < nkeys; ++i)
+      if (keys[i] == key) return used[i];
+    if (nkeys == (int)keys.size()) {
+      keys.push_back(key);
+      used.emplace_back();
+    }
+    keys[nkeys] = key;
+    used[nkeys].assign(1, Seg{0, 0});
+    return used[nkeys++];
+  }
 };
-using Pending = std::vector<Res>;   // reservations evaluated but not applied to a Net
 
 struct Transfer {
   i64 t_st = 0, t_en = 0;
@@ -236,11 +310,41 @@ struct Transfer {
   std::vector<TSeg> segs;
 };
 
+// cursor over a step profile: i = the segment holding the current time
+struct Cur {
+  const Seg *p = nullptr;
+  int n = 0, i = 0;
+  void seek(const Profile *pr, i64 t) {
+    if (!pr) {
+      n = 0;
+      return;
+    }
+    p = pr->data();
+    n = (int)pr->size();
+    const Seg *it = std::upper_bound(p, p + n, t, [](i64 v, const Seg &s) { return v < s.t; });
+    i = it == p ? 0 : (int)(it - p) - 1;
+  }
+  i64 at(i64 t) {                                  // value at t (t never decreases)
+    if (!n) return 0;
+    while (i + 1 < n && p[i + 1].t <= t) ++i;
+    return p[i].r;
+  }
+  i64 next() const { return (n && i + 1 < n) ? p[i + 1].t : T_INF; }
+};
+
 // O1: water-fill `size` bytes from t_avail along the path residual (Fig. 5(b)),
 // on `net` minus the pending reservations of L0 and L1.  Returns false if the
 // path residual is zero forever after t_avail.
+// A walk step of a transfer: on [t0, t1) every path link k had `slack[k]` more residual than
+// the path minimum the transfer used.  Reserving at most slack[k] more on link k inside the
+// window leaves the path minimum, hence the whole transfer, unchanged (used by the
+// ordering's per-class cache, order_final).
+struct WalkRec {
+  i64 t0, t1, slack[3];
+};
+
 static bool transfer(const Net &net, const Pending *L0, const Pending *L1, i64 size, int src, int dst, i64 t_avail,
-                     Transfer &out) {
+                     Transfer &out, std::vector<WalkRec> *rec = nullptr) {
   const NetDef &d = *net.def;
   out.segs.clear();
   out.path = path_of(d, src, dst);
@@ -250,125 +354,89 @@ static bool transfer(const Net &net, const Pending *L0, const Pending *L1, i64 s
     return true;
   }
   struct Lk {
-    const Seg *p;
-    int n, idx;
-    Seg own;
-    int e0, e1;       // pending-reservation events of this link, sorted by time: [e0, e1) in `ev`
-    i64 used;         // pending rate active at the cursor
+    Cur base, u0, u1;   // the link's residual, minus the reserved rate of L0 and of L1
+    Seg own;            // a pair link not reserved yet: its capacity
   };
-  struct Ev {
-    i64 t, d;         // at time t the pending rate changes by d
-  };
-  thread_local std::vector<Ev> ev;
-  ev.clear();
   Lk lk[3];
   const int nk = out.path.nk;
   for (int k = 0; k < nk; ++k) {
     const i64 key = out.path.key[k];
     const Profile *pr = net.get(key);
     if (pr) {
-      lk[k].p = pr->data();
-      lk[k].n = (int)pr->size();
+      lk[k].base.seek(pr, t_avail);
     } else {
       lk[k].own = Seg{0, std::max<i64>(net.capacity(key), 0)};
-      lk[k].p = &lk[k].own;
-      lk[k].n = 1;
+      lk[k].base.p = &lk[k].own;
+      lk[k].base.n = 1;
+      lk[k].base.i = 0;
     }
-    // last segment with start <= t_avail
-    const Seg *b = lk[k].p, *e = lk[k].p + lk[k].n;
-    const Seg *it = std::upper_bound(b, e, t_avail, [](i64 v, const Seg &s) { return v < s.t; });
-    lk[k].idx = it == b ? 0 : (int)(it - b) - 1;
-    lk[k].e0 = (int)ev.size();
-    lk[k].used = 0;
-    for (const Pending *L : {L0, L1})
-      if (L)
-        for (const Res &r : *L)
-          if (r.key == key && r.s.b > t_avail) {
-            if (r.s.a <= t_avail)
-              lk[k].used += r.s.r;
-            else
-              ev.push_back({r.s.a, r.s.r});
-            ev.push_back({r.s.b, -r.s.r});
-          }
-    lk[k].e1 = (int)ev.size();
-    for (int i = lk[k].e0 + 1; i < lk[k].e1; ++i) {      // insertion sort: a few dozen events at most
-      Ev x = ev[i];
-      int j = i - 1;
-      for (; j >= lk[k].e0 && ev[j].t > x.t; --j) ev[j + 1] = ev[j];
-      ev[j + 1] = x;
-    }
+    lk[k].u0.seek(L0 ? L0->find(key) : nullptr, t_avail);
+    lk[k].u1.seek(L1 ? L1->find(key) : nullptr, t_avail);
   }
   i128 need = (i128)size * NS_PER_S;
   i64 cur = t_avail;
   bool started = false;
   for (;;) {
-    i64 r = T_INF, nb = T_INF;
+    // r = path residual at cur, nb = its next possible change; while some link is saturated
+    // the path stays at 0 at least until every saturated link's own next change (zjump), so
+    // the walk jumps there instead of stepping through the other links' breakpoints
+    i64 r = T_INF, nb = T_INF, zjump = t_avail, rks[3];
     for (int k = 0; k < nk; ++k) {
       Lk &L = lk[k];
-      while (L.idx + 1 < L.n && L.p[L.idx + 1].t <= cur) ++L.idx;
-      while (L.e0 < L.e1 && ev[L.e0].t <= cur) L.used += ev[L.e0++].d;
-      const i64 rk = L.p[L.idx].r - L.used;
-      i64 nbk = L.idx + 1 < L.n ? L.p[L.idx + 1].t : T_INF;
-      if (L.e0 < L.e1) nbk = std::min(nbk, ev[L.e0].t);
+      const i64 rk = L.base.at(cur) - L.u0.at(cur) - L.u1.at(cur);
+      rks[k] = rk;
+      const i64 nbk = std::min(L.base.next(), std::min(L.u0.next(), L.u1.next()));
+      if (rk == 0) zjump = std::max(zjump, nbk);
       r = std::min(r, rk);
       nb = std::min(nb, nbk);
     }
     if (r < 0) throw PlanFail{MLF_E_INVALID, "internal: negative residual"};
-    if (r > 0) {
-      if (!started) {
-        out.t_st = cur;
-        started = true;
-      }
-      if (nb == T_INF || (i128)r * (nb - cur) >= need) {
-        i128 dt = (need + r - 1) / r;
-        if ((i128)cur + dt > (i128)T_LIMIT) throw PlanFail{MLF_E_INVALID, "model time overflow"};
-        out.t_en = cur + (i64)dt;
-        out.segs.push_back({cur, out.t_en, r});
-        return true;
-      }
-      need -= (i128)r * (nb - cur);
-      out.segs.push_back({cur, nb, r});
-    } else if (nb == T_INF) {
-      return false;
+    if (r == 0) {
+      if (zjump == T_INF) return false;          // a link on the path is saturated forever
+      cur = zjump;
+      continue;
     }
+    if (!started) {
+      out.t_st = cur;
+      started = true;
+    }
+    if (nb == T_INF || (i128)r * (nb - cur) >= need) {
+      i128 dt = (need + r - 1) / r;
+      if ((i128)cur + dt > (i128)T_LIMIT) throw PlanFail{MLF_E_INVALID, "model time overflow"};
+      out.t_en = cur + (i64)dt;
+      out.segs.push_back({cur, out.t_en, r});
+      if (rec) rec->push_back({cur, out.t_en, {rks[0] - r, nk > 1 ? rks[1] - r : 0, nk > 2 ? rks[2] - r : 0}});
+      return true;
+    }
+    need -= (i128)r * (nb - cur);
+    out.segs.push_back({cur, nb, r});
+    if (rec) rec->push_back({cur, nb, {rks[0] - r, nk > 1 ? rks[1] - r : 0, nk > 2 ? rks[2] - r : 0}});
     cur = nb;
   }
 }
 
 static void add_pending(Pending &P, const Transfer &tr) {
-  for (int k = 0; k < tr.path.nk; ++k)
-    for (auto &s : tr.segs) P.push_back({tr.path.key[k], s});
+  for (int k = 0; k < tr.path.nk; ++k) combine(P.slot(tr.path.key[k]), tr.segs.data(), (int)tr.segs.size(), +1);
 }
 
 // O2: NetUp — subtract reservations from the residual profiles.
-static void split_at(Profile &p, i64 t) {
-  auto it = std::lower_bound(p.begin(), p.end(), t, [](const Seg &s, i64 v) { return s.t < v; });
-  if (it != p.end() && it->t == t) return;
-  i64 r = (it == p.begin()) ? p.front().r : std::prev(it)->r;
-  p.insert(it, Seg{t, r});
-}
-static void subtract(Profile &p, i64 a, i64 b, i64 r) {
-  split_at(p, a);
-  split_at(p, b);
-  auto lo = std::lower_bound(p.begin(), p.end(), a, [](const Seg &s, i64 v) { return s.t < v; });
-  auto it = lo;
-  for (; it != p.end() && it->t < b; ++it) {
-    it->r -= r;
-    if (it->r < 0) throw PlanFail{MLF_E_INVALID, "internal: residual went negative"};
-  }
-  // keep the profile canonical (no two adjacent segments with equal rates) around the edit:
-  // a fully reserved stretch collapses into one zero segment, so later t_en walks skip it in
-  // one step.  The residual function is unchanged, hence so is every t_en.
-  size_t i0 = (size_t)(lo - p.begin());
-  i0 = i0 > 0 ? i0 - 1 : 0;
-  size_t i1 = std::min(p.size(), (size_t)(it - p.begin()) + 1);
-  size_t w = i0 + 1;
-  for (size_t i = i0 + 1; i < i1; ++i)
-    if (p[i].r != p[w - 1].r) p[w++] = p[i];
-  if (w < i1) p.erase(p.begin() + w, p.begin() + i1);
-}
 static void apply_pending(Net &net, const Pending &P) {
-  for (const Res &r : P) subtract(net.mut(r.key), r.s.a, r.s.b, r.s.r);
+  thread_local std::vector<TSeg> segs;
+  for (int i = 0; i < P.nkeys; ++i) {
+    const Profile &u = P.used[i];
+    segs.clear();
+    for (size_t q = 0; q + 1 < u.size(); ++q)
+      if (u[q].r) segs.push_back({u[q].t, u[q + 1].t, u[q].r});
+    combine(net.mut(P.keys[i]), segs.data(), (int)segs.size(), -1);
+  }
+}
+static void copy_pending(Pending &dst, const Pending &src) {
+  dst.nkeys = src.nkeys;
+  dst.keys.assign(src.keys.begin(), src.keys.begin() + src.nkeys);
+  dst.used.assign(src.used.begin(), src.used.begin() + src.nkeys);
+}
+static void apply_transfer(Net &net, const Transfer &tr) {
+  for (int k = 0; k < tr.path.nk; ++k) combine(net.mut(tr.path.key[k]), tr.segs.data(), (int)tr.segs.size(), -1);
 }
 
 // App. B.2: component sizes proportional to the shard weights.
@@ -391,21 +459,50 @@ struct Ctx {
   std::vector<int> servers, aggs, replicas, raggs;
   std::vector<i64> weights;
   i64 wsum = 0;
+  bool dup_dsts = false;     // a destination list (servers / replicas) repeats a node
 };
 
 // Multi-component transfer: components reserved sequentially in destination
 // order (R11) into `local` (pending on top of net - L0); t_en = max, t_st = min.
+// record_all = false (a pure evaluation, nothing is applied afterwards): `local` keeps only the
+// links a LATER component can share — up(src), and a later destination's own links when the
+// destination list repeats a node — which is all the later transfers read.
+// The walk of one send, component by component (CompRec: path + its WalkRec range).
+struct CompRec {
+  Path path;
+  int w0, w1;
+};
+struct SendRec {
+  std::vector<CompRec> comps;
+  std::vector<WalkRec> walk;
+};
+
 static bool send(const Net &net, const Pending *L0, const Ctx &c, const std::vector<int> &dsts, int src, i64 size,
-                 i64 t_avail, Send &out, Pending &local) {
+                 i64 t_avail, Send &out, Pending &local, bool record_all = true, SendRec *rec = nullptr) {
   thread_local std::vector<i64> comp;
   thread_local Transfer tr;
   component_bytes(size, c.weights, c.wsum, comp);
   local.clear();
   out.t_st = T_INF;
   out.t_en = 0;
+  const i64 n = c.d.n;
+  const bool all = record_all || c.dup_dsts;
+  if (rec) {
+    rec->comps.clear();
+    rec->walk.clear();
+  }
   for (size_t j = 0; j < dsts.size(); ++j) {
-    if (!transfer(net, L0, &local, comp[j], src, dsts[j], t_avail, tr)) return false;
-    add_pending(local, tr);
+    const int w0 = rec ? (int)rec->walk.size() : 0;
+    if (!transfer(net, L0, &local, comp[j], src, dsts[j], t_avail, tr, rec ? &rec->walk : nullptr)) return false;
+    if (rec) rec->comps.push_back({tr.path, w0, (int)rec->walk.size()});
+    if (j + 1 < dsts.size()) {
+      if (all)
+        add_pending(local, tr);
+      else if (tr.path.nk && tr.path.key[0] < n)       // up(src) is always the first path link
+        combine(local.slot(tr.path.key[0]), tr.segs.data(), (int)tr.segs.size(), +1);
+    } else if (record_all) {
+      add_pending(local, tr);
+    }
     out.t_st = std::min(out.t_st, tr.t_st);
     out.t_en = std::max(out.t_en, tr.t_en);
   }
@@ -431,9 +528,35 @@ struct Item {
 struct OrderRes {
   std::vector<int> order;
   std::vector<uint8_t> reason;
+  // the reservation of every kept update, in O(U) order, on the batch-start network with the
+  // earlier kept ones applied: exactly Alg. 3's direct prefix (R10), reused by plan_aggregation
+  std::vector<Pending> res;
+  std::vector<Send> sends;
 };
 
 static constexpr int kMinParallelEvals = 32;   // component transfers per scan worth a pool dispatch
+
+// True if reserving `M` on top of the network a send was recorded on leaves the send's result
+// unchanged: on every walk step, no path link loses more than its slack (components are
+// reserved one after another, so an unchanged component also leaves the later components'
+// inputs unchanged).  Saturated stretches were skipped by the walk and stay saturated.
+static bool send_unchanged(const SendRec &rec, const Pending &M) {
+  for (const CompRec &cr : rec.comps)
+    for (int k = 0; k < cr.path.nk; ++k) {
+      const Profile *u = M.find(cr.path.key[k]);
+      if (!u) continue;
+      Cur cu;
+      for (int w = cr.w0; w < cr.w1; ++w) {
+        const WalkRec &wr = rec.walk[w];
+        if (w == cr.w0) cu.seek(u, wr.t0);
+        // the largest reserved rate of M on [t0, t1)
+        i64 mx = cu.at(wr.t0);
+        for (int q = cu.i + 1; q < cu.n && cu.p[q].t < wr.t1; ++q) mx = std::max(mx, cu.p[q].r);
+        if (mx > wr.slack[k]) return false;
+      }
+    }
+  return true;
+}
 
 static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 tau, i64 v_init) {
   const int n = (int)batch.size();
@@ -448,7 +571,7 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
   const int G = (int)c.servers.size();
   std::vector<i64> ten(n);
   std::vector<uint8_t> ok(n);
-  std::vector<int> pool, uniq, rep(n, -1);
+  std::vector<int> pool, uniq, miss, rep(n, -1);
   // t_en is a pure function of (network, node, size, t_avail): updates sharing the triple
   // (virtual workers on one GPU usually share all three) form one class, evaluated once per scan
   std::vector<int> cls(n), cls_rep, cls_stamp;
@@ -474,6 +597,15 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
     cls_stamp.assign(k + 1, -1);
   }
   int scan = 0;
+  // Per-class result cache.  Network states get ids: nw_id = NW, la_id = NW + the look-ahead's
+  // reservation of g*; NW takes la_id when g* is kept and keeps nw_id when it is dropped.
+  struct ClassCache {
+    int tag = -1;
+    i64 t_en = 0;
+    SendRec rec;
+  };
+  std::vector<ClassCache> cache(cls_rep.size());
+  int nw_id = 0, la_id = 0, next_id = 1;
 
   // ShrtDline(pos, cands, NW + L0): the due set's argmin if any, else ShrtUp (R4, R6).
   auto pick = [&](i64 pos, const std::vector<int> &cands, const Pending *L0) -> int {
@@ -498,16 +630,35 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
       }
       rep[g] = cls_rep[k];
     }
+    // a class evaluated on NW (tag nw_id) keeps its result on NW + L0 when L0 = the look-ahead's
+    // reservation costs none of its walk steps more than their slack (send_unchanged); the
+    // others are evaluated again, on the pool when there are enough of them
+    const int tag = L0 ? la_id : nw_id;
+    miss.clear();
+    for (int g : uniq) {
+      ClassCache &cc = cache[cls[g]];
+      if (cc.tag == tag || (L0 && cc.tag == nw_id && send_unchanged(cc.rec, *L0))) {
+        cc.tag = tag;
+        ok[g] = 1;
+        ten[g] = cc.t_en;
+      } else {
+        miss.push_back(g);
+      }
+    }
     Pool::get().run(
-        (int)uniq.size(),
+        (int)miss.size(),
         [&](int i) {
           thread_local Pending local;
-          const int g = uniq[i];
+          const int g = miss[i];
+          ClassCache &cc = cache[cls[g]];
           Send s;
-          ok[g] = send(nw, L0, c, c.servers, batch[g].node, batch[g].size, batch[g].t_avail, s, local);
+          ok[g] = send(nw, L0, c, c.servers, batch[g].node, batch[g].size, batch[g].t_avail, s, local, false,
+                       &cc.rec);
           ten[g] = s.t_en;
+          cc.tag = ok[g] ? tag : -1;
+          cc.t_en = s.t_en;
         },
-        std::max(1, kMinParallelEvals / std::max(1, G)));
+        std::max(2, kMinParallelEvals / std::max(1, G)));
     int best = -1;
     for (int g : pool) {
       ok[g] = ok[rep[g]];
@@ -544,6 +695,7 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
       if (g != g_star && dl[g] >= p + 1) cands.push_back(g);
     bool drop = false;
     int g_next = -1;
+    la_id = next_id++;
     if (!cands.empty()) {
       g_next = pick(p + 1, cands, &star);              // on NetUp(NW, g*)
       if (t_star > ten[g_next]) drop = true;           // Alg. 2 line 10
@@ -555,6 +707,10 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
     }
     res.order.push_back(g_star);
     apply_pending(nw, star);
+    nw_id = la_id;
+    res.res.emplace_back();
+    copy_pending(res.res.back(), star);
+    res.sends.push_back(s_star);
     ++p;
     cached = g_next;
   }
@@ -577,8 +733,11 @@ struct AggCase {
 
 // Alg. 3 DetAgg(n), continued from the state after its n direct sends (R10-R12):
 // `nw` holds that network, t_max/commits the direct part.
+// `cutoff`: the case only matters if its total can still be < cutoff (the argmin's best so
+// far); t_max never decreases, so the walk stops as soon as t_max > cutoff (result: not feasible
+// for the argmin).  T_INF = no cutoff.
 static void det_agg_tail(AggCase &cs, Net &nw, i64 t_max, const std::vector<Item> &items, const Ctx &c,
-                         const std::vector<int> &dsts, const std::vector<int> &aggs) {
+                         const std::vector<int> &dsts, const std::vector<int> &aggs, i64 cutoff = T_INF) {
   const int n = cs.n;
   bool have = n > 0;
   const int k = (int)aggs.size();
@@ -598,18 +757,15 @@ static void det_agg_tail(AggCase &cs, Net &nw, i64 t_max, const std::vector<Item
     return true;
   };
   thread_local Transfer tr;
-  thread_local Pending P;
   while (i < (int)items.size()) {
-    if (aid > k) return;
+    if (aid > k || t_max > cutoff) return;
     if (!transfer(nw, nullptr, nullptr, items[i].size, items[i].node, aggs[aid - 1], items[i].t_avail, tr)) return;
     if (have && tr.t_en > t_max) {                            // line 10
       if (gcount == 0) return;
       if (!flush()) return;
       continue;
     }
-    P.clear();                                                // lines 16-18
-    add_pending(P, tr);
-    apply_pending(nw, P);
+    apply_transfer(nw, tr);                                   // lines 16-18
     if (cs.record) {
       cs.m_st.push_back(tr.t_st);
       cs.m_en.push_back(tr.t_en);
@@ -621,21 +777,33 @@ static void det_agg_tail(AggCase &cs, Net &nw, i64 t_max, const std::vector<Item
     ++i;
   }
   if (gcount > 0 && !flush()) return;
+  if (t_max > cutoff) return;
   cs.feasible = true;
   cs.total = t_max;
 }
 
 // The n-update direct prefix (Alg. 3 lines 3-7) applied to `nw`.
+// Reservations of the direct prefix already computed by Alg. 2 (OrderRes::res / sends): item i
+// of O(U) sent to the servers on the batch-start network with items 0..i-1 applied.
+struct PrefixHint {
+  const std::vector<Pending> *res = nullptr;
+  const std::vector<Send> *sends = nullptr;
+};
+
 struct Prefix {
   Net nw;
   i64 t_max = 0;
   std::vector<CommitRec> commits;
   bool ok = true;
-  explicit Prefix(const Net &n0) : nw(n0) {}
+  const PrefixHint *hint = nullptr;
+  explicit Prefix(const Net &n0, const PrefixHint *h = nullptr) : nw(n0), hint(h) {}
   void extend(const std::vector<Item> &items, int i, const Ctx &c, const std::vector<int> &dsts) {
     if (!ok) return;
     Send s;
-    if (!send_apply(nw, c, dsts, items[i].node, items[i].size, items[i].t_avail, s)) {
+    if (hint) {                                  // the same send_apply, replayed from Alg. 2
+      apply_pending(nw, (*hint->res)[i]);
+      s = (*hint->sends)[i];
+    } else if (!send_apply(nw, c, dsts, items[i].node, items[i].size, items[i].t_avail, s)) {
       ok = false;
       return;
     }
@@ -662,7 +830,7 @@ static AggCase det_agg(int n, const std::vector<Item> &items, const Net &net0, c
 // Alg. 3 lines 21-24: all |U|+1 cases, argmin total, ties -> smallest n (R14).
 static AggCase plan_aggregation(const std::vector<Item> &items, const Net &net0, const Ctx &c,
                                 const std::vector<int> &dsts, const std::vector<int> &aggs, Net *net_out,
-                                bool record = false) {
+                                bool record = false, const PrefixHint *hint = nullptr) {
   const int N = (int)items.size();
   // no aggregators: every case n < |U| meets aid = 1 > k at its first tail item (R12), so
   // only the all-direct case is feasible
@@ -675,7 +843,7 @@ static AggCase plan_aggregation(const std::vector<Item> &items, const Net &net0,
   std::vector<Prefix> starts;
   starts.reserve(tasks);
   {
-    Prefix pre(net0);
+    Prefix pre(net0, hint);
     int done = 0;
     for (int t = 0; t < tasks; ++t) {
       const int n0 = (int)((int64_t)(N + 1) * t / tasks);
@@ -686,6 +854,26 @@ static AggCase plan_aggregation(const std::vector<Item> &items, const Net &net0,
   std::atomic<bool> failed{false};
   PlanFail first_err{MLF_OK, ""};
   std::mutex err_m;
+  // Exact pruning for the argmin (ties -> smallest n): a case's total is its running t_max,
+  // which only grows, so a case (or its tail) whose t_max exceeds the best total found so far
+  // by any task cannot be the argmin; and the direct prefix's t_max is nondecreasing in n, so
+  // once it exceeds the best, every larger n of this task is pruned too.  Strict comparisons:
+  // an equal total from a smaller n must still be found.  With Alg. 2's reservations at hand
+  // the all-direct total (the largest kept t_en) seeds the bound.
+  i64 seed = T_INF;
+  if (hint && (int)hint->sends->size() == N) {
+    seed = 0;
+    for (const Send &x : *hint->sends) seed = std::max(seed, x.t_en);
+  }
+  std::atomic<i64> best_total{seed};
+  // every task keeps its best case (smallest total, then smallest n) with the network after it,
+  // so the argmin's plan needs no recomputation
+  struct Best {
+    int n = -1;
+    AggCase cs;
+    std::unique_ptr<Net> nw;
+  };
+  std::vector<Best> tbest(tasks);
   Pool::get().run(
       tasks,
       [&](int t) {
@@ -693,14 +881,39 @@ static AggCase plan_aggregation(const std::vector<Item> &items, const Net &net0,
           const int n0 = (int)((int64_t)(N + 1) * t / tasks), n1 = (int)((int64_t)(N + 1) * (t + 1) / tasks);
           if (n0 >= n1) return;
           Prefix &pre = starts[t];
+          thread_local Transfer tr;
           for (int n = n0; n < n1; ++n) {
             if (!pre.ok) break;
-            AggCase cs;
-            cs.n = n;
-            cs.commits = pre.commits;
-            Net nw = pre.nw;
-            det_agg_tail(cs, nw, pre.t_max, items, c, dsts, aggs);
-            totals[n] = cs.feasible ? cs.total : -1;
+            const i64 cut = best_total.load(std::memory_order_relaxed);
+            if (pre.t_max > cut) break;
+            // the tail's first step, read-only: with a server-bound transfer already made
+            // (n > 0) an item that cannot reach agg[0] by t_max leaves group 1 empty, and the
+            // case is infeasible (R12) — most cases end here, without copying the network
+            bool dead = false;
+            if (n > 0 && n < N) {
+              dead = !transfer(pre.nw, nullptr, nullptr, items[n].size, items[n].node, aggs[0], items[n].t_avail, tr) ||
+                     tr.t_en > pre.t_max;
+            }
+            if (!dead) {
+              AggCase cs;
+              cs.n = n;
+              cs.commits = pre.commits;
+              auto nw = std::make_unique<Net>(pre.nw);
+              det_agg_tail(cs, *nw, pre.t_max, items, c, dsts, aggs, cut);
+              totals[n] = cs.feasible ? cs.total : -1;
+              if (cs.feasible) {
+                Best &b = tbest[t];
+                if (b.n < 0 || cs.total < b.cs.total) {
+                  b.n = n;
+                  b.cs = std::move(cs);
+                  b.nw = std::move(nw);
+                }
+                i64 cur = best_total.load(std::memory_order_relaxed);
+                while (b.cs.total < cur &&
+                       !best_total.compare_exchange_weak(cur, b.cs.total, std::memory_order_relaxed)) {
+                }
+              }
+            }
             if (n < N) pre.extend(items, n, c, dsts);
           }
         } catch (const PlanFail &e) {
@@ -714,6 +927,12 @@ static AggCase plan_aggregation(const std::vector<Item> &items, const Net &net0,
   for (int n = 0; n <= N; ++n)
     if (totals[n] >= 0 && (best < 0 || totals[n] < totals[best])) best = n;
   if (best < 0) throw PlanFail{MLF_E_UNSCHEDULABLE, "no feasible aggregation case"};
+  if (!record)
+    for (auto &b : tbest)
+      if (b.n == best) {
+        if (net_out) *net_out = std::move(*b.nw);
+        return std::move(b.cs);
+      }
   return det_agg(best, items, net0, c, dsts, aggs, net_out, record);
 }
 
@@ -803,6 +1022,11 @@ static mlf_status plan_impl(const mlf_net *net, const mlf_batch *batch, const ml
     c.weights.push_back(w);
     c.wsum += w;
   }
+  auto has_dup = [](std::vector<int> v) {
+    std::sort(v.begin(), v.end());
+    return std::adjacent_find(v.begin(), v.end()) != v.end();
+  };
+  c.dup_dsts = has_dup(c.servers) || has_dup(c.replicas);
   std::vector<Item> items(n), carried(prm->n_carried);
   for (int g = 0; g < n; ++g) {
     items[g] = {batch->node[g], batch->bytes[g], batch->version[g], batch->t_avail_ns[g], batch->norm[g]};
@@ -856,7 +1080,9 @@ static mlf_status plan_impl(const mlf_net *net, const mlf_batch *batch, const ml
   // 2. aggregation on the batch-start network (R10)
   Net net0(&c.d);
   Net after(&c.d);
-  AggCase cs = plan_aggregation(ordered, net0, c, c.servers, c.aggs, &after);
+  PrefixHint hint{&ores.res, &ores.sends};
+  AggCase cs = plan_aggregation(ordered, net0, c, c.servers, c.aggs, &after, false,
+                                prm->sync_mode ? nullptr : &hint);
   std::vector<i64> times = chained_times(cs.commits);
 
   out->n_commit = (int)ores.order.size();
@@ -1033,6 +1259,11 @@ static mlf_status plan_dist_impl(const mlf_net *net, int32_t n, const int32_t *r
     if (!node_ok(prm->distributor[i])) throw PlanFail{MLF_E_INVALID, "distributor node out of range"};
     c.aggs.push_back(prm->distributor[i]);
   }
+  auto has_dup = [](std::vector<int> v) {
+    std::sort(v.begin(), v.end());
+    return std::adjacent_find(v.begin(), v.end()) != v.end();
+  };
+  c.dup_dsts = has_dup(c.servers);
   std::vector<Item> items(n);
   for (int i = 0; i < n; ++i) {
     if (!node_ok(req[i])) throw PlanFail{MLF_E_INVALID, "request node out of range"};
@@ -1061,7 +1292,7 @@ static mlf_status plan_dist_impl(const mlf_net *net, int32_t n, const int32_t *r
       auto it = ten.find(items[g].node);
       if (it == ten.end()) {
         Send s;
-        if (!send(nw, nullptr, c, c.servers, items[g].node, items[g].size, 0, s, local))
+        if (!send(nw, nullptr, c, c.servers, items[g].node, items[g].size, 0, s, local, false))
           throw PlanFail{MLF_E_UNSCHEDULABLE, "a request's path from a server is down"};
         it = ten.emplace(items[g].node, s.t_en).first;
       }
