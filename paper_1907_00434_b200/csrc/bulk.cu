@@ -303,8 +303,8 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_bulk(const __grid_co
 }
 
 // ---------------------------------------------------------------------------------------
-// Momentum (NEXT-1): Eq. 2 with gamma > 0 in its aggregate form (oracle/momentum.py
-// weighted_f32 is the pinned-order definition).  Same pipeline; each tile streams w, h and
+// Momentum (NEXT-1): Eq. 2 with gamma > 0 in its aggregate form, evaluated in the fp32 order
+// DESIGN.md R21 pins (u = -(lr*g), two left folds, then w and h).  Same pipeline; each tile streams w, h and
 // the operands; per commit c with members u_i = -(lr*g_i):
 //   A = fold(cA_i * u_i), B = fold(cB_i * u_i), w += sh*h + A, h = gm*h + B.
 __device__ __forceinline__ float4 mul4(float s, float4 x) {
@@ -717,6 +717,190 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_momentum_rr(const __
 }
 
 // ---------------------------------------------------------------------------------------
+// bf16 momentum, wide: the all-bf16 momentum pass with kCW consumer warps (16: twice the
+// warps of the kernels above) and 16 KB bf16 stages.  ncu on fused_commit_momentum_rr<4096,12,
+// true> (config 2 bf16, gamma 0.9, tau 32; profiles/r02) shows the consumers latency-bound: 2.25
+// warps per scheduler, 0.82 eligible, issue slots 57% busy, DRAM 63%.  Here a tile is kTile =
+// 8192 elements: each bf16 operand tile fills one 16 KB stage (all 12 stages carry 16 KB), the
+// fp32 w and h tiles span two stages each, and every consumer thread still folds 16 elements
+// per stage (kTile / kCW / 32), so the per-stage hand-off cost per element is unchanged while
+// the warps available to hide latency double.  Each CTA owns one contiguous range of
+// n / grid elements (multiples of 8) walked in tiles, so every CTA moves the same bytes (no
+// last-wave imbalance of round-robin 8192-element tiles: 3125 tiles over 148 CTAs = 21.1).
+// Same arithmetic, order and roundings as fused_commit_momentum_rr<., ., true>.
+template <bool kFull, int kChunks, int kCons>
+__device__ __forceinline__ void mom_fold_bf16_w(const uint8_t *st, int tid, int cnt, float lr, float ca, float cb,
+                                                float4 *A, float4 *B) {
+  const float2 nlr = make_float2(-lr, -lr), ca2 = make_float2(ca, ca), cb2 = make_float2(cb, cb);
+#pragma unroll
+  for (int k = 0; k < kChunks; ++k) {
+    const int c = tid + k * kCons;
+    if (kFull || c * 4 < cnt) {
+      const float4 g = widen_bf16x4(reinterpret_cast<const uint2 *>(st)[c]);
+      const float2 u0 = mul2(nlr, lo2(g)), u1 = mul2(nlr, hi2(g));
+      A[k] = add4(A[k], cat2(mul2(ca2, u0), mul2(ca2, u1)));
+      B[k] = add4(B[k], cat2(mul2(cb2, u0), mul2(cb2, u1)));
+    }
+  }
+}
+
+template <int kTile, int kStages, int kCW>
+__global__ void __launch_bounds__(kCW * 32 + 32, 1) fused_commit_momentum_bh(const __grid_constant__ MomentumArgs a) {
+  constexpr int kCons = kCW * 32;
+  constexpr int kStageBytes = kTile * 2;            // one bf16 operand tile
+  constexpr int kHalf = kTile / 2;                  // fp32 elements per stage
+  constexpr int kChunks = kTile / 4 / kCons;        // float4 chunks per consumer thread per tile
+  constexpr int kHalfChunks = kChunks / 2;          // ... of them in the first fp32 half-stage
+  static_assert(kChunks % 2 == 0 && kTile % (8 * kCons) == 0, "tile must split evenly");
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)kStages * kStageBytes);
+  uint64_t *empty = full + kStages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t n_bulk = a.n & ~int64_t(7);
+  const int64_t n8 = n_bulk / 8;
+  const int64_t r_begin = n8 * blockIdx.x / gridDim.x * 8, r_end = n8 * (blockIdx.x + 1) / gridDim.x * 8;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == kCW) {
+    if (lane == 0) {
+      uint32_t L = 0;
+      for (int64_t e0 = r_begin; e0 < r_end; e0 += kTile) {
+        const uint32_t cnt = (uint32_t)(r_end - e0 < kTile ? r_end - e0 : kTile);
+        for (int j = -4; j < a.n_ops; ++j, ++L) {   // -4, -3: the halves of w; -2, -1: of h
+          const uint32_t s = L % kStages;
+          if (L >= (uint32_t)kStages) {
+            mbar_wait(&empty[s], ((L / kStages) & 1) ^ 1);
+            fence_proxy_async_smem();
+          }
+          const void *src;
+          uint32_t bytes;
+          if (j < 0) {
+            const uint32_t h0 = (j & 1) ? (uint32_t)kHalf : 0u;        // -3, -1: second half
+            const uint32_t h = cnt > h0 ? (cnt - h0 < (uint32_t)kHalf ? cnt - h0 : (uint32_t)kHalf) : 0u;
+            src = (j < -2 ? a.w : a.h) + e0 + h0;
+            bytes = h * 4;
+          } else {
+            src = static_cast<const uint16_t *>(a.op[j]) + a.src_off + e0;
+            bytes = cnt * 2;
+          }
+          mbar_expect_tx(&full[s], bytes);
+          if (bytes) bulk_g2s(smem + (size_t)s * kStageBytes, src, bytes, &full[s]);
+        }
+      }
+    }
+    return;
+  }
+  const int tid = threadIdx.x;
+  uint32_t L = 0;
+  for (int64_t e0 = r_begin; e0 < r_end; e0 += kTile) {
+    const int cnt = (int)(r_end - e0 < kTile ? r_end - e0 : kTile);
+    const bool full_tile = cnt == kTile;
+    float4 w[kChunks], h[kChunks], A[kChunks], B[kChunks];
+#pragma unroll
+    for (int k = 0; k < kChunks; ++k) A[k] = B[k] = kNegZero4;
+    // w and h: two half-stages each; chunk k lives in the first half iff k < kHalfChunks
+#pragma unroll
+    for (int which = 0; which < 4; ++which) {
+      const uint32_t s = L % kStages;
+      mbar_wait(&full[s], (L / kStages) & 1);
+      const float4 *sp = reinterpret_cast<const float4 *>(smem + (size_t)s * kStageBytes);
+      const int k0 = (which & 1) ? kHalfChunks : 0;
+#pragma unroll
+      for (int kk = 0; kk < kHalfChunks; ++kk) {
+        const int k = k0 + kk;
+        const int c = tid + k * kCons;
+        if (c * 4 < cnt) (which < 2 ? w[k] : h[k]) = sp[c - ((which & 1) ? kHalf / 4 : 0)];
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      ++L;
+    }
+    if (a.backup_after == -1) {
+#pragma unroll
+      for (int k = 0; k < kChunks; ++k) {
+        const int c = tid + k * kCons;
+        if (c * 4 < cnt) {
+          __stcs(reinterpret_cast<float4 *>(a.backup + e0) + c, w[k]);
+          __stcs(reinterpret_cast<float4 *>(a.backup_h + e0) + c, h[k]);
+        }
+      }
+    }
+    for (int j = 0; j < a.n_ops; ++j, ++L) {
+      const uint32_t s = L % kStages;
+      const uint8_t f = a.flag[j];
+      const float ca = a.cA[j], cb = a.cB[j];
+      mbar_wait(&full[s], (L / kStages) & 1);
+      const uint8_t *st = smem + (size_t)s * kStageBytes;
+      if (full_tile) mom_fold_bf16_w<true, kChunks, kCons>(st, tid, cnt, a.lr, ca, cb, A, B);
+      else mom_fold_bf16_w<false, kChunks, kCons>(st, tid, cnt, a.lr, ca, cb, A, B);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (f & kOpLast) {
+        const float sh = a.sh[j], gm = a.gm[j];
+#pragma unroll
+        for (int k = 0; k < kChunks; ++k) {
+          w[k] = add4(w[k], add4(mul4(sh, h[k]), A[k]));
+          h[k] = add4(mul4(gm, h[k]), B[k]);
+          A[k] = B[k] = kNegZero4;                    // the next commit's fold starts at -0
+        }
+        if (j == a.backup_after) {
+#pragma unroll
+          for (int k = 0; k < kChunks; ++k) {
+            const int c = tid + k * kCons;
+            if (c * 4 < cnt) {
+              __stcs(reinterpret_cast<float4 *>(a.backup + e0) + c, w[k]);
+              __stcs(reinterpret_cast<float4 *>(a.backup_h + e0) + c, h[k]);
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kChunks; ++k) {
+      const int c = tid + k * kCons;
+      if (c * 4 < cnt) {
+        __stcs(reinterpret_cast<float4 *>(a.w + e0) + c, w[k]);
+        __stcs(reinterpret_cast<float4 *>(a.h + e0) + c, h[k]);
+      }
+    }
+  }
+  // ragged tail (< 8 elements) on CTA 0
+  const int64_t tail = a.n - n_bulk;
+  if (blockIdx.x == 0 && tid < tail) {
+    const int64_t e = n_bulk + tid;
+    float wv = a.w[e], hv = a.h[e], Av = 0.f, Bv = 0.f;
+    if (a.backup_after == -1) {
+      a.backup[e] = wv;
+      a.backup_h[e] = hv;
+    }
+    for (int j = 0; j < a.n_ops; ++j) {
+      const uint8_t f = a.flag[j];
+      const float g = __uint_as_float(uint32_t(static_cast<const uint16_t *>(a.op[j])[a.src_off + e]) << 16);
+      const float u = -__fmul_rn(a.lr, g);
+      const float pa = __fmul_rn(a.cA[j], u), pb = __fmul_rn(a.cB[j], u);
+      Av = (f & kOpFirst) ? pa : __fadd_rn(Av, pa);
+      Bv = (f & kOpFirst) ? pb : __fadd_rn(Bv, pb);
+      if (f & kOpLast) {
+        wv = __fadd_rn(wv, __fadd_rn(__fmul_rn(a.sh[j], hv), Av));
+        hv = __fadd_rn(__fmul_rn(a.gm[j], hv), Bv);
+        if (j == a.backup_after) {
+          a.backup[e] = wv;
+          a.backup_h[e] = hv;
+        }
+      }
+    }
+    a.w[e] = wv;
+    a.h[e] = hv;
+  }
+}
+
+// ---------------------------------------------------------------------------------------
 // The same commit for bf16 operands with 16 KB bulk copies: a tile is kTile = 8192
 // elements, so every bf16 operand tile fills one 16 KB stage and the fp32 w tile spans two.
 // With the fp32 layout (4096-element tiles) bf16 copies are 8 KB and the per-stage hand-off
@@ -1052,6 +1236,19 @@ static cudaError_t launch_momentum_t(const MomentumArgs &a, cudaStream_t s, int 
 cudaError_t launch_commit_momentum(const MomentumArgs &a, cudaStream_t s, int sm_count) {
   bool all_bf16 = a.n_ops > 0;
   for (int j = 0; j < a.n_ops && all_bf16; ++j) all_bf16 = (a.flag[j] & kOpBf16) != 0;
+  const char *wide = getenv("MLF_MOM_WIDE");           // 0: the 8-warp kernels (A/B experiments)
+  if (all_bf16 && !(wide && atoi(wide) == 0)) {
+    constexpr int kT = 8192, kS = 12, kCW = 16;
+    constexpr size_t smem = (size_t)kS * kT * 2 + 2 * kS * sizeof(uint64_t);
+    static std::atomic<uint64_t> init{0};
+    if (cudaError_t e = ensure_smem(bulk::fused_commit_momentum_bh<kT, kS, kCW>, smem, init); e != cudaSuccess)
+      return e;
+    const int64_t n_tiles = ((a.n & ~int64_t(7)) + kT - 1) / kT;
+    const int sms = sm_count > 0 ? sm_count : 148;
+    const int grid = (int)(n_tiles < sms ? (n_tiles > 0 ? n_tiles : 1) : sms);
+    bulk::fused_commit_momentum_bh<kT, kS, kCW><<<grid, kCW * 32 + 32, smem, s>>>(a);
+    return cudaGetLastError();
+  }
   return all_bf16 ? launch_momentum_t<true>(a, s, sm_count) : launch_momentum_t<false>(a, s, sm_count);
 }
 

@@ -124,7 +124,10 @@ __global__ void __launch_bounds__(32, 1) bulk_copy_kernel(const __grid_constant_
     const int64_t rest = a.bytes[j] - off;
     len = (uint32_t)(rest < kChunk ? rest : kChunk);
   };
-  // issue loads for up to kStages chunks, then per chunk: wait load, store it, refill the stage
+  // issue loads for up to kStages chunks, then per chunk: wait load, store it; the stage of the
+  // store issued kLag chunks earlier is refilled once that store has read it (wait_group.read
+  // kLag), so kLag stores and kStages - kLag loads stay in flight
+  constexpr uint32_t kLag = 4;
   int64_t i_load = next(0), i_store = i_load;
   uint32_t L = 0, S = 0;
   auto issue_load = [&](int64_t i, uint32_t stage) {
@@ -155,10 +158,10 @@ __global__ void __launch_bounds__(32, 1) bulk_copy_kernel(const __grid_constant_
                  "r"(saddr(sm + (size_t)stage * kChunk)), "r"(len)
                  : "memory");
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-    if (i_load < rounds) {
-      // the stage is refilled only after its bulk store has read it
-      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-      issue_load(i_load, stage);
+    if (S >= kLag && i_load < rounds) {
+      // at most kLag store groups still reading: the store of chunk S - kLag has read its stage
+      asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kLag) : "memory");
+      issue_load(i_load, L % kStages);           // L % kStages == (S - kLag) % kStages
       i_load = next(i_load + 1);
       ++L;
     }
