@@ -349,6 +349,23 @@ __device__ __forceinline__ void mom_fold_bf16(const uint8_t *st, int tid, int cn
   }
 }
 
+// a kOpSingle commit (see kernels.h): u = -(lr*g); h = gm*h + u; w = w + h, the same roundings
+// as the weighted-sum form of a one-member commit
+template <bool kFull, int kChunks, int kCons>
+__device__ __forceinline__ void mom_single(const uint8_t *st, bool bf, int tid, int cnt, float lr, float gm,
+                                           float4 *w, float4 *h) {
+#pragma unroll
+  for (int k = 0; k < kChunks; ++k) {
+    const int c = tid + k * kCons;
+    if (kFull || c * 4 < cnt) {
+      const float4 g = bf ? widen_bf16x4(reinterpret_cast<const uint2 *>(st)[c]) : reinterpret_cast<const float4 *>(st)[c];
+      const float4 u = cat2(mul2(make_float2(-lr, -lr), lo2(g)), mul2(make_float2(-lr, -lr), hi2(g)));
+      h[k] = add4(mul4(gm, h[k]), u);
+      w[k] = add4(w[k], h[k]);
+    }
+  }
+}
+
 template <int kTile, int kStages, bool kBf>
 __global__ void __launch_bounds__(kThreads, 1) fused_commit_momentum(const __grid_constant__ MomentumArgs a) {
   constexpr int kStageBytes = kTile * 4;
@@ -462,7 +479,11 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_momentum(const __gri
       const float ca = a.cA[j], cb = a.cB[j];
       mbar_wait(&full[s], (L / kStages) & 1);
       const uint8_t *st = smem + (size_t)s * kStageBytes;
-      if constexpr (kBf) {
+      const bool single = f & kOpSingle;
+      if (single) {
+        if (full_tile) mom_single<true, kChunks, kConsumers>(st, f & kOpBf16, tid, cnt, a.lr, a.gm[j], w, h);
+        else mom_single<false, kChunks, kConsumers>(st, f & kOpBf16, tid, cnt, a.lr, a.gm[j], w, h);
+      } else if constexpr (kBf) {
         if (full_tile) mom_fold_bf16<true, kChunks>(st, tid, cnt, a.lr, ca, cb, A, B);
         else mom_fold_bf16<false, kChunks>(st, tid, cnt, a.lr, ca, cb, A, B);
       } else {
@@ -481,7 +502,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_momentum(const __gri
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
-      if (f & kOpLast) {
+      if ((f & kOpLast) && !single) {
         const float sh = a.sh[j], gm = a.gm[j];
 #pragma unroll
         for (int k = 0; k < kChunks; ++k) {
@@ -489,14 +510,14 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_momentum(const __gri
           h[k] = add4(mul4(gm, h[k]), B[k]);
           if constexpr (kBf) A[k] = B[k] = kNegZero4;  // the next commit's fold starts at -0
         }
-        if (j == a.backup_after) {
+      }
+      if (j == a.backup_after) {
 #pragma unroll
-          for (int k = 0; k < kChunks; ++k) {
-            const int c = tid + k * kConsumers;
-            if (c * 4 < cnt) {
-              __stcs(reinterpret_cast<float4 *>(a.backup + e0) + c, w[k]);
-              __stcs(reinterpret_cast<float4 *>(a.backup_h + e0) + c, h[k]);
-            }
+        for (int k = 0; k < kChunks; ++k) {
+          const int c = tid + k * kConsumers;
+          if (c * 4 < cnt) {
+            __stcs(reinterpret_cast<float4 *>(a.backup + e0) + c, w[k]);
+            __stcs(reinterpret_cast<float4 *>(a.backup_h + e0) + c, h[k]);
           }
         }
       }
@@ -636,7 +657,11 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_momentum_rr(const __
       const float ca = a.cA[j], cb = a.cB[j];
       mbar_wait(&full[s], (L / kStages) & 1);
       const uint8_t *st = smem + (size_t)s * kStageBytes;
-      if constexpr (kBf) {
+      const bool single = f & kOpSingle;
+      if (single) {
+        if (full_tile) mom_single<true, kChunks, kConsumers>(st, f & kOpBf16, tid, cnt, a.lr, a.gm[j], w, h);
+        else mom_single<false, kChunks, kConsumers>(st, f & kOpBf16, tid, cnt, a.lr, a.gm[j], w, h);
+      } else if constexpr (kBf) {
         if (full_tile) mom_fold_bf16<true, kChunks>(st, tid, cnt, a.lr, ca, cb, A, B);
         else mom_fold_bf16<false, kChunks>(st, tid, cnt, a.lr, ca, cb, A, B);
       } else {
@@ -655,7 +680,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_momentum_rr(const __
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
-      if (f & kOpLast) {
+      if ((f & kOpLast) && !single) {
         const float sh = a.sh[j], gm = a.gm[j];
 #pragma unroll
         for (int k = 0; k < kChunks; ++k) {
@@ -663,14 +688,14 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_momentum_rr(const __
           h[k] = add4(mul4(gm, h[k]), B[k]);
           if constexpr (kBf) A[k] = B[k] = kNegZero4;  // the next commit's fold starts at -0
         }
-        if (j == a.backup_after) {
+      }
+      if (j == a.backup_after) {
 #pragma unroll
-          for (int k = 0; k < kChunks; ++k) {
-            const int c = tid + k * kConsumers;
-            if (c * 4 < cnt) {
-              __stcs(reinterpret_cast<float4 *>(a.backup + e0) + c, w[k]);
-              __stcs(reinterpret_cast<float4 *>(a.backup_h + e0) + c, h[k]);
-            }
+        for (int k = 0; k < kChunks; ++k) {
+          const int c = tid + k * kConsumers;
+          if (c * 4 < cnt) {
+            __stcs(reinterpret_cast<float4 *>(a.backup + e0) + c, w[k]);
+            __stcs(reinterpret_cast<float4 *>(a.backup_h + e0) + c, h[k]);
           }
         }
       }
@@ -837,11 +862,18 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) fused_commit_momentum_bh(con
       const float ca = a.cA[j], cb = a.cB[j];
       mbar_wait(&full[s], (L / kStages) & 1);
       const uint8_t *st = smem + (size_t)s * kStageBytes;
-      if (full_tile) mom_fold_bf16_w<true, kChunks, kCons>(st, tid, cnt, a.lr, ca, cb, A, B);
-      else mom_fold_bf16_w<false, kChunks, kCons>(st, tid, cnt, a.lr, ca, cb, A, B);
+      const bool single = f & kOpSingle;
+      if (single) {
+        if (full_tile) mom_single<true, kChunks, kCons>(st, true, tid, cnt, a.lr, a.gm[j], w, h);
+        else mom_single<false, kChunks, kCons>(st, true, tid, cnt, a.lr, a.gm[j], w, h);
+      } else if (full_tile) {
+        mom_fold_bf16_w<true, kChunks, kCons>(st, tid, cnt, a.lr, ca, cb, A, B);
+      } else {
+        mom_fold_bf16_w<false, kChunks, kCons>(st, tid, cnt, a.lr, ca, cb, A, B);
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
-      if (f & kOpLast) {
+      if ((f & kOpLast) && !single) {
         const float sh = a.sh[j], gm = a.gm[j];
 #pragma unroll
         for (int k = 0; k < kChunks; ++k) {
@@ -849,14 +881,14 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) fused_commit_momentum_bh(con
           h[k] = add4(mul4(gm, h[k]), B[k]);
           A[k] = B[k] = kNegZero4;                    // the next commit's fold starts at -0
         }
-        if (j == a.backup_after) {
+      }
+      if (j == a.backup_after) {
 #pragma unroll
-          for (int k = 0; k < kChunks; ++k) {
-            const int c = tid + k * kCons;
-            if (c * 4 < cnt) {
-              __stcs(reinterpret_cast<float4 *>(a.backup + e0) + c, w[k]);
-              __stcs(reinterpret_cast<float4 *>(a.backup_h + e0) + c, h[k]);
-            }
+        for (int k = 0; k < kChunks; ++k) {
+          const int c = tid + k * kCons;
+          if (c * 4 < cnt) {
+            __stcs(reinterpret_cast<float4 *>(a.backup + e0) + c, w[k]);
+            __stcs(reinterpret_cast<float4 *>(a.backup_h + e0) + c, h[k]);
           }
         }
       }

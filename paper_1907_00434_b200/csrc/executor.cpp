@@ -523,6 +523,7 @@ static void launch_momentum(mlf_ctx *c, const mlf_plan_out *p, const std::vector
         a.cB[o] = (float)pw[m - i];
         a.sh[o] = (float)sh;
         a.gm[o] = (float)pw[m];
+        if (m == 1 && a.cA[o] == 1.f && a.cB[o] == 1.f && a.sh[o] == a.gm[o]) a.flag[o] |= kOpSingle;
       }
       if (boundary > 0 && ci == boundary) a.backup_after = (int32_t)(e - 1 - i0);
       q = e;

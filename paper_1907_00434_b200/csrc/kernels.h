@@ -16,6 +16,11 @@ constexpr int kMaxBcast = 8;
 constexpr uint8_t kOpFirst = 1;   // first member of its commit: x = u (not x += u)
 constexpr uint8_t kOpLast = 2;    // last member of its commit: w <- w - lr*x after it
 constexpr uint8_t kOpBf16 = 4;    // operand is bf16 (widened exactly), else fp32
+// momentum only: a one-member commit whose weights are cA = cB = 1 and sh = gm (every m = 1
+// commit: cA = g^0, cB = g^0, sh = gm = g).  Its two weighted sums reduce exactly to
+// h' = gm*h + u, w' = w + h' (1*u == u and -0 + u == u bitwise), which the kernels evaluate
+// directly: one product and two sums per element instead of five products and four sums.
+constexpr uint8_t kOpSingle = 8;
 
 // The fused reduce + scale + apply (+ mirror store) pass over one shard slice.
 // Dynamic shared memory above 48 KB must be opted into per kernel and per device.  One bit

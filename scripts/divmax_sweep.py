@@ -21,8 +21,8 @@ from paper_1907_00434_b200 import mlfabric as m  # noqa: E402
 from synthgen import configs  # noqa: E402
 
 
-def run(div_max: float, batches: int, tau: int):
-    cfg = configs.config(2, tau=tau, with_replica=True, replica_mode=1, div_max=div_max)
+def run(div_max: float, batches: int, tau: int, kr: int):
+    cfg = configs.config(2, tau=tau, with_replica=True, replica_mode=1, div_max=div_max, replica_aggs=kr)
     S_bytes = cfg["S"] * cfg["e"]
     carried, v, vp = [], 0, 0
     rbytes = commits = 0
@@ -42,8 +42,9 @@ def run(div_max: float, batches: int, tau: int):
         commits += p["n_commit"]
         vp, v = v, v + p["n_commit"]
     per_update = rbytes / (commits * S_bytes)
-    return {"div_max": div_max, "replica_bytes_per_update": round(per_update, 4),
-            "savings_vs_unaggregated": round(1.0 / per_update, 3), "max_lead": lead_max}
+    return {"k_replica_aggs": kr, "div_max": div_max, "replica_bytes_per_update": round(per_update, 4),
+            "savings_vs_unaggregated": round(1.0 / per_update, 3), "max_lead": lead_max,
+            "final_lead": len(carried)}
 
 
 def main():
@@ -51,12 +52,14 @@ def main():
     ap.add_argument("--batches", type=int, default=40)
     ap.add_argument("--tau", type=int, default=32)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--kr", type=int, nargs="+", default=[8, 4], help="replica aggregators k' (P:1178-1179)")
     a = ap.parse_args()
-    rows = [run(d, a.batches, a.tau) for d in (0.0, 1.0, 2.0, 4.0, 8.0, 16.0, 30.0, 60.0, 120.0, 600.0)]
+    rows = [run(d, a.batches, a.tau, kr) for kr in a.kr
+            for d in (0.0, 1.0, 2.0, 4.0, 8.0, 16.0, 30.0, 60.0, 120.0, 300.0, 600.0)]
     for r in rows:
         print(json.dumps(r))
     if a.out:
-        json.dump({"experiment": "replica bytes vs Div_max (Fig. 11 analogue), config 2 + replica, "
+        json.dump({"experiment": "replica bytes vs Div_max (Fig. 11 analogue), config 2 + replica, k' in " + str(a.kr) + ", "
                                  f"{a.batches} batches, tau {a.tau}, count-based Div_max", "rows": rows},
                   open(a.out, "w"), indent=1)
 

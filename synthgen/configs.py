@@ -37,19 +37,23 @@ def shard_bounds(S: int, G: int, align: int = 64):
 def config(cid: int, *, G: int | None = None, tau: int | None = None, dtype: str = "f32",
            seed: int = SEED_ROOT, scale_S: int | None = None, gamma: float = 0.0,
            replica_mode: int = 0, div_max: float | None = None, with_replica: bool = False,
-           workers: int | None = None) -> dict:
+           workers: int | None = None, replica_aggs: int = 8) -> dict:
     """replica_mode 0 = mirror (R16), 1 = replica trees (NEXT-2).  with_replica adds a replica
-    to config 2 (a replica server with a 10 Gb/s ingress and 4 replica aggregators).
-    `workers` shrinks the worker count of configs 3-5 (tests whose oracle plans must be fast)."""
+    to config 2: a replica server with a 10 Gb/s ingress and k' = replica_aggs replica
+    aggregators (P:1178-1179 "a separate k' aggregators are earmarked for the replica"; the
+    paper gives no k'.  8 is the smallest k' with which the replica keeps pace with the server
+    on this workload: with k' = 4 the replica's lead grows to Div_max for every Div_max >= 16,
+    DESIGN.md "NEXT-2").  `workers` shrinks the worker count of configs 3-5 (tests whose
+    oracle plans must be fast)."""
     d = _config(cid, G=G, tau=tau, dtype=dtype, seed=seed, scale_S=scale_S, gamma=gamma,
-                with_replica=with_replica, workers=workers)
+                with_replica=with_replica, workers=workers, replica_aggs=replica_aggs)
     d["replica_mode"] = replica_mode
     if div_max is not None:
         d["div_max"] = div_max
     return d
 
 
-def _config(cid: int, *, G, tau, dtype, seed, scale_S, gamma, with_replica, workers) -> dict:
+def _config(cid: int, *, G, tau, dtype, seed, scale_S, gamma, with_replica, workers, replica_aggs=8) -> dict:
     """Static part of config `cid` (1..5)."""
     if cid == 1:
         W, S, G = 4, 1 << 20, 1
@@ -93,12 +97,12 @@ def _config(cid: int, *, G, tau, dtype, seed, scale_S, gamma, with_replica, work
         d["tau"] = 4 if tau is None else tau
         d["replan_rates"] = True
         if with_replica:
-            # a replica server on its own 10 Gb/s machine with k' = 4 replica
-            # aggregators earmarked among the workers
+            # a replica server on its own 10 Gb/s machine with k' replica
+            # aggregators earmarked among the workers, disjoint from the server's
             n = W + 2
             d["replica"] = True
             d["replicas"] = [W + 1]
-            d["raggs"] = perm[4:8]
+            d["raggs"] = perm[4:4 + replica_aggs]
             d["replica_rate"] = 10 * GBPS
     else:
         # box model: planner node g = GPU g.  Its NIC up/down = NVLink egress/ingress per

@@ -85,8 +85,8 @@ def test_momentum_config2_every_element_vs_sequential_eq2(dtype):
     plans = []
     for it in range(2):
         pb, pd, draws = wl.step(it)
+        wl.ctx.sync()
         plans.append(pd)
-    wl.ctx.sync()
     w_gpu = wl.w.cpu().numpy()
     h_gpu = wl.h.cpu().numpy()
     wl.ctx.close()

@@ -472,6 +472,33 @@ def test_invalid_plan_rejected_without_device_work():
     ctx.close()
 
 
+def test_executor_rejects_a_plan_beyond_the_delay_bound():
+    """registerAsServer(tau_max) (Table 1): the executor re-checks (v + p) - v(g) <= tau_max for
+    every committed update (R1) and rejects a stale plan before any device work."""
+    dev = torch.device("cuda", 0)
+    S = 64
+    slots = [torch.ones(S, device=dev) for _ in range(3)]
+    wt = torch.zeros(S, device=dev)
+    ctx = m.Context(device=0, model_shard=wt, update_slots=slots, lr=1.0, model_elems=S, v0=10, tau_max=3,
+                    stream=torch.cuda.current_stream().cuda_stream)
+    for g, v in enumerate([10, 8, 10]):
+        ctx.submit(g, v)
+    # positions 1, 2, 3 commit versions 11, 12, 13: update 1 (v = 8) at position 2 has delay 4 > 3
+    stale = {"n_commit": 3, "order": [0, 1, 2], "drop_reason": [0, 0, 0], "group": [0, 0, 0], "n_direct": 3,
+             "n_groups": 0, "group_node": [], "n_server_commits": 3, "commit_first": [0, 1, 2],
+             "commit_count": [1, 1, 1], "replica_boundary_commit": -1}
+    with pytest.raises(m.MlfError) as e:
+        ctx.execute(m.plan_from_dict(stale))
+    assert e.value.code == m.MLF_E_INVALID and "tau_max" in str(e.value)
+    assert ctx.stats()[0] == 0 and torch.all(wt == 0)
+    # update 1 first: delays 3, 2, 3 are all within the bound
+    ok = dict(stale, order=[1, 0, 2])
+    ctx.execute(m.plan_from_dict(ok))
+    ctx.sync()
+    assert ctx.version() == 13 and torch.all(wt == -3)
+    ctx.close()
+
+
 @pytest.mark.parametrize("it_count", [3])
 def test_config1_end_to_end_vs_oracle(it_count):
     os.environ["MLF_COMMIT_IMPL"] = "ldg"
@@ -509,9 +536,17 @@ def test_config2_full_size_sampled(tau, dtype, impl):
     dt = sg.DTYPE_BF16 if dtype == "bf16" else sg.DTYPE_F32
     w_ref = sg.w0_values(cfg["seed"], idx)
     for it in range(2):
+        v_init = wl.v_init
         pb, pd, draws = wl.step(it)
         wl.ctx.sync()
-        w_ref, _, _ = execute_plan(w_ref, pd, lambda g: sg.update_values(cfg["seed"], g, it, idx, dt), cfg["lr"])
+        # the plan the GPU executed is the oracle's plan of the same inputs
+        up, down, site = configs.network(cfg, it)
+        batch = [Item(cfg["worker_node"][g], S * cfg["e"], d["version"], d["t_avail"], d["norm"])
+                 for g, d in enumerate(draws)]
+        op = oracle_plan(make_net(cfg["n_nodes"], up, down, None, site), batch,
+                         Params(servers=cfg["servers"], aggs=cfg["aggs"], v_init=v_init, tau_max=cfg["tau"]))
+        assert op == pd, it
+        w_ref, _, _ = execute_plan(w_ref, op, lambda g: sg.update_values(cfg["seed"], g, it, idx, dt), cfg["lr"])
         got = wl.w.cpu().numpy()[idx]
         assert np.array_equal(bits(got), bits(w_ref))
         assert pd["n_commit"] == min(tau, 32)
