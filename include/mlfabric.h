@@ -341,8 +341,12 @@ mlf_status mlf_execute(mlf_ctx *ctx, const mlf_plan_out *plan);
 #define MLF_PHASE_COMMIT 2
 mlf_status mlf_execute_phase(mlf_ctx *ctx, const mlf_plan_out *plan, int32_t phase);
 
-/* Wait for the last execute; *device_ms (may be NULL) = CUDA-event time from its
- * first to its last kernel on this device.  Releases the batch's slots. */
+/* Wait for the last execute; *device_ms (may be NULL) = CUDA-event time on cfg.stream from the
+ * first device operation of that execute to its last.  With host-resident updates on one GPU
+ * (the mlf_set_pull_host / mlf_set_update_host pipeline) the H2D copies run on a separate copy
+ * stream and may start before the window opens, overlapping the previous batch; device_ms then
+ * covers the compute stream only, and end-to-end rates are taken by wall time.  Releases the
+ * batch's slots. */
 mlf_status mlf_sync(mlf_ctx *ctx, float *device_ms);
 
 /* Slots are released per executed batch as soon as that batch's device work has finished
@@ -438,6 +442,9 @@ mlf_status mlf_copy_kernel(int32_t device, void *dst, const void *src, int64_t b
 mlf_status mlf_copy_engine(int32_t device, void *dst, const void *src, int64_t bytes, void *stream);
 /* The same copy with TMA bulk copies only (global -> shared -> global, 16 KB chunks). */
 mlf_status mlf_copy_bulk(int32_t device, void *dst, const void *src, int64_t bytes, void *stream);
+/* Read-only probe: stream `bytes` of src into shared memory with TMA bulk copies, write nothing
+ * (the read end of bench.py's mixed read/write HBM ceiling).  src and bytes 16-byte aligned. */
+mlf_status mlf_read_probe(int32_t device, const void *src, int64_t bytes, void *stream);
 
 #ifdef __cplusplus
 }

@@ -479,10 +479,12 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_momentum(const __gri
       const float ca = a.cA[j], cb = a.cB[j];
       mbar_wait(&full[s], (L / kStages) & 1);
       const uint8_t *st = smem + (size_t)s * kStageBytes;
-      const bool single = f & kOpSingle;
+      // the one-member fast path only in the all-bf16 (consumer-bound) instantiation: in the
+      // generic one its extra code measured 13% slower at config 2 fp32 tau 32 (profiles/r02)
+      const bool single = kBf && (f & kOpSingle);
       if (single) {
-        if (full_tile) mom_single<true, kChunks, kConsumers>(st, f & kOpBf16, tid, cnt, a.lr, a.gm[j], w, h);
-        else mom_single<false, kChunks, kConsumers>(st, f & kOpBf16, tid, cnt, a.lr, a.gm[j], w, h);
+        if (full_tile) mom_single<true, kChunks, kConsumers>(st, true, tid, cnt, a.lr, a.gm[j], w, h);
+        else mom_single<false, kChunks, kConsumers>(st, true, tid, cnt, a.lr, a.gm[j], w, h);
       } else if constexpr (kBf) {
         if (full_tile) mom_fold_bf16<true, kChunks>(st, tid, cnt, a.lr, ca, cb, A, B);
         else mom_fold_bf16<false, kChunks>(st, tid, cnt, a.lr, ca, cb, A, B);
@@ -510,14 +512,28 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_momentum(const __gri
           h[k] = add4(mul4(gm, h[k]), B[k]);
           if constexpr (kBf) A[k] = B[k] = kNegZero4;  // the next commit's fold starts at -0
         }
-      }
-      if (j == a.backup_after) {
+        if constexpr (!kBf) {
+          if (j == a.backup_after) {
 #pragma unroll
-        for (int k = 0; k < kChunks; ++k) {
-          const int c = tid + k * kConsumers;
-          if (c * 4 < cnt) {
-            __stcs(reinterpret_cast<float4 *>(a.backup + e0) + c, w[k]);
-            __stcs(reinterpret_cast<float4 *>(a.backup_h + e0) + c, h[k]);
+            for (int k = 0; k < kChunks; ++k) {
+              const int c = tid + k * kConsumers;
+              if (c * 4 < cnt) {
+                __stcs(reinterpret_cast<float4 *>(a.backup + e0) + c, w[k]);
+                __stcs(reinterpret_cast<float4 *>(a.backup_h + e0) + c, h[k]);
+              }
+            }
+          }
+        }
+      }
+      if constexpr (kBf) {
+        if (j == a.backup_after) {
+#pragma unroll
+          for (int k = 0; k < kChunks; ++k) {
+            const int c = tid + k * kConsumers;
+            if (c * 4 < cnt) {
+              __stcs(reinterpret_cast<float4 *>(a.backup + e0) + c, w[k]);
+              __stcs(reinterpret_cast<float4 *>(a.backup_h + e0) + c, h[k]);
+            }
           }
         }
       }
@@ -657,10 +673,12 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_momentum_rr(const __
       const float ca = a.cA[j], cb = a.cB[j];
       mbar_wait(&full[s], (L / kStages) & 1);
       const uint8_t *st = smem + (size_t)s * kStageBytes;
-      const bool single = f & kOpSingle;
+      // the one-member fast path only in the all-bf16 (consumer-bound) instantiation: in the
+      // generic one its extra code measured 13% slower at config 2 fp32 tau 32 (profiles/r02)
+      const bool single = kBf && (f & kOpSingle);
       if (single) {
-        if (full_tile) mom_single<true, kChunks, kConsumers>(st, f & kOpBf16, tid, cnt, a.lr, a.gm[j], w, h);
-        else mom_single<false, kChunks, kConsumers>(st, f & kOpBf16, tid, cnt, a.lr, a.gm[j], w, h);
+        if (full_tile) mom_single<true, kChunks, kConsumers>(st, true, tid, cnt, a.lr, a.gm[j], w, h);
+        else mom_single<false, kChunks, kConsumers>(st, true, tid, cnt, a.lr, a.gm[j], w, h);
       } else if constexpr (kBf) {
         if (full_tile) mom_fold_bf16<true, kChunks>(st, tid, cnt, a.lr, ca, cb, A, B);
         else mom_fold_bf16<false, kChunks>(st, tid, cnt, a.lr, ca, cb, A, B);
@@ -688,14 +706,28 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_momentum_rr(const __
           h[k] = add4(mul4(gm, h[k]), B[k]);
           if constexpr (kBf) A[k] = B[k] = kNegZero4;  // the next commit's fold starts at -0
         }
-      }
-      if (j == a.backup_after) {
+        if constexpr (!kBf) {
+          if (j == a.backup_after) {
 #pragma unroll
-        for (int k = 0; k < kChunks; ++k) {
-          const int c = tid + k * kConsumers;
-          if (c * 4 < cnt) {
-            __stcs(reinterpret_cast<float4 *>(a.backup + e0) + c, w[k]);
-            __stcs(reinterpret_cast<float4 *>(a.backup_h + e0) + c, h[k]);
+            for (int k = 0; k < kChunks; ++k) {
+              const int c = tid + k * kConsumers;
+              if (c * 4 < cnt) {
+                __stcs(reinterpret_cast<float4 *>(a.backup + e0) + c, w[k]);
+                __stcs(reinterpret_cast<float4 *>(a.backup_h + e0) + c, h[k]);
+              }
+            }
+          }
+        }
+      }
+      if constexpr (kBf) {
+        if (j == a.backup_after) {
+#pragma unroll
+          for (int k = 0; k < kChunks; ++k) {
+            const int c = tid + k * kConsumers;
+            if (c * 4 < cnt) {
+              __stcs(reinterpret_cast<float4 *>(a.backup + e0) + c, w[k]);
+              __stcs(reinterpret_cast<float4 *>(a.backup_h + e0) + c, h[k]);
+            }
           }
         }
       }
@@ -1268,8 +1300,10 @@ static cudaError_t launch_momentum_t(const MomentumArgs &a, cudaStream_t s, int 
 cudaError_t launch_commit_momentum(const MomentumArgs &a, cudaStream_t s, int sm_count) {
   bool all_bf16 = a.n_ops > 0;
   for (int j = 0; j < a.n_ops && all_bf16; ++j) all_bf16 = (a.flag[j] & kOpBf16) != 0;
-  const char *wide = getenv("MLF_MOM_WIDE");           // 0: the 8-warp kernels (A/B experiments)
-  if (all_bf16 && !(wide && atoi(wide) == 0)) {
+  // the 16-warp kernel for all-bf16 lists of >= MLF_MOM_WIDE operands (0: never)
+  const char *wide = getenv("MLF_MOM_WIDE");
+  const int wide_min = wide ? atoi(wide) : 6;
+  if (all_bf16 && wide_min > 0 && a.n_ops >= wide_min) {
     constexpr int kT = 8192, kS = 12, kCW = 16;
     constexpr size_t smem = (size_t)kS * kT * 2 + 2 * kS * sizeof(uint64_t);
     static std::atomic<uint64_t> init{0};

@@ -484,6 +484,8 @@ struct CommitOp {
 // float64 powers of the double gamma summed left to right, each rounded once to fp32 (R21).
 static void launch_momentum(mlf_ctx *c, const mlf_plan_out *p, const std::vector<CommitOp> &ops, int boundary) {
   const double g = c->cfg.gamma;
+  const char *se = getenv("MLF_MOM_SINGLE");            // 0: no one-member fast path (A/B experiments)
+  const bool single_ok = !(se && atoi(se) == 0);
   size_t i0 = 0;
   bool first_launch = true;
   while (i0 < ops.size() || (first_launch && c->cfg.shard_elems > 0 && boundary == 0)) {
@@ -523,7 +525,7 @@ static void launch_momentum(mlf_ctx *c, const mlf_plan_out *p, const std::vector
         a.cB[o] = (float)pw[m - i];
         a.sh[o] = (float)sh;
         a.gm[o] = (float)pw[m];
-        if (m == 1 && a.cA[o] == 1.f && a.cB[o] == 1.f && a.sh[o] == a.gm[o]) a.flag[o] |= kOpSingle;
+        if (single_ok && m == 1 && a.cA[o] == 1.f && a.cB[o] == 1.f && a.sh[o] == a.gm[o]) a.flag[o] |= kOpSingle;
       }
       if (boundary > 0 && ci == boundary) a.backup_after = (int32_t)(e - 1 - i0);
       q = e;
@@ -1170,6 +1172,17 @@ extern "C" mlf_status mlf_copy_bulk(int32_t device, void *dst, const void *src, 
     int sm = 148;
     CK(cudaDeviceGetAttribute(&sm, cudaDevAttrMultiProcessorCount, device));
     CK(launch_bulk_copy(dst, src, bytes, static_cast<cudaStream_t>(stream), sm));
+  });
+}
+
+extern "C" mlf_status mlf_read_probe(int32_t device, const void *src, int64_t bytes, void *stream) {
+  return guard([&] {
+    if (bytes % 16 != 0 || (reinterpret_cast<uintptr_t>(src) & 15))
+      throw Fail{MLF_E_INVALID, "read probe needs a 16-byte aligned pointer and size"};
+    CK(cudaSetDevice(device));
+    int sm = 148;
+    CK(cudaDeviceGetAttribute(&sm, cudaDevAttrMultiProcessorCount, device));
+    CK(launch_bulk_read(src, bytes, static_cast<cudaStream_t>(stream), sm));
   });
 }
 

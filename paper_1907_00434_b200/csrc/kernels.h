@@ -101,6 +101,7 @@ cudaError_t launch_synth(void *dst, int64_t n, int64_t elem_offset, int dtype, u
                          int variant, cudaStream_t s);
 cudaError_t launch_copy(void *dst, const void *src, int64_t bytes, cudaStream_t s, int sm_count);
 cudaError_t launch_bulk_copy(void *dst, const void *src, int64_t bytes, cudaStream_t s, int sm_count);
+cudaError_t launch_bulk_read(const void *src, int64_t bytes, cudaStream_t s, int sm_count);
 
 // one launch gathering up to kMaxShards 16-byte-aligned pieces (float4 counts)
 constexpr int kMaxShards = 16;

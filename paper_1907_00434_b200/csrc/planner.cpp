@@ -340,7 +340,7 @@ struct Cur {
 // window leaves the path minimum, hence the whole transfer, unchanged (used by the
 // ordering's per-class cache, order_final).
 struct WalkRec {
-  i64 t0, t1, slack[3];
+  i64 t0, t1, r, slack[3];   // r: the rate the transfer used on [t0, t1)
 };
 
 static bool transfer(const Net &net, const Pending *L0, const Pending *L1, i64 size, int src, int dst, i64 t_avail,
@@ -405,18 +405,14 @@ static bool transfer(const Net &net, const Pending *L0, const Pending *L1, i64 s
       if ((i128)cur + dt > (i128)T_LIMIT) throw PlanFail{MLF_E_INVALID, "model time overflow"};
       out.t_en = cur + (i64)dt;
       out.segs.push_back({cur, out.t_en, r});
-      if (rec) rec->push_back({cur, out.t_en, {rks[0] - r, nk > 1 ? rks[1] - r : 0, nk > 2 ? rks[2] - r : 0}});
+      if (rec) rec->push_back({cur, out.t_en, r, {rks[0] - r, nk > 1 ? rks[1] - r : 0, nk > 2 ? rks[2] - r : 0}});
       return true;
     }
     need -= (i128)r * (nb - cur);
     out.segs.push_back({cur, nb, r});
-    if (rec) rec->push_back({cur, nb, {rks[0] - r, nk > 1 ? rks[1] - r : 0, nk > 2 ? rks[2] - r : 0}});
+    if (rec) rec->push_back({cur, nb, r, {rks[0] - r, nk > 1 ? rks[1] - r : 0, nk > 2 ? rks[2] - r : 0}});
     cur = nb;
   }
-}
-
-static void add_pending(Pending &P, const Transfer &tr) {
-  for (int k = 0; k < tr.path.nk; ++k) combine(P.slot(tr.path.key[k]), tr.segs.data(), (int)tr.segs.size(), +1);
 }
 
 // O2: NetUp — subtract reservations from the residual profiles.
@@ -467,42 +463,65 @@ struct Ctx {
 // record_all = false (a pure evaluation, nothing is applied afterwards): `local` keeps only the
 // links a LATER component can share — up(src), and a later destination's own links when the
 // destination list repeats a node — which is all the later transfers read.
-// The walk of one send, component by component (CompRec: path + its WalkRec range).
+// The walk of one send, component by component (CompRec: path, its WalkRec range, times).
 struct CompRec {
   Path path;
   int w0, w1;
+  i64 t_st, t_en;
 };
 struct SendRec {
   std::vector<CompRec> comps;
   std::vector<WalkRec> walk;
 };
 
+// the reserved segments of a recorded component (identical to its Transfer::segs)
+static void rec_segs(const SendRec &rec, const CompRec &cr, std::vector<TSeg> &segs) {
+  segs.clear();
+  for (int w = cr.w0; w < cr.w1; ++w) segs.push_back({rec.walk[w].t0, rec.walk[w].t1, rec.walk[w].r});
+}
+
+// Multi-component transfer: components reserved sequentially in destination
+// order (R11) into `local` (pending on top of net - L0); t_en = max, t_st = min.
+// record_all = false (a pure evaluation, nothing is applied afterwards): `local` keeps only the
+// links a LATER component can share — up(src), and a later destination's own links when the
+// destination list repeats a node — which is all the later transfers read.
+// rec: the walk is recorded; from > 0 resumes a recorded send whose components 0..from-1 are
+// still valid on this network (their recorded reservations are replayed into `local`).
 static bool send(const Net &net, const Pending *L0, const Ctx &c, const std::vector<int> &dsts, int src, i64 size,
-                 i64 t_avail, Send &out, Pending &local, bool record_all = true, SendRec *rec = nullptr) {
+                 i64 t_avail, Send &out, Pending &local, bool record_all = true, SendRec *rec = nullptr,
+                 int from = 0) {
   thread_local std::vector<i64> comp;
   thread_local Transfer tr;
+  thread_local std::vector<TSeg> segs;
   component_bytes(size, c.weights, c.wsum, comp);
   local.clear();
   out.t_st = T_INF;
   out.t_en = 0;
   const i64 n = c.d.n;
   const bool all = record_all || c.dup_dsts;
+  auto reserve = [&](size_t j, const Path &path, const std::vector<TSeg> &sg) {
+    if (j + 1 < dsts.size() ? all : record_all) {
+      for (int k = 0; k < path.nk; ++k) combine(local.slot(path.key[k]), sg.data(), (int)sg.size(), +1);
+    } else if (j + 1 < dsts.size() && path.nk && path.key[0] < n) {   // up(src) is always the first path link
+      combine(local.slot(path.key[0]), sg.data(), (int)sg.size(), +1);
+    }
+  };
   if (rec) {
-    rec->comps.clear();
-    rec->walk.clear();
+    for (int j = 0; j < from; ++j) {
+      const CompRec &cr = rec->comps[j];
+      rec_segs(*rec, cr, segs);
+      reserve((size_t)j, cr.path, segs);
+      out.t_st = std::min(out.t_st, cr.t_st);
+      out.t_en = std::max(out.t_en, cr.t_en);
+    }
+    rec->walk.resize(from > 0 ? rec->comps[from].w0 : 0);
+    rec->comps.resize(from);
   }
-  for (size_t j = 0; j < dsts.size(); ++j) {
+  for (size_t j = from; j < dsts.size(); ++j) {
     const int w0 = rec ? (int)rec->walk.size() : 0;
     if (!transfer(net, L0, &local, comp[j], src, dsts[j], t_avail, tr, rec ? &rec->walk : nullptr)) return false;
-    if (rec) rec->comps.push_back({tr.path, w0, (int)rec->walk.size()});
-    if (j + 1 < dsts.size()) {
-      if (all)
-        add_pending(local, tr);
-      else if (tr.path.nk && tr.path.key[0] < n)       // up(src) is always the first path link
-        combine(local.slot(tr.path.key[0]), tr.segs.data(), (int)tr.segs.size(), +1);
-    } else if (record_all) {
-      add_pending(local, tr);
-    }
+    if (rec) rec->comps.push_back({tr.path, w0, (int)rec->walk.size(), tr.t_st, tr.t_en});
+    reserve(j, tr.path, tr.segs);
     out.t_st = std::min(out.t_st, tr.t_st);
     out.t_en = std::max(out.t_en, tr.t_en);
   }
@@ -536,12 +555,17 @@ struct OrderRes {
 
 static constexpr int kMinParallelEvals = 32;   // component transfers per scan worth a pool dispatch
 
-// True if reserving `M` on top of the network a send was recorded on leaves the send's result
-// unchanged: on every walk step, no path link loses more than its slack (components are
-// reserved one after another, so an unchanged component also leaves the later components'
-// inputs unchanged).  Saturated stretches were skipped by the walk and stay saturated.
-static bool send_unchanged(const SendRec &rec, const Pending &M) {
-  for (const CompRec &cr : rec.comps)
+// The first component of a recorded send whose result changes when `M` is reserved on top of
+// the network it was recorded on (comps.size(): none).  A component is unchanged if on every
+// walk step no path link loses more than its slack; components are reserved one after another,
+// so an unchanged prefix also leaves the next component's inputs unchanged.  Saturated
+// stretches were skipped by the walk and stay saturated.  The unchanged components' slacks are
+// reduced by what M takes, so the record describes the send on the new network.
+static int first_changed(SendRec &rec, const Pending &M) {
+  thread_local std::vector<i64> take;
+  for (size_t j = 0; j < rec.comps.size(); ++j) {
+    const CompRec &cr = rec.comps[j];
+    take.assign((size_t)(cr.w1 - cr.w0) * 3, 0);
     for (int k = 0; k < cr.path.nk; ++k) {
       const Profile *u = M.find(cr.path.key[k]);
       if (!u) continue;
@@ -552,10 +576,14 @@ static bool send_unchanged(const SendRec &rec, const Pending &M) {
         // the largest reserved rate of M on [t0, t1)
         i64 mx = cu.at(wr.t0);
         for (int q = cu.i + 1; q < cu.n && cu.p[q].t < wr.t1; ++q) mx = std::max(mx, cu.p[q].r);
-        if (mx > wr.slack[k]) return false;
+        if (mx > wr.slack[k]) return (int)j;
+        take[(size_t)(w - cr.w0) * 3 + k] = mx;
       }
     }
-  return true;
+    for (int w = cr.w0; w < cr.w1; ++w)
+      for (int k = 0; k < cr.path.nk; ++k) rec.walk[w].slack[k] -= take[(size_t)(w - cr.w0) * 3 + k];
+  }
+  return (int)rec.comps.size();
 }
 
 static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 tau, i64 v_init) {
@@ -571,7 +599,7 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
   const int G = (int)c.servers.size();
   std::vector<i64> ten(n);
   std::vector<uint8_t> ok(n);
-  std::vector<int> pool, uniq, miss, rep(n, -1);
+  std::vector<int> pool, uniq, miss, miss_from, rep(n, -1);
   // t_en is a pure function of (network, node, size, t_avail): updates sharing the triple
   // (virtual workers on one GPU usually share all three) form one class, evaluated once per scan
   std::vector<int> cls(n), cls_rep, cls_stamp;
@@ -601,7 +629,7 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
   // reservation of g*; NW takes la_id when g* is kept and keeps nw_id when it is dropped.
   struct ClassCache {
     int tag = -1;
-    i64 t_en = 0;
+    i64 t_st = 0, t_en = 0;
     SendRec rec;
   };
   std::vector<ClassCache> cache(cls_rep.size());
@@ -635,14 +663,18 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
     // others are evaluated again, on the pool when there are enough of them
     const int tag = L0 ? la_id : nw_id;
     miss.clear();
+    miss_from.clear();
     for (int g : uniq) {
       ClassCache &cc = cache[cls[g]];
-      if (cc.tag == tag || (L0 && cc.tag == nw_id && send_unchanged(cc.rec, *L0))) {
+      int from = 0;
+      if (cc.tag != tag && L0 && cc.tag == nw_id) from = first_changed(cc.rec, *L0);
+      if (cc.tag == tag || (L0 && cc.tag == nw_id && from == (int)cc.rec.comps.size())) {
         cc.tag = tag;
         ok[g] = 1;
         ten[g] = cc.t_en;
       } else {
         miss.push_back(g);
+        miss_from.push_back(from);       // the components before `from` keep their results
       }
     }
     Pool::get().run(
@@ -653,9 +685,10 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
           ClassCache &cc = cache[cls[g]];
           Send s;
           ok[g] = send(nw, L0, c, c.servers, batch[g].node, batch[g].size, batch[g].t_avail, s, local, false,
-                       &cc.rec);
+                       &cc.rec, miss_from[i]);
           ten[g] = s.t_en;
           cc.tag = ok[g] ? tag : -1;
+          cc.t_st = s.t_st;
           cc.t_en = s.t_en;
         },
         std::max(2, kMinParallelEvals / std::max(1, G)));
@@ -689,7 +722,20 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
     const i64 t_star = ten[g_star];
     cached = -1;
     Send s_star;
-    send(nw, nullptr, c, c.servers, batch[g_star].node, batch[g_star].size, batch[g_star].t_avail, s_star, star);
+    const ClassCache &cg = cache[cls[g_star]];
+    if (cg.tag == nw_id) {
+      // g*'s class was evaluated on exactly this network: its recorded walk is the reservation
+      thread_local std::vector<TSeg> segs;
+      star.clear();
+      for (const CompRec &cr : cg.rec.comps) {
+        rec_segs(cg.rec, cr, segs);
+        for (int k = 0; k < cr.path.nk; ++k) combine(star.slot(cr.path.key[k]), segs.data(), (int)segs.size(), +1);
+      }
+      s_star.t_st = cg.t_st;
+      s_star.t_en = cg.t_en;
+    } else {
+      send(nw, nullptr, c, c.servers, batch[g_star].node, batch[g_star].size, batch[g_star].t_avail, s_star, star);
+    }
     std::vector<int> cands;
     for (int g : unproc)
       if (g != g_star && dl[g] >= p + 1) cands.push_back(g);
@@ -882,6 +928,7 @@ static AggCase plan_aggregation(const std::vector<Item> &items, const Net &net0,
           if (n0 >= n1) return;
           Prefix &pre = starts[t];
           thread_local Transfer tr;
+          std::unique_ptr<Net> scratch;                // reused across cases (keeps its buffers)
           for (int n = n0; n < n1; ++n) {
             if (!pre.ok) break;
             const i64 cut = best_total.load(std::memory_order_relaxed);
@@ -898,7 +945,11 @@ static AggCase plan_aggregation(const std::vector<Item> &items, const Net &net0,
               AggCase cs;
               cs.n = n;
               cs.commits = pre.commits;
-              auto nw = std::make_unique<Net>(pre.nw);
+              if (scratch)
+                *scratch = pre.nw;
+              else
+                scratch = std::make_unique<Net>(pre.nw);
+              std::unique_ptr<Net> nw = std::move(scratch);
               det_agg_tail(cs, *nw, pre.t_max, items, c, dsts, aggs, cut);
               totals[n] = cs.feasible ? cs.total : -1;
               if (cs.feasible) {
@@ -906,13 +957,14 @@ static AggCase plan_aggregation(const std::vector<Item> &items, const Net &net0,
                 if (b.n < 0 || cs.total < b.cs.total) {
                   b.n = n;
                   b.cs = std::move(cs);
-                  b.nw = std::move(nw);
+                  std::swap(b.nw, nw);                 // the previous best's network becomes scratch
                 }
                 i64 cur = best_total.load(std::memory_order_relaxed);
                 while (b.cs.total < cur &&
                        !best_total.compare_exchange_weak(cur, b.cs.total, std::memory_order_relaxed)) {
                 }
               }
+              if (nw) scratch = std::move(nw);
             }
             if (n < N) pre.extend(items, n, c, dsts);
           }
@@ -950,17 +1002,19 @@ static std::vector<i64> chained_times(const std::vector<CommitRec> &cm) {
 // Eq. 9/12 bound with the momentum coefficients (R15); fixed evaluation order.
 static double divergence_bound(const double *norms, int m, double gamma, double h0) {
   if (m == 0) return 0.0;
-  std::vector<double> pw(m + 1);
+  thread_local std::vector<double> pw, cum;
+  pw.resize(m + 1);
+  cum.resize(m + 1);
   pw[0] = 1.0;
   for (int j = 1; j <= m; ++j) pw[j] = pw[j - 1] * gamma;
   double coef_h = 0.0;
   for (int j = 1; j <= m; ++j) coef_h += pw[j];
+  // cum[k] = pw[0] + ... + pw[k], summed left to right: the same additions in the same order
+  // as summing each coefficient on its own, so every coefficient is bitwise the same
+  cum[0] = pw[0];
+  for (int k = 1; k <= m; ++k) cum[k] = cum[k - 1] + pw[k];
   double d = coef_h * h0;
-  for (int i = 1; i <= m; ++i) {
-    double cf = 0.0;
-    for (int j = 0; j <= m - i; ++j) cf += pw[j];
-    d += cf * norms[i - 1];
-  }
+  for (int i = 1; i <= m; ++i) d += cum[m - i] * norms[i - 1];
   return d;
 }
 

@@ -169,6 +169,53 @@ __global__ void __launch_bounds__(32, 1) bulk_copy_kernel(const __grid_constant_
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// Read-only roofline probe: every CTA streams its 16 KB chunks of src into a ring of shared-memory
+// stages with TMA bulk copies and waits for each to land; nothing is written back.  The read end of
+// the mixed read/write HBM ceiling bench.py reports (bench.py roofline_extras).
+__global__ void __launch_bounds__(32, 1) bulk_read_kernel(const char *src, int64_t n_chunks, int64_t bytes) {
+  using namespace bulkcopy;
+  extern __shared__ __align__(128) uint8_t sm[];
+  uint64_t *full = reinterpret_cast<uint64_t *>(sm + (size_t)kStages * kChunk);
+  if (threadIdx.x != 0) return;
+  for (int s = 0; s < kStages; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(saddr(&full[s])));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  uint32_t L = 0, S = 0;
+  int64_t i_load = blockIdx.x, i_wait = blockIdx.x;
+  auto issue = [&](int64_t i, uint32_t stage) {
+    const int64_t off = i * kChunk;
+    const uint32_t len = (uint32_t)(bytes - off < kChunk ? bytes - off : kChunk);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(&full[stage])), "r"(len)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     saddr(sm + (size_t)stage * kChunk)),
+                 "l"(src + off), "r"(len), "r"(saddr(&full[stage]))
+                 : "memory");
+  };
+  for (; L < (uint32_t)kStages && i_load < n_chunks; ++L, i_load += gridDim.x) issue(i_load, L);
+  for (; i_wait < n_chunks; i_wait += gridDim.x, ++S) {
+    const uint32_t stage = S % kStages, parity = (S / kStages) & 1;
+    asm volatile(
+        "{\n\t.reg .pred p;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W_%=;\n}" ::"r"(
+            saddr(&full[stage])),
+        "r"(parity)
+        : "memory");
+    if (i_load < n_chunks) {                       // the stage was consumed on arrival: refill it
+      issue(i_load, stage);
+      i_load += gridDim.x;
+    }
+  }
+}
+
+cudaError_t launch_bulk_read(const void *src, int64_t bytes, cudaStream_t s, int sm_count) {
+  using namespace bulkcopy;
+  if (bytes <= 0) return cudaSuccess;
+  const size_t smem = (size_t)kStages * kChunk + kStages * sizeof(uint64_t);
+  static std::atomic<uint64_t> init{0};
+  if (cudaError_t e = ensure_smem(bulk_read_kernel, smem, init); e != cudaSuccess) return e;
+  bulk_read_kernel<<<sm_count, 32, smem, s>>>(static_cast<const char *>(src), (bytes + kChunk - 1) / kChunk, bytes);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_bulk_segs(const BulkSegs &a, cudaStream_t s, int sm_count) {
   using namespace bulkcopy;
   if (a.n <= 0 || a.cstart[a.n] <= 0) return cudaSuccess;

@@ -26,7 +26,7 @@ EXPORTS = (
     "mlf_execute", "mlf_execute_phase", "mlf_sync", "mlf_pull_model", "mlf_stats", "mlf_destroy",
     "mlf_last_error", "mlf_ipc_export", "mlf_ipc_open", "mlf_ipc_close", "mlf_phase_event_export",
     "mlf_phase_events_open", "mlf_gather", "mlf_synth_fill", "mlf_copy_kernel", "mlf_copy_engine",
-    "mlf_copy_bulk", "mlf_plan_distribution", "mlf_distribute_phase", "mlf_release",
+    "mlf_copy_bulk", "mlf_read_probe", "mlf_plan_distribution", "mlf_distribute_phase", "mlf_release",
 )
 
 
@@ -140,6 +140,7 @@ _lib.mlf_synth_fill.argtypes = [C.c_int32, _p, C.c_int64, C.c_int64, C.c_int32, 
 _lib.mlf_copy_kernel.argtypes = [C.c_int32, _p, _p, C.c_int64, _p]
 _lib.mlf_copy_engine.argtypes = [C.c_int32, _p, _p, C.c_int64, _p]
 _lib.mlf_copy_bulk.argtypes = [C.c_int32, _p, _p, C.c_int64, _p]
+_lib.mlf_read_probe.argtypes = [C.c_int32, _p, C.c_int64, _p]
 _lib.mlf_gather.argtypes = [C.c_int32, _p, C.c_int32, C.POINTER(_p), _i64p, _i64p, C.c_int32, _p]
 
 
@@ -542,6 +543,10 @@ def gather(device: int, dst_ptr: int, shard_ptrs, begins, elems, copy_engine: in
 
 def copy_bulk(device: int, dst_ptr: int, src_ptr: int, nbytes: int, stream=None):
     _check(_lib.mlf_copy_bulk(device, dst_ptr, src_ptr, int(nbytes), stream))
+
+
+def read_probe(device: int, src_ptr: int, nbytes: int, stream=None):
+    _check(_lib.mlf_read_probe(device, src_ptr, int(nbytes), stream))
 
 
 def copy_engine(device: int, dst_ptr: int, src_ptr: int, nbytes: int, stream=None):

@@ -193,14 +193,31 @@ class ShardedWorkload:
         torch.cuda.current_stream().synchronize()
         self.barrier()
 
+    def plan_once(self, iteration: int):
+        """The batch's plan: mlf_plan on rank 0 only (with the host's cores to itself), the integer
+        plan broadcast over the gloo control group and rebuilt with plan_from_dict elsewhere.
+        mlf_plan is deterministic, so this equals every rank planning for itself, and every
+        rank's mlf_execute still validates the plan against its own copy of the batch."""
+        wl = self.wl
+        pd = None
+        if self.rank == 0:
+            t0 = time.perf_counter()
+            pb = wl.plan(iteration)
+            self.last_plan_ms = (time.perf_counter() - t0) * 1e3
+            pd = pb.to_dict(self.cfg["W"])
+        obj = [pd]
+        dist.broadcast_object_list(obj, src=0, group=self.ctrl)
+        pd = obj[0]
+        if self.rank != 0:
+            pb = m.plan_from_dict(pd)
+            self.last_plan_ms = 0.0
+        return pb, pd
+
     def step(self, iteration: int, flush=None):
         """One batch on every rank.  Returns (plan dict, this rank's device ms)."""
         wl = self.wl
         draws = wl.submit_all(iteration)
-        t0 = time.perf_counter()
-        pb = wl.plan(iteration)
-        self.last_plan_ms = (time.perf_counter() - t0) * 1e3
-        pd = pb.to_dict(self.cfg["W"])
+        pb, pd = self.plan_once(iteration)
         if flush is not None:
             flush()
         torch.cuda.current_stream().synchronize()
