@@ -372,6 +372,11 @@ def run_single(a):
             _, r5, T5, _, _ = measure(32, a.dtype, nv, 3, "bulk", gamma=0.9)
             var["momentum0.9_tau32_bulk"] = summarize(r5, T5)
             if a.dtype == "f32":
+                # NEXT-1 with bf16 updates: the consumer-bound case (16-warp momentum kernel)
+                for t in (4, 8, 32):
+                    _, r7, T7, _, _ = measure(t, "bf16", nv, 3, "bulk", gamma=0.9)
+                    var[f"momentum0.9_bf16_tau{t}_bulk"] = summarize(r7, T7)
+            if a.dtype == "f32":
                 # SURVEY §8(d) config 2's bf16 variant: 2-byte updates widened exactly in the kernel
                 for t in (4, 32):
                     _, r6, T6, _, _ = measure(t, "bf16", nv, 3, "bulk")

@@ -353,42 +353,59 @@ static bool transfer(const Net &net, const Pending *L0, const Pending *L1, i64 s
     out.t_st = out.t_en = t_avail;
     return true;
   }
-  struct Lk {
-    Cur base, u0, u1;   // the link's residual, minus the reserved rate of L0 and of L1
-    Seg own;            // a pair link not reserved yet: its capacity
+  // one cursor per (link, profile): the link's residual, then the reserved rates of L0 and L1
+  // on it (only those that exist); cur[c].sign = +1 for a residual, -1 for a reservation
+  struct C {
+    const Seg *p;
+    int n, i, link;
+    i64 sign;
   };
-  Lk lk[3];
+  C cs[9];
+  Seg own[3];                 // pair links not reserved yet: their capacity
+  int nc = 0;
   const int nk = out.path.nk;
+  auto add = [&](const Profile *pr, int k, i64 sign) {
+    C &c = cs[nc++];
+    c.p = pr->data();
+    c.n = (int)pr->size();
+    const Seg *it = std::upper_bound(c.p, c.p + c.n, t_avail, [](i64 v, const Seg &x) { return v < x.t; });
+    c.i = it == c.p ? 0 : (int)(it - c.p) - 1;
+    c.link = k;
+    c.sign = sign;
+  };
   for (int k = 0; k < nk; ++k) {
     const i64 key = out.path.key[k];
-    const Profile *pr = net.get(key);
-    if (pr) {
-      lk[k].base.seek(pr, t_avail);
+    if (const Profile *pr = net.get(key)) {
+      add(pr, k, +1);
     } else {
-      lk[k].own = Seg{0, std::max<i64>(net.capacity(key), 0)};
-      lk[k].base.p = &lk[k].own;
-      lk[k].base.n = 1;
-      lk[k].base.i = 0;
+      own[k] = Seg{0, std::max<i64>(net.capacity(key), 0)};
+      cs[nc++] = C{&own[k], 1, 0, k, +1};
     }
-    lk[k].u0.seek(L0 ? L0->find(key) : nullptr, t_avail);
-    lk[k].u1.seek(L1 ? L1->find(key) : nullptr, t_avail);
+    if (L0)
+      if (const Profile *u = L0->find(key)) add(u, k, -1);
+    if (L1)
+      if (const Profile *u = L1->find(key)) add(u, k, -1);
   }
   i128 need = (i128)size * NS_PER_S;
   i64 cur = t_avail;
   bool started = false;
   for (;;) {
-    // r = path residual at cur, nb = its next possible change; while some link is saturated
-    // the path stays at 0 at least until every saturated link's own next change (zjump), so
-    // the walk jumps there instead of stepping through the other links' breakpoints
-    i64 r = T_INF, nb = T_INF, zjump = t_avail, rks[3];
+    // rks[k] = link k's residual at cur, nbk[k] = its next possible change; r = the path
+    // minimum, nb = its next possible change; while some link is saturated the path stays at 0
+    // at least until every saturated link's own next change (zjump), so the walk jumps there
+    // instead of stepping through the other links' breakpoints
+    i64 rks[3] = {0, 0, 0}, nbk[3] = {T_INF, T_INF, T_INF};
+    for (int q = 0; q < nc; ++q) {
+      C &c = cs[q];
+      while (c.i + 1 < c.n && c.p[c.i + 1].t <= cur) ++c.i;
+      rks[c.link] += c.sign * c.p[c.i].r;
+      if (c.i + 1 < c.n && c.p[c.i + 1].t < nbk[c.link]) nbk[c.link] = c.p[c.i + 1].t;
+    }
+    i64 r = T_INF, nb = T_INF, zjump = t_avail;
     for (int k = 0; k < nk; ++k) {
-      Lk &L = lk[k];
-      const i64 rk = L.base.at(cur) - L.u0.at(cur) - L.u1.at(cur);
-      rks[k] = rk;
-      const i64 nbk = std::min(L.base.next(), std::min(L.u0.next(), L.u1.next()));
-      if (rk == 0) zjump = std::max(zjump, nbk);
-      r = std::min(r, rk);
-      nb = std::min(nb, nbk);
+      if (rks[k] == 0) zjump = std::max(zjump, nbk[k]);
+      r = std::min(r, rks[k]);
+      nb = std::min(nb, nbk[k]);
     }
     if (r < 0) throw PlanFail{MLF_E_INVALID, "internal: negative residual"};
     if (r == 0) {
@@ -553,7 +570,14 @@ struct OrderRes {
   std::vector<Send> sends;
 };
 
-static constexpr int kMinParallelEvals = 32;   // component transfers per scan worth a pool dispatch
+// component transfers per scan worth a pool dispatch (MLF_PLAN_MIN_EVALS overrides; tuning)
+static int min_parallel_evals() {
+  static const int v = [] {
+    const char *e = getenv("MLF_PLAN_MIN_EVALS");
+    return e && atoi(e) > 0 ? atoi(e) : 32;
+  }();
+  return v;
+}
 
 // The first component of a recorded send whose result changes when `M` is reserved on top of
 // the network it was recorded on (comps.size(): none).  A component is unchanged if on every
@@ -691,7 +715,7 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
           cc.t_st = s.t_st;
           cc.t_en = s.t_en;
         },
-        std::max(2, kMinParallelEvals / std::max(1, G)));
+        std::max(2, min_parallel_evals() / std::max(1, G)));
     int best = -1;
     for (int g : pool) {
       ok[g] = ok[rep[g]];

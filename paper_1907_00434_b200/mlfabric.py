@@ -292,7 +292,10 @@ def plan_raw(net: MlfNet, batch: MlfBatch, prm: MlfPlanParams, capacity: int, ke
 def plan_from_dict(d: dict) -> MlfPlanOut:
     """Build an mlf_plan_out from a plan dict (e.g. to feed a hand-made plan to execute)."""
     n = max(len(d["drop_reason"]), len(d["order"]), 1)
-    b = PlanBuffers(max(n, len(d.get("punted", [])), len(d["commit_first"]), len(d.get("group_node", []))))
+    # replica outputs index carried ++ order: they can be longer than the batch
+    b = PlanBuffers(max(n, len(d.get("punted", [])), len(d["commit_first"]), len(d.get("group_node", [])),
+                        len(d.get("replica_commit_first", [])),
+                        d.get("replica_frozen", 0) + d.get("n_punted", 0)))
     o = b.out
     o.n_commit = d["n_commit"]
     b.order[:len(d["order"])] = d["order"]
@@ -307,6 +310,7 @@ def plan_from_dict(d: dict) -> MlfPlanOut:
     o.replica_frozen = d.get("replica_frozen", 0)
     o.replica_boundary_commit = d.get("replica_boundary_commit", -1)
     o.n_punted = d.get("n_punted", 0)
+    b.punted[:len(d.get("punted", []))] = d.get("punted", [])
     o.delayed_last = d.get("delayed_last", 0)
     o.t_total_ns = d.get("t_total_ns", 0)
     rf = d.get("replica_commit_first", [])
