@@ -359,8 +359,10 @@ __device__ __forceinline__ void mom_single(const uint8_t *st, bool bf, int tid, 
     const int c = tid + k * kCons;
     if (kFull || c * 4 < cnt) {
       const float4 g = bf ? widen_bf16x4(reinterpret_cast<const uint2 *>(st)[c]) : reinterpret_cast<const float4 *>(st)[c];
-      const float4 u = cat2(mul2(make_float2(-lr, -lr), lo2(g)), mul2(make_float2(-lr, -lr), hi2(g)));
-      h[k] = add4(mul4(gm, h[k]), u);
+      const float2 nlr = make_float2(-lr, -lr), gm2 = make_float2(gm, gm);
+      const float4 u = cat2(mul2(nlr, lo2(g)), mul2(nlr, hi2(g)));
+      // gm*h packed too (each lane rounds as mul.rn); the adds stay scalar (no FFMA2, R17)
+      h[k] = add4(cat2(mul2(gm2, lo2(h[k])), mul2(gm2, hi2(h[k]))), u);
       w[k] = add4(w[k], h[k]);
     }
   }
@@ -854,7 +856,14 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) fused_commit_momentum_bh(con
     return;
   }
   const int tid = threadIdx.x;
-  uint32_t L = 0;
+  // ring position kept incrementally (stage index and phase parity), no division per stage
+  uint32_t s = 0, ph = 0;
+  auto advance = [&]() {
+    if (++s == (uint32_t)kStages) {
+      s = 0;
+      ph ^= 1u;
+    }
+  };
   for (int64_t e0 = r_begin; e0 < r_end; e0 += kTile) {
     const int cnt = (int)(r_end - e0 < kTile ? r_end - e0 : kTile);
     const bool full_tile = cnt == kTile;
@@ -864,8 +873,7 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) fused_commit_momentum_bh(con
     // w and h: two half-stages each; chunk k lives in the first half iff k < kHalfChunks
 #pragma unroll
     for (int which = 0; which < 4; ++which) {
-      const uint32_t s = L % kStages;
-      mbar_wait(&full[s], (L / kStages) & 1);
+      mbar_wait(&full[s], ph);
       const float4 *sp = reinterpret_cast<const float4 *>(smem + (size_t)s * kStageBytes);
       const int k0 = (which & 1) ? kHalfChunks : 0;
 #pragma unroll
@@ -876,7 +884,7 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) fused_commit_momentum_bh(con
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
-      ++L;
+      advance();
     }
     if (a.backup_after == -1) {
 #pragma unroll
@@ -888,23 +896,22 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1) fused_commit_momentum_bh(con
         }
       }
     }
-    for (int j = 0; j < a.n_ops; ++j, ++L) {
-      const uint32_t s = L % kStages;
+    for (int j = 0; j < a.n_ops; ++j) {
       const uint8_t f = a.flag[j];
-      const float ca = a.cA[j], cb = a.cB[j];
-      mbar_wait(&full[s], (L / kStages) & 1);
+      mbar_wait(&full[s], ph);
       const uint8_t *st = smem + (size_t)s * kStageBytes;
       const bool single = f & kOpSingle;
       if (single) {
         if (full_tile) mom_single<true, kChunks, kCons>(st, true, tid, cnt, a.lr, a.gm[j], w, h);
         else mom_single<false, kChunks, kCons>(st, true, tid, cnt, a.lr, a.gm[j], w, h);
       } else if (full_tile) {
-        mom_fold_bf16_w<true, kChunks, kCons>(st, tid, cnt, a.lr, ca, cb, A, B);
+        mom_fold_bf16_w<true, kChunks, kCons>(st, tid, cnt, a.lr, a.cA[j], a.cB[j], A, B);
       } else {
-        mom_fold_bf16_w<false, kChunks, kCons>(st, tid, cnt, a.lr, ca, cb, A, B);
+        mom_fold_bf16_w<false, kChunks, kCons>(st, tid, cnt, a.lr, a.cA[j], a.cB[j], A, B);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
+      advance();
       if ((f & kOpLast) && !single) {
         const float sh = a.sh[j], gm = a.gm[j];
 #pragma unroll
@@ -1300,9 +1307,10 @@ static cudaError_t launch_momentum_t(const MomentumArgs &a, cudaStream_t s, int 
 cudaError_t launch_commit_momentum(const MomentumArgs &a, cudaStream_t s, int sm_count) {
   bool all_bf16 = a.n_ops > 0;
   for (int j = 0; j < a.n_ops && all_bf16; ++j) all_bf16 = (a.flag[j] & kOpBf16) != 0;
-  // the 16-warp kernel for all-bf16 lists of >= MLF_MOM_WIDE operands (0: never)
+  // the 16-warp kernel for all-bf16 lists of >= MLF_MOM_WIDE operands (0: never); measured at
+  // least as fast as the 8-warp kernels at every tau of config 2 (tau 4: 98.7% vs 97.8%)
   const char *wide = getenv("MLF_MOM_WIDE");
-  const int wide_min = wide ? atoi(wide) : 6;
+  const int wide_min = wide ? atoi(wide) : 1;
   if (all_bf16 && wide_min > 0 && a.n_ops >= wide_min) {
     constexpr int kT = 8192, kS = 12, kCW = 16;
     constexpr size_t smem = (size_t)kS * kT * 2 + 2 * kS * sizeof(uint64_t);
