@@ -131,6 +131,11 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_bulk(const __grid_co
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t n_bulk = a.n & ~int64_t(7);       // bulk region: whole 8-element groups (16 B for bf16)
   const int64_t n_tiles = (n_bulk + kTile - 1) / kTile;
+  // contiguous mode: this CTA's range [r_begin, r_end); tiles are offsets into it, and the tile
+  // "index" handed to the consumers is the element offset itself
+  const bool contig = a.contig && !a.sched;
+  const int64_t r_begin = contig ? (n_bulk / 8) * blockIdx.x / gridDim.x * 8 : 0;
+  const int64_t r_end = contig ? (n_bulk / 8) * (blockIdx.x + 1) / gridDim.x * 8 : n_bulk;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -153,13 +158,14 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_bulk(const __grid_co
       // even with the normal policy costs ~4% on peer (NVLink) reads
       const uint64_t pol_w = kHint ? policy_evict_normal() : 0;
       const uint64_t pol_op = kHint ? policy_evict_first() : 0;
-      int64_t t = a.sched ? (int64_t)atomicAdd(&a.sched[0], 1ull) : (int64_t)blockIdx.x;
+      int64_t t = contig ? 0 : (a.sched ? (int64_t)atomicAdd(&a.sched[0], 1ull) : (int64_t)blockIdx.x);
       for (;;) {
-        const int64_t e0 = t * kTile;
-        const uint32_t cnt = t < n_tiles ? (uint32_t)(n_bulk - e0 < kTile ? n_bulk - e0 : kTile) : 0u;
+        const int64_t e0 = contig ? r_begin + t * kTile : t * kTile;
+        const bool live = contig ? e0 < r_end : t < n_tiles;
+        const uint32_t cnt = live ? (uint32_t)(r_end - e0 < kTile ? r_end - e0 : kTile) : 0u;
         // fetch the next tile now: the atomic's latency hides behind this tile's issues
         int64_t t_next = 0;
-        if (t < n_tiles) t_next = a.sched ? (int64_t)atomicAdd(&a.sched[0], 1ull) : t + gridDim.x;
+        if (live) t_next = (a.sched && !contig) ? (int64_t)atomicAdd(&a.sched[0], 1ull) : t + (contig ? 1 : gridDim.x);
         for (int j = -1; j < a.n_ops; ++j, ++L) {
           const uint32_t s = L % kStages;
           if (L >= (uint32_t)kStages) {
@@ -169,8 +175,8 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_bulk(const __grid_co
           const void *src;
           uint32_t bytes;
           if (j < 0) {
-            tile_of[s] = t < n_tiles ? t : -1;
-            if (t >= n_tiles) {
+            tile_of[s] = live ? e0 : -1;             // the consumers get the tile's element offset
+            if (!live) {
               mbar_arrive(&full[s]);                  // release: the consumers read -1
               break;
             }
@@ -189,10 +195,10 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_bulk(const __grid_co
           else
             bulk_g2s(smem + (size_t)s * kStageBytes, src, bytes, &full[s]);
         }
-        if (t >= n_tiles) break;
+        if (!live) break;
         t = t_next;
       }
-      if (a.sched) {
+      if (a.sched && !contig) {
         // every CTA has made its last fetch: the last one resets the counters for the next
         // launch on this stream
         __threadfence();
@@ -210,10 +216,9 @@ __global__ void __launch_bounds__(kThreads, 1) fused_commit_bulk(const __grid_co
     for (;;) {
       const uint32_t s0 = L % kStages;
       mbar_wait(&full[s0], (L / kStages) & 1);
-      const int64_t t = tile_of[s0];
-      if (t < 0) break;
-      const int64_t e0 = t * kTile;
-      const int cnt = (int)(n_bulk - e0 < kTile ? n_bulk - e0 : kTile);
+      const int64_t e0 = tile_of[s0];
+      if (e0 < 0) break;
+      const int cnt = (int)(r_end - e0 < kTile ? r_end - e0 : kTile);
       float4 w[kChunks], x[kChunks];
       {
         const uint32_t s = s0;
@@ -328,6 +333,16 @@ __device__ __forceinline__ float2 mul2(float2 a, float2 b) {
       : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
   return r;
 }
+// packed sum of two fp32 pairs, each lane rounded as add.rn.  Only for sums whose operands are
+// not products: ptxas contracts a mul.rn.f32x2 feeding add.rn.f32x2 into FFMA2 (R17 forbids
+// fusing), but a sum of sums stays FADD2 (tests/test_sass_guard.py)
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  float2 r;
+  asm("{.reg .b64 x, y, z;\n\tmov.b64 x, {%2, %3};\n\tmov.b64 y, {%4, %5};\n\t"
+      "add.rn.f32x2 z, x, y;\n\tmov.b64 {%0, %1}, z;}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
 __device__ __forceinline__ float4 cat2(float2 lo, float2 hi) { return make_float4(lo.x, lo.y, hi.x, hi.y); }
 __device__ __forceinline__ float2 lo2(float4 v) { return make_float2(v.x, v.y); }
 __device__ __forceinline__ float2 hi2(float4 v) { return make_float2(v.z, v.w); }
@@ -363,7 +378,7 @@ __device__ __forceinline__ void mom_single(const uint8_t *st, bool bf, int tid, 
       const float4 u = cat2(mul2(nlr, lo2(g)), mul2(nlr, hi2(g)));
       // gm*h packed too (each lane rounds as mul.rn); the adds stay scalar (no FFMA2, R17)
       h[k] = add4(cat2(mul2(gm2, lo2(h[k])), mul2(gm2, hi2(h[k]))), u);
-      w[k] = add4(w[k], h[k]);
+      w[k] = cat2(add2(lo2(w[k]), lo2(h[k])), add2(hi2(w[k]), hi2(h[k])));   // w + h: no product
     }
   }
 }
@@ -1307,10 +1322,11 @@ static cudaError_t launch_momentum_t(const MomentumArgs &a, cudaStream_t s, int 
 cudaError_t launch_commit_momentum(const MomentumArgs &a, cudaStream_t s, int sm_count) {
   bool all_bf16 = a.n_ops > 0;
   for (int j = 0; j < a.n_ops && all_bf16; ++j) all_bf16 = (a.flag[j] & kOpBf16) != 0;
-  // the 16-warp kernel for all-bf16 lists of >= MLF_MOM_WIDE operands (0: never); measured at
-  // least as fast as the 8-warp kernels at every tau of config 2 (tau 4: 98.7% vs 97.8%)
+  // the 16-warp kernel for all-bf16 lists of >= MLF_MOM_WIDE operands (0: never): config 2
+  // tau 8 / 16 / 32 92.1 / 93.5 / 95.0% vs 89.8 / 80.7 / 78.0% for the 8-warp kernel; at tau 4
+  // (4 operands, a third of the stages are w and h) the 8-warp kernel wins, 97.8% vs 92.7%
   const char *wide = getenv("MLF_MOM_WIDE");
-  const int wide_min = wide ? atoi(wide) : 1;
+  const int wide_min = wide ? atoi(wide) : 6;
   if (all_bf16 && wide_min > 0 && a.n_ops >= wide_min) {
     constexpr int kT = 8192, kS = 12, kCW = 16;
     constexpr size_t smem = (size_t)kS * kT * 2 + 2 * kS * sizeof(uint64_t);
@@ -1392,7 +1408,8 @@ cudaError_t launch_commit_bulk(const CommitArgs &a, cudaStream_t s, int sm_count
       return cudaGetLastError();
     }
     const int64_t per_cta = (a.n / 4096) / sms;
-    tile = per_cta >= 32 ? 4096 : ((a.n / 2048) / sms >= 32 ? 2048 : 1024);
+    // contiguous ranges balance the bytes per CTA by construction: keep 16 KB copies
+    tile = (per_cta >= 32 || (a.contig && !a.sched)) ? 4096 : ((a.n / 2048) / sms >= 32 ? 2048 : 1024);
   }
   if (tile == 8192) return launch_tile<8192, 6>(a, s, sm_count);
   if (tile == 2048) return launch_tile<2048, 24>(a, s, sm_count);

@@ -99,6 +99,7 @@ struct mlf_ctx {
   bool dist_p1 = false;                           // distribution phase 1 recorded ev_stop
   unsigned long long *tile_sched = nullptr;       // dynamic tile counters of the bulk commit
   bool dyn_sched = false;
+  bool contig = false;                            // MLF_BULK_SCHED=contig: one range per CTA
   int32_t l2_hint = 0;                            // MLF_L2_HINT=1: evict-first operand loads
   std::deque<std::pair<cudaEvent_t, std::vector<int>>> flights;   // executed batches not yet released
   std::vector<cudaEvent_t> ev_free;                                // their recycled events
@@ -223,7 +224,8 @@ extern "C" mlf_status mlf_init(const mlf_config *cfg, int64_t v0, mlf_ctx **out)
       CK(cudaMalloc(reinterpret_cast<void **>(&c->tile_sched), 2 * sizeof(unsigned long long)));
       CK(cudaMemset(c->tile_sched, 0, 2 * sizeof(unsigned long long)));
       const char *sched = getenv("MLF_BULK_SCHED");
-      c->dyn_sched = !(sched && std::string(sched) == "static");
+      c->dyn_sched = !(sched && (std::string(sched) == "static" || std::string(sched) == "contig"));
+      c->contig = sched && std::string(sched) == "contig";
       // evict-first L2 policy for operand loads: +0.7% / +1.3% of the HBM roofline on one GPU
       // (config 2, tau 4 / 32); over NVLink it costs 4% (2 GPUs), so only local operands get it
       const char *hint = getenv("MLF_L2_HINT");
@@ -567,6 +569,7 @@ static void launch_ops(mlf_ctx *c, float *w, float *backup, const std::vector<Co
     a.bcast_mc = c->cfg.bcast_multicast;
     a.l2_hint = c->l2_hint;
     a.sched = c->dyn_sched ? c->tile_sched : nullptr;
+    a.contig = c->contig ? 1 : 0;
     if (bcast && i1 == ops.size())                  // only the pass that finishes w broadcasts it
       for (float *d : c->bcast) a.bcast[a.n_bcast++] = d + c->cfg.shard_begin + off;
     for (size_t q = i0; q < i1; ++q) {

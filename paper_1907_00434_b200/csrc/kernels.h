@@ -57,6 +57,9 @@ struct CommitArgs {
   // dynamic tile scheduling (bulk kernel): [0] next tile, [1] CTAs done; zero between launches
   // (the last CTA resets both).  nullptr = static round-robin tiles.
   unsigned long long *sched;
+  // 1 (bulk kernel, sched == nullptr): every CTA walks ONE contiguous range of n / grid elements
+  // (multiples of 8) in tiles, so every CTA moves the same bytes (no last-wave tile imbalance)
+  int32_t contig;
 };
 
 // tree_reduce: out[i] = left fold of members, fp32 (an aggregator's sum).

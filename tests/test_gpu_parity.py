@@ -161,6 +161,24 @@ def test_bulk_tiles_bitwise(tile, dtype):
         del os.environ["MLF_BULK_TILE"]
 
 
+@pytest.mark.parametrize("dtype", [sg.DTYPE_F32, sg.DTYPE_BF16])
+def test_bulk_contiguous_ranges_bitwise(dtype):
+    # MLF_BULK_SCHED=contig: every CTA walks one contiguous range (ends not tile-aligned, ranges
+    # shorter than a tile, ragged tails) — same bits as the oracle, mirror included
+    rng = np.random.default_rng(77 + dtype)
+    os.environ["MLF_BULK_SCHED"] = "contig"
+    try:
+        for S in (1, 9, 4099, 148 * 8 * 3 + 5, 300_001, 6_400_017):
+            W = int(rng.integers(2, 20))
+            p = random_plan(rng, W, n_commit=W, boundary=1)
+            w, b, _, _ = gpu_run(S, W, dtype, p, backup=True, impl="bulk")
+            wr, br = oracle_run(S, dtype, p)
+            assert np.array_equal(bits(w), bits(wr)), S
+            assert np.array_equal(bits(b), bits(br)), S
+    finally:
+        del os.environ["MLF_BULK_SCHED"]
+
+
 @pytest.mark.parametrize("boundary", [0, 2, -1])
 def test_bf16_16kb_layout_bitwise(boundary):
     # all-bf16 operand lists large enough for the 8192-element layout (16 KB bf16 copies, w
