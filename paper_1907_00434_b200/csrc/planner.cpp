@@ -732,8 +732,9 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
   // network (NW with g* reserved), so its result is the look-ahead's g° (and t_en):
   // reusing it halves the scans without changing any decision.
   int cached = -1;
+  std::vector<int> keep, cands;
   for (;;) {
-    std::vector<int> keep;
+    keep.clear();
     for (int g : unproc) {
       if (dl[g] < p)
         res.reason[g] = 1;                          // expired (R4)
@@ -760,7 +761,7 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
     } else {
       send(nw, nullptr, c, c.servers, batch[g_star].node, batch[g_star].size, batch[g_star].t_avail, s_star, star);
     }
-    std::vector<int> cands;
+    cands.clear();
     for (int g : unproc)
       if (g != g_star && dl[g] >= p + 1) cands.push_back(g);
     bool drop = false;
@@ -910,9 +911,15 @@ static AggCase plan_aggregation(const std::vector<Item> &items, const Net &net0,
   // one sequential pass, then every task extends its own copy incrementally
   // (small batches: one task, no dispatch overhead)
   const int tasks = (N + 1) * (int)dsts.size() < 256 ? 1 : std::max(1, std::min(N + 1, 2 * Pool::get().threads()));
+  // With Alg. 2's reservations at hand (hint) every task replays its own start prefix from the
+  // batch-start network (cheap merges, in parallel); otherwise the starts are sent in one
+  // sequential pass and copied.
+  const bool replay = hint && tasks > 1;
   std::vector<Prefix> starts;
   starts.reserve(tasks);
-  {
+  if (replay) {
+    for (int t = 0; t < tasks; ++t) starts.emplace_back(net0, hint);
+  } else {
     Prefix pre(net0, hint);
     int done = 0;
     for (int t = 0; t < tasks; ++t) {
@@ -951,6 +958,8 @@ static AggCase plan_aggregation(const std::vector<Item> &items, const Net &net0,
           const int n0 = (int)((int64_t)(N + 1) * t / tasks), n1 = (int)((int64_t)(N + 1) * (t + 1) / tasks);
           if (n0 >= n1) return;
           Prefix &pre = starts[t];
+          if (replay)
+            for (int i = 0; i < n0; ++i) pre.extend(items, i, c, dsts);
           thread_local Transfer tr;
           std::unique_ptr<Net> scratch;                // reused across cases (keeps its buffers)
           for (int n = n0; n < n1; ++n) {
