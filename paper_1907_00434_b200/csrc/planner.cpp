@@ -570,11 +570,15 @@ struct OrderRes {
   std::vector<Send> sends;
 };
 
-// component transfers per scan worth a pool dispatch (MLF_PLAN_MIN_EVALS overrides; tuning)
+// component transfers per Alg. 2 scan worth a pool dispatch (MLF_PLAN_MIN_EVALS overrides).
+// Measured on a B200 box's host: with the per-class cache a scan re-evaluates ~5 classes, and
+// handing them to other cores costs about what it saves (config 4: 2.1 ms at 4 threads with or
+// without parallel scans) or more (config 5: 2.6 ms serial vs 3.0-3.3 ms at 4-8 threads), so
+// by default only scans of >= 256 component transfers go to the pool; Alg. 3's cases do.
 static int min_parallel_evals() {
   static const int v = [] {
     const char *e = getenv("MLF_PLAN_MIN_EVALS");
-    return e && atoi(e) > 0 ? atoi(e) : 32;
+    return e && atoi(e) > 0 ? atoi(e) : 256;
   }();
   return v;
 }

@@ -3,7 +3,8 @@
 (1) one-way: the fused commit on cuda:0 with its 16 operands in cuda:1's HBM;
 (2) two-way: the same commit on cuda:0 (operands on cuda:1) and, at the same time, on cuda:1
     (operands on cuda:0) — every byte a GPU reads crosses NVLink, in both directions at once;
-(3) the same two-way pattern with TMA bulk copies and with copy engines (no commit arithmetic).
+(3) the same two-way pattern with TMA bulk copies and with copy engines (no commit arithmetic),
+    pulled by the reader or pushed by the owner (remote writes instead of remote reads).
 Per case: device time (CUDA events, max over the two GPUs), per-direction GB/s, and the NVLink
 data counters of both GPUs from `nvidia-smi nvlink -gt d` (KiB transmitted / received over all
 links) read before and after the timed repetitions.  Prints one JSON line.  Needs >= 2 GPUs."""
@@ -97,10 +98,19 @@ def main():
         return lambda d: fn(d, dst[d].data_ptr(), slots[1 - d].data_ptr(), nbytes,
                             torch.cuda.current_stream(torch.device("cuda", d)).cuda_stream)
 
+    def push_with(fn):
+        # the same bytes moved by the SOURCE GPU: it reads its own HBM and writes into the peer
+        return lambda d: fn(d, dst[1 - d].data_ptr(), slots[d].data_ptr(), nbytes,
+                            torch.cuda.current_stream(torch.device("cuda", d)).cuda_stream)
+
     res = {"bytes_per_direction": nbytes, "operands": W}
     cases = (("commit_one_way", (0,), commit), ("commit_two_way", (0, 1), commit),
              ("tma_bulk_two_way", (0, 1), copy_with(m.copy_bulk)), ("copy_engine_two_way", (0, 1), copy_with(m.copy_engine)),
-             ("tma_bulk_one_way", (0,), copy_with(m.copy_bulk)))
+             ("tma_bulk_one_way", (0,), copy_with(m.copy_bulk)),
+             ("tma_bulk_push_two_way", (0, 1), push_with(m.copy_bulk)),
+             ("sm_store_push_two_way", (0, 1), push_with(m.copy_kernel)),
+             ("copy_engine_push_two_way", (0, 1), push_with(m.copy_engine)),
+             ("tma_bulk_push_one_way", (0,), push_with(m.copy_bulk)))
     for name, devs, fn in cases:
         timed(devs, fn)                                     # warm-up
         for d in (0, 1):
