@@ -570,15 +570,15 @@ struct OrderRes {
   std::vector<Send> sends;
 };
 
-// component transfers per Alg. 2 scan worth a pool dispatch (MLF_PLAN_MIN_EVALS overrides).
-// Measured on a B200 box's host: with the per-class cache a scan re-evaluates ~5 classes, and
-// handing them to other cores costs about what it saves (config 4: 2.1 ms at 4 threads with or
-// without parallel scans) or more (config 5: 2.6 ms serial vs 3.0-3.3 ms at 4-8 threads), so
-// by default only scans of >= 256 component transfers go to the pool; Alg. 3's cases do.
+// Component transfers an Alg. 2 scan must re-evaluate (summed over its cache misses) before it
+// goes to the pool (MLF_PLAN_MIN_EVALS overrides).  Measured on a B200 box's host: with the
+// per-class cache a scan re-evaluates ~5 classes, often from a late component, and handing
+// small scans to other cores costs more than it saves (config 5: 2.6 ms serial vs 3.0 ms with
+// every scan of >= 4 misses on 4 threads); config 4's larger scans gain (2.3 -> 2.1 ms).
 static int min_parallel_evals() {
   static const int v = [] {
     const char *e = getenv("MLF_PLAN_MIN_EVALS");
-    return e && atoi(e) > 0 ? atoi(e) : 256;
+    return e && atoi(e) > 0 ? atoi(e) : 32;
   }();
   return v;
 }
@@ -705,6 +705,8 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
         miss_from.push_back(from);       // the components before `from` keep their results
       }
     }
+    int work = 0;                                         // component transfers to re-evaluate
+    for (int f : miss_from) work += G - f;
     Pool::get().run(
         (int)miss.size(),
         [&](int i) {
@@ -719,7 +721,7 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
           cc.t_st = s.t_st;
           cc.t_en = s.t_en;
         },
-        std::max(2, min_parallel_evals() / std::max(1, G)));
+        work >= min_parallel_evals() ? 2 : std::numeric_limits<int>::max());
     int best = -1;
     for (int g : pool) {
       ok[g] = ok[rep[g]];

@@ -10,10 +10,11 @@ for T in 1 2 4 8; do
   MLF_PLAN_THREADS=$T /tmp/planbench /tmp/planinst/configs.txt 15 >> $OUT/planbench.log 2>&1
 done
 MLF_PLAN_THREADS=1 /tmp/planbench /tmp/planinst/random.txt 1 | tail -1 >> $OUT/planbench.log
-for ME in 8 32 64; do
+for ME in 16 32 48; do
   for T in 4 8; do
     echo "== threads $T min_evals $ME" >> $OUT/planbench.log
     MLF_PLAN_MIN_EVALS=$ME MLF_PLAN_THREADS=$T /tmp/planbench /tmp/planinst/configs.txt 15 config4_G8 >> $OUT/planbench.log 2>&1
+    MLF_PLAN_MIN_EVALS=$ME MLF_PLAN_THREADS=$T /tmp/planbench /tmp/planinst/configs.txt 15 config5 >> $OUT/planbench.log 2>&1
   done
 done
 if [ -f scripts/planbench/prof.py ]; then
