@@ -10,17 +10,21 @@
 // Compiled with -ffp-contract=off so the only floating point (the divergence
 // bound) is evaluated exactly in the documented order.
 //
-// Performance (planning is O(#U^2 * G) transfer evaluations):
-//  * a candidate's tentative reservation is never materialised: evaluations read
-//    the residual as base profile minus a short list of pending reservation
-//    segments (the candidate's earlier components, the look-ahead's g*), with
-//    monotone per-link cursors instead of repeated binary searches;
-//  * the ShrtUp/ShrtDline candidate scans and the #U+1 DetAgg cases ("can be
-//    parallelized") run on a thread pool; results are reduced in
-//    index order, so the plan equals the sequential one bit for bit (ties ->
-//    lowest index, R6/R14);
-//  * DetAgg(n) shares its n-update direct prefix with DetAgg(n-1): each worker
-//    thread extends one prefix state incrementally instead of re-sending it.
+// Performance (planning is O(#U^2 * G) transfer evaluations).  Every item
+// below is exact — the plan equals the plain sequential one bit for bit (scripts/planbench
+// replays 3074 instances; the oracle tests compare with oracle/):
+//  * a candidate's tentative reservation is never materialised: evaluations read the residual
+//    as the link's step profile minus the pending reservations (step profiles too), walked
+//    with cursors; a saturated link makes the walk jump to that link's next change;
+//  * NetUp merges all of a link's reserved segments in one canonical pass (a canonical
+//    profile is unique, so the application order never changes a later t_en);
+//  * Alg. 2 caches each class's send with its walk and per-link slacks: after a reservation,
+//    unchanged leading components are kept and only the rest re-evaluated, and g*'s own
+//    reservation is replayed from its record;
+//  * Alg. 3 replays Alg. 2's reservations as its direct prefix (R10), prunes cases whose
+//    running t_max exceeds the best total, and keeps the argmin case instead of recomputing;
+//  * large ShrtUp/ShrtDline scans and the #U+1 DetAgg cases ("can be parallelized",
+//    P:1664-1668) run on a thread pool, reduced in index order (ties -> lowest index, R6/R14).
 #include "planner.h"
 
 #include <algorithm>
