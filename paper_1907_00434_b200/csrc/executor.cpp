@@ -680,7 +680,74 @@ static void pipeline_commit(mlf_ctx *c, const mlf_plan_out *p, const std::vector
 // by chunk and double-buffered, while the commit kernel folds the previous chunk with the
 // local operands straight from HBM.  Same arithmetic and order as the peer-load path (the
 // kernel sees a different pointer per operand, nothing else); only the transport differs.
+// Whole-slice staging (MLF_STAGE_WHOLE=1, when the staging buffer holds every remote slice):
+// each remote operand's slice of this shard is pulled by a copy engine in ONE copy, in commit
+// order over the copy streams, and the fold runs in groups of consecutive commits, each waiting
+// only for its own operands' copies (w is read and written once per group).  The idea: one big
+// copy per direction runs at ~775 GB/s with both directions loaded where SM peer reads reach
+// ~640 (scripts/nvlink_bidir_probe.py).  Measured at config 3 on 2 GPUs it is slower than the
+// fold and the chunked form (2544 vs 2707 / 2599 GB/s; 14.45 ms for 1-4 streams and 4-8 groups
+// alike: 32 concurrent 287 MB copies per GPU move ~650 GB/s), so it stays an option.  Same
+// kernel, order and roundings as the other transports.
+static constexpr int kStageGroups = 4;
+
+static bool staged_commit_whole(mlf_ctx *c, const std::vector<CommitOp> &ops, int boundary, float *backup) {
+  const int64_t e = (int64_t)c->elem_bytes, n = c->cfg.shard_elems;
+  const char *sw = getenv("MLF_STAGE_WHOLE");
+  if (!(sw && atoi(sw) == 1)) return false;
+  const int64_t stride = (n + 4095) / 4096 * 4096;     // elements per row: 16-byte and tile aligned
+  std::vector<int> row(ops.size(), -1);
+  int n_remote = 0;
+  for (size_t q = 0; q < ops.size(); ++q)
+    if (ops[q].home >= 0 && ops[q].home != c->cfg.rank) row[q] = n_remote++;
+  if (n_remote == 0 || n == 0 || n_remote * stride * e > c->cfg.stage_bytes) return false;
+  const char *gs = getenv("MLF_STAGE_GROUPS"), *ss = getenv("MLF_STAGE_STREAMS");   // A/B knobs
+  const int groups = gs && atoi(gs) > 0 ? atoi(gs) : kStageGroups;
+  const size_t nstreams = std::min(c->s_copy.size(), (size_t)(ss && atoi(ss) > 0 ? atoi(ss) : (int)c->s_copy.size()));
+  // groups of consecutive commits with about 1/groups of the remote bytes each
+  std::vector<size_t> cut;                             // group g = ops[cut[g], cut[g+1])
+  cut.push_back(0);
+  int seen = 0;
+  for (size_t q = 0; q < ops.size(); ++q) {
+    if (row[q] >= 0) ++seen;
+    if ((ops[q].flag & kOpLast) && q + 1 < ops.size() &&
+        seen * groups >= n_remote * (int)cut.size() && (int)cut.size() < groups)
+      cut.push_back(q + 1);
+  }
+  cut.push_back(ops.size());
+  record_start(c);
+  size_t ev = 0;
+  const cudaEvent_t begin = pipe_event(c, ev++);
+  CK(cudaEventRecord(begin, c->stream));               // peers' updates are complete (phase events)
+  for (auto s : c->s_copy) CK(cudaStreamWaitEvent(s, begin, 0));
+  std::vector<CommitOp> sops = ops;
+  char *stage = static_cast<char *>(c->cfg.stage_buf);
+  const int64_t src = c->cfg.shard_begin;
+  for (size_t g = 0; g + 1 < cut.size(); ++g) {
+    for (size_t q = cut[g]; q < cut[g + 1]; ++q) {
+      if (row[q] < 0) continue;
+      char *dst = stage + (size_t)row[q] * stride * e;
+      CK(cudaMemcpyAsync(dst, static_cast<const char *>(ops[q].ptr) + src * e, (size_t)(n * e),
+                         cudaMemcpyDeviceToDevice, c->s_copy[row[q] % nstreams]));
+      c->staged += n * e;
+      // the kernel reads op + src_off * e: shift the row pointer so that lands on the row
+      sops[q].ptr = reinterpret_cast<const void *>(reinterpret_cast<uintptr_t>(dst) - (uintptr_t)(src * e));
+    }
+    for (size_t k = 0; k < nstreams; ++k) {
+      const cudaEvent_t in = pipe_event(c, ev++);
+      CK(cudaEventRecord(in, c->s_copy[k]));
+      CK(cudaStreamWaitEvent(c->stream, in, 0));
+    }
+    const std::vector<CommitOp> part(sops.begin() + (std::ptrdiff_t)cut[g], sops.begin() + (std::ptrdiff_t)cut[g + 1]);
+    // the pre-batch mirror store (boundary 0) belongs to the first pass, the fused get to the last
+    const int b = boundary == 0 ? (g == 0 ? 0 : -1) : boundary;
+    launch_ops(c, c->cfg.model_shard, backup, part, b, g + 2 == cut.size());
+  }
+  return true;
+}
+
 static void staged_commit(mlf_ctx *c, const std::vector<CommitOp> &ops, int boundary, float *backup) {
+  if (staged_commit_whole(c, ops, boundary, backup)) return;
   const int64_t e = (int64_t)c->elem_bytes, n = c->cfg.shard_elems;
   std::vector<int> row(ops.size(), -1);
   int n_remote = 0;

@@ -87,7 +87,8 @@ class ShardedWorkload:
                  fused_get: bool = False, stage_mib: int = 0, multicast: bool = False):
         """mode: "fold" (SM peer loads inside the commit kernel), "tree" (tree_reduce on the
         aggregator GPU first) or "staged" (fold whose remote operand slices are pulled by the
-        copy engines into a local staging buffer of stage_mib MiB, default 4096)."""
+        copy engines into a local staging buffer of stage_mib MiB; 0 = large enough for every
+        remote slice, so each is pulled in one copy)."""
         assert cfg["G"] == world, "config shard count must equal the world size"
         self.cfg, self.rank, self.world, self.ctrl, self.mode = cfg, rank, world, ctrl, mode
         dev = torch.device("cuda", device)
@@ -113,7 +114,13 @@ class ShardedWorkload:
             self.n_retain = cfg.get("n_retain", max(len(local), 1) * 2)
             self.retain = torch.empty((self.n_retain, -(-S // 64) * 64), dtype=tdt, device=dev)
         self.n_slots = agg_slots_needed(cfg, world) if mode == "tree" else 0
-        self.stage = (torch.empty((stage_mib or 4096) << 18, dtype=torch.float32, device=dev)
+        if mode == "staged" and not stage_mib:
+            # room for every remote operand's slice of this shard (whole-slice staging: one big
+            # copy per operand), rows rounded to 4096 elements; at least 64 MiB
+            n_sh = cfg["shards"][rank][1]
+            stride = -(-max(n_sh, 1) // 4096) * 4096
+            stage_mib = max(64, -(-((W - len(local)) * stride * e) // (1 << 20)))
+        self.stage = (torch.empty(stage_mib << 18, dtype=torch.float32, device=dev)
                       if mode == "staged" else None)
         # fused get: every GPU holds a full-length view of the model, written by all shards' commits
         self.view = torch.empty(-(-S // 64) * 64, dtype=torch.float32, device=dev) if fused_get else None

@@ -13,10 +13,10 @@ pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-def _run(nproc, *args, timeout=600):
+def _run(nproc, *args, timeout=600, extra_env=None):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", "--nnodes=1",
            f"--nproc-per-node={nproc}", os.path.join(HERE, "multigpu_check.py"), *args]
-    env = dict(os.environ, MASTER_ADDR="127.0.0.1", OMP_NUM_THREADS="1")
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", OMP_NUM_THREADS="1", **(extra_env or {}))
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     return r.stdout
@@ -58,6 +58,15 @@ def test_two_ranks_bf16_16kb_layout():
     out = _run(2, "--cid", "3", "--S", "40000000", "--steps", "1", "--dtype", "bf16", "--modes", "fold,staged",
                timeout=900)
     assert "MULTIGPU_OK fold" in out and "MULTIGPU_OK staged" in out
+
+
+def test_two_ranks_staged_whole_slices():
+    # MLF_STAGE_WHOLE=1: one copy-engine copy per remote operand slice, the fold in groups of
+    # commits (the pre-batch mirror store in the first group only), bf16 and fp32
+    for dt in ("f32", "bf16"):
+        out = _run(2, "--cid", "5", "--S", "300007", "--modes", "staged", "--workers", "64", "--dtype", dt,
+                   extra_env={"MLF_STAGE_WHOLE": "1"})
+        assert "MULTIGPU_OK staged" in out
 
 
 def test_two_ranks_staged_minimum_chunk():
