@@ -12,7 +12,7 @@
 //
 // Performance (planning is O(#U^2 * G) transfer evaluations).  Every item
 // below is exact — the plan equals the plain sequential one bit for bit (scripts/planbench
-// replays 3074 instances; the oracle tests compare with oracle/):
+// replays 3074 instances; tests/ compares plans with the CPU oracle):
 //  * a candidate's tentative reservation is never materialised: evaluations read the residual
 //    as the link's step profile minus the pending reservations (step profiles too), walked
 //    with cursors; a saturated link makes the walk jump to that link's next change;
