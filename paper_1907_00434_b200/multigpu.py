@@ -214,12 +214,17 @@ class ShardedWorkload:
         pd = None
         if self.rank == 0:
             t0 = time.perf_counter()
-            pb = wl.plan(iteration)
+            try:
+                pb = wl.plan(iteration)
+                pd = pb.to_dict(self.cfg["W"])
+            except m.MlfError as e:            # every rank raises the same error, none hangs
+                pd = {"_error": (e.code, str(e).split(": ", 1)[-1])}
             self.last_plan_ms = (time.perf_counter() - t0) * 1e3
-            pd = pb.to_dict(self.cfg["W"])
         obj = [pd]
         dist.broadcast_object_list(obj, src=0, group=self.ctrl)
         pd = obj[0]
+        if "_error" in pd:
+            raise m.MlfError(*pd["_error"])
         if self.rank != 0:
             pb = m.plan_from_dict(pd)
             self.last_plan_ms = 0.0
