@@ -749,10 +749,15 @@ static bool staged_commit_whole(mlf_ctx *c, const std::vector<CommitOp> &ops, in
 static void staged_commit(mlf_ctx *c, const std::vector<CommitOp> &ops, int boundary, float *backup) {
   if (staged_commit_whole(c, ops, boundary, backup)) return;
   const int64_t e = (int64_t)c->elem_bytes, n = c->cfg.shard_elems;
+  // MLF_STAGE_EVERY=k (A/B knob, default 1): only every k-th remote operand is pulled by the
+  // copy engines, the others stay SM peer loads in the same kernel — the two transports then
+  // share the NVLink ingress
+  const char *se = getenv("MLF_STAGE_EVERY");
+  const int every = se && atoi(se) > 0 ? atoi(se) : 1;
   std::vector<int> row(ops.size(), -1);
-  int n_remote = 0;
+  int n_remote = 0, seen_remote = 0;
   for (size_t q = 0; q < ops.size(); ++q)
-    if (ops[q].home >= 0 && ops[q].home != c->cfg.rank) row[q] = n_remote++;
+    if (ops[q].home >= 0 && ops[q].home != c->cfg.rank && seen_remote++ % every == 0) row[q] = n_remote++;
   constexpr int64_t kAlign = 4096;                 // elements: keeps every row 16-byte (and tile) aligned
   int64_t C = n_remote ? c->cfg.stage_bytes / (2 * n_remote * e) : 0;
   // at least 4 chunks per shard (the last chunk's fold is not overlapped); larger copies run

@@ -60,6 +60,10 @@ struct PlanFail {
 // ---------------------------------------------------------------- thread pool
 // Persistent workers; run(n, f) calls f(i) for i in [0, n) and returns when all
 // are done.  Concurrent callers (mlf_plan is reentrant) fall back to serial.
+// Items are claimed from one atomic word (job generation << 32 | next item), so a job ends
+// when its items are done, not when every worker has checked in: a worker that is asleep or
+// late simply finds nothing left (the caller takes every item itself if need be), and a late
+// claim can never hit the next job (its generation differs, the CAS fails).
 class Pool {
  public:
   static Pool &get() {
@@ -72,22 +76,21 @@ class Pool {
       for (int i = 0; i < n; ++i) f(i);
       return;
     }
-    {
-      std::lock_guard<std::mutex> g(m_);
-      job_ = &f;
-      n_ = n;
-      next_.store(0);
-      pending_.store((int)th_.size());
-      gen_.fetch_add(1, std::memory_order_release);
+    job_ = &f;
+    n_.store(n, std::memory_order_relaxed);
+    // items per claim: few enough claims that the claim word does not bounce between cores for
+    // every ~50 ns item, enough chunks to balance uneven items
+    chunk_.store(std::max(1, n / (4 * threads())), std::memory_order_relaxed);
+    done_.store(0, std::memory_order_relaxed);
+    const uint64_t g = ++gen_;
+    state_.store(g << 32, std::memory_order_seq_cst);     // publishes job_ and n_
+    if (sleepers_.load(std::memory_order_seq_cst) > 0) {
+      std::lock_guard<std::mutex> lk(m_);
+      cv_.notify_all();
     }
-    cv_.notify_all();
-    work();
-    // the scans of one ordering step are tens of microseconds: spin before sleeping
-    for (int spin = 0; pending_.load(std::memory_order_acquire) != 0 && spin < kSpin; ++spin) relax();
-    if (pending_.load(std::memory_order_acquire) != 0) {
-      std::unique_lock<std::mutex> g(m_);
-      done_.wait(g, [&] { return pending_.load() == 0; });
-    }
+    work(g);
+    // items other workers claimed are still running: they take microseconds
+    while (done_.load(std::memory_order_acquire) < n) relax();
     job_ = nullptr;
     busy_.unlock();
   }
@@ -104,19 +107,32 @@ class Pool {
     for (int i = 0; i < t; ++i) th_.emplace_back([this] { loop(); });
   }
   ~Pool() {
+    stop_flag_.store(true, std::memory_order_seq_cst);
     {
-      std::lock_guard<std::mutex> g(m_);
-      stop_ = true;
-      ++gen_;
+      std::lock_guard<std::mutex> lk(m_);
+      cv_.notify_all();
     }
-    cv_.notify_all();
     for (auto &t : th_) t.join();
   }
-  void work() {
+  // claim the next items [i, e) of job generation g (false: none left, or that job is over)
+  bool claim(uint64_t g, int &i, int &e) {
+    uint64_t s = state_.load(std::memory_order_acquire);
     for (;;) {
-      int i = next_.fetch_add(1);
-      if (i >= n_) return;
-      (*job_)(i);
+      const int n = n_.load(std::memory_order_relaxed), at = (int)(uint32_t)s;
+      if ((s >> 32) != g || at >= n) return false;
+      const int k = std::min(chunk_.load(std::memory_order_relaxed), n - at);
+      if (state_.compare_exchange_weak(s, s + (uint64_t)k, std::memory_order_acq_rel, std::memory_order_acquire)) {
+        i = at;
+        e = at + k;
+        return true;
+      }
+    }
+  }
+  void work(uint64_t g) {
+    int i, e;
+    while (claim(g, i, e)) {
+      for (int q = i; q < e; ++q) (*job_)(q);   // valid: the job cannot end before these are done
+      done_.fetch_add(e - i, std::memory_order_release);
     }
   }
   static void relax() {
@@ -128,30 +144,38 @@ class Pool {
     uint64_t seen = 0;
     for (;;) {
       // spin for the next job (a plan's scans come back to back), then sleep
-      for (int spin = 0; gen_.load(std::memory_order_acquire) == seen && spin < kSpin; ++spin) relax();
-      {
-        std::unique_lock<std::mutex> g(m_);
-        cv_.wait(g, [&] { return stop_ || gen_.load() != seen; });
-        if (stop_) return;
-        seen = gen_.load();
+      uint64_t g = seen;
+      for (int spin = 0;; ++spin) {
+        if (stop_flag_.load(std::memory_order_acquire)) return;
+        g = state_.load(std::memory_order_acquire) >> 32;
+        if (g != seen) break;
+        if (spin < kSpin) {
+          relax();
+          continue;
+        }
+        std::unique_lock<std::mutex> lk(m_);
+        sleepers_.fetch_add(1, std::memory_order_seq_cst);
+        cv_.wait(lk, [&] {
+          return stop_flag_.load(std::memory_order_seq_cst) || (state_.load(std::memory_order_seq_cst) >> 32) != seen;
+        });
+        sleepers_.fetch_sub(1, std::memory_order_seq_cst);
+        spin = 0;
       }
-      work();
-      if (pending_.fetch_sub(1, std::memory_order_acq_rel) == 1) {
-        std::lock_guard<std::mutex> g(m_);
-        done_.notify_one();
-      }
+      seen = g;
+      work(g);
     }
   }
   static constexpr int kSpin = 4000;               // tens of microseconds of pause instructions
   std::vector<std::thread> th_;
   std::mutex m_, busy_;
-  std::condition_variable cv_, done_;
+  std::condition_variable cv_;
   const std::function<void(int)> *job_ = nullptr;
-  int n_ = 0;
-  std::atomic<int> pending_{0};
-  std::atomic<int> next_{0};
-  std::atomic<uint64_t> gen_{0};
-  bool stop_ = false;
+  uint64_t gen_ = 0;                               // written by the caller holding busy_ only
+  alignas(64) std::atomic<uint64_t> state_{0};
+  std::atomic<int> n_{0}, chunk_{1};
+  alignas(64) std::atomic<int> done_{0};
+  alignas(64) std::atomic<int> sleepers_{0};
+  std::atomic<bool> stop_flag_{false};
 };
 
 // ---------------------------------------------------------------- network
@@ -237,12 +261,40 @@ struct TSeg {
 // range.  The function is exactly the one of adding the segments one by one, and a canonical
 // profile is unique, so the representation (hence every later t_en) does not depend on the
 // order in which reservations were applied.
+struct Transfer {
+  i64 t_st = 0, t_en = 0;
+  Path path;
+  std::vector<TSeg> segs;
+};
+
+struct Ev {
+  i64 t, d;
+};
+// Per-thread scratch buffers of the hot functions.  Reached through a constant-initialised
+// thread_local pointer, so an access is one TLS load (a thread_local std::vector would go
+// through the TLS init wrapper on every call); created on a thread's first use, freed at its exit.
+struct Scratch {
+  std::vector<Ev> ev;
+  Profile tmp;
+  std::vector<TSeg> segs_apply, segs_send;
+  std::vector<i64> comp, take;
+  Transfer tr_send;
+};
+static thread_local Scratch *t_scratch = nullptr;
+static Scratch *make_scratch() {
+  static thread_local std::unique_ptr<Scratch> owner;
+  owner.reset(new Scratch());
+  return t_scratch = owner.get();
+}
+static inline Scratch &scratch() {
+  Scratch *s = t_scratch;
+  return __builtin_expect(s != nullptr, 1) ? *s : *make_scratch();
+}
+
 static void combine(Profile &p, const TSeg *s, int m, int sign) {
-  struct Ev {
-    i64 t, d;
-  };
-  thread_local std::vector<Ev> ev;
-  thread_local Profile tmp;
+  Scratch &S = scratch();
+  std::vector<Ev> &ev = S.ev;
+  Profile &tmp = S.tmp;
   ev.clear();
   for (int i = 0; i < m; ++i)
     if (s[i].r != 0 && s[i].a < s[i].b) {
@@ -306,12 +358,6 @@ struct Pending {
     used[nkeys].assign(1, Seg{0, 0});
     return used[nkeys++];
   }
-};
-
-struct Transfer {
-  i64 t_st = 0, t_en = 0;
-  Path path;
-  std::vector<TSeg> segs;
 };
 
 // cursor over a step profile: i = the segment holding the current time
@@ -438,7 +484,7 @@ static bool transfer(const Net &net, const Pending *L0, const Pending *L1, i64 s
 
 // O2: NetUp — subtract reservations from the residual profiles.
 static void apply_pending(Net &net, const Pending &P) {
-  thread_local std::vector<TSeg> segs;
+  std::vector<TSeg> &segs = scratch().segs_apply;
   for (int i = 0; i < P.nkeys; ++i) {
     const Profile &u = P.used[i];
     segs.clear();
@@ -511,9 +557,10 @@ static void rec_segs(const SendRec &rec, const CompRec &cr, std::vector<TSeg> &s
 static bool send(const Net &net, const Pending *L0, const Ctx &c, const std::vector<int> &dsts, int src, i64 size,
                  i64 t_avail, Send &out, Pending &local, bool record_all = true, SendRec *rec = nullptr,
                  int from = 0) {
-  thread_local std::vector<i64> comp;
-  thread_local Transfer tr;
-  thread_local std::vector<TSeg> segs;
+  Scratch &S = scratch();
+  Transfer &tr = S.tr_send;
+  std::vector<i64> &comp = S.comp;
+  std::vector<TSeg> &segs = S.segs_send;
   component_bytes(size, c.weights, c.wsum, comp);
   local.clear();
   out.t_st = T_INF;
@@ -565,6 +612,23 @@ struct Item {
 };
 
 // ---------------------------------------------------------------- O3 ordering
+// What Alg. 3 needs from the networks Alg. 2 passes through (R10: case n starts from the
+// batch-start network with the first n kept updates sent direct, which is exactly Alg. 2's NW
+// after its n-th kept update).  Filled by order_final when given:
+//  * snaps[j]: NW after j*kEvery kept updates (a case replays at most kEvery-1 reservations);
+//  * tmax[n]: the direct prefix's t_max (the largest t_en of kept updates 0..n-1);
+//  * dead[n]: case n ends at its first tail item — that item cannot reach aggs[0] by tmax[n]
+//    and group 1 would be empty (R12, det_agg_tail's first step on the same network);
+//  * last: NW after every kept update (the all-direct case's network).
+struct AggProbe {
+  static constexpr int kEvery = 8;
+  const std::vector<int> *aggs = nullptr;
+  std::vector<Net> snaps;
+  std::vector<i64> tmax;
+  std::vector<uint8_t> dead;
+  std::unique_ptr<Net> last;
+};
+
 struct OrderRes {
   std::vector<int> order;
   std::vector<uint8_t> reason;
@@ -592,9 +656,14 @@ static int min_parallel_evals() {
 // walk step no path link loses more than its slack; components are reserved one after another,
 // so an unchanged prefix also leaves the next component's inputs unchanged.  Saturated
 // stretches were skipped by the walk and stay saturated.  The unchanged components' slacks are
-// reduced by what M takes, so the record describes the send on the new network.
-static int first_changed(SendRec &rec, const Pending &M) {
-  thread_local std::vector<i64> take;
+// reduced by what M takes, so the record describes the send on the new network; each reduction
+// is appended to `log` (if given) so that it can be undone.
+struct TakeLog {
+  int w, k;
+  i64 amount;
+};
+static int first_changed(SendRec &rec, const Pending &M, std::vector<TakeLog> *log = nullptr) {
+  std::vector<i64> &take = scratch().take;
   for (size_t j = 0; j < rec.comps.size(); ++j) {
     const CompRec &cr = rec.comps[j];
     take.assign((size_t)(cr.w1 - cr.w0) * 3, 0);
@@ -613,12 +682,18 @@ static int first_changed(SendRec &rec, const Pending &M) {
       }
     }
     for (int w = cr.w0; w < cr.w1; ++w)
-      for (int k = 0; k < cr.path.nk; ++k) rec.walk[w].slack[k] -= take[(size_t)(w - cr.w0) * 3 + k];
+      for (int k = 0; k < cr.path.nk; ++k) {
+        const i64 t = take[(size_t)(w - cr.w0) * 3 + k];
+        if (!t) continue;
+        rec.walk[w].slack[k] -= t;
+        if (log) log->push_back({w, k, t});
+      }
   }
   return (int)rec.comps.size();
 }
 
-static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 tau, i64 v_init) {
+static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 tau, i64 v_init,
+                            AggProbe *probe = nullptr) {
   const int n = (int)batch.size();
   std::vector<i64> dl(n);
   for (int g = 0; g < n; ++g) dl[g] = batch[g].version + tau - v_init;
@@ -628,10 +703,9 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
   res.reason.assign(n, 0);
   Net nw(&c.d);
   i64 p = 1;
-  const int G = (int)c.servers.size();
   std::vector<i64> ten(n);
   std::vector<uint8_t> ok(n);
-  std::vector<int> pool, uniq, miss, miss_from, rep(n, -1);
+  std::vector<int> pool, uniq, miss, rep(n, -1);
   // t_en is a pure function of (network, node, size, t_avail): updates sharing the triple
   // (virtual workers on one GPU usually share all three) form one class, evaluated once per scan
   std::vector<int> cls(n), cls_rep, cls_stamp;
@@ -659,13 +733,21 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
   int scan = 0;
   // Per-class result cache.  Network states get ids: nw_id = NW, la_id = NW + the look-ahead's
   // reservation of g*; NW takes la_id when g* is kept and keeps nw_id when it is dropped.
+  // A look-ahead scan moves classes from NW to NW + g*; when g* is then dropped the network is
+  // NW again, so the scan keeps what it overwrote: the NW record of every class it re-evaluated
+  // (bk) and every slack reduction it made (takes), and a drop puts both back.
   struct ClassCache {
     int tag = -1;
     i64 t_st = 0, t_en = 0;
     SendRec rec;
+    bool moved = false, backed = false;      // this look-ahead moved it to la_id / saved its record
+    i64 bk_t_st = 0, bk_t_en = 0;
+    SendRec bk;
+    std::vector<TakeLog> takes;
   };
   std::vector<ClassCache> cache(cls_rep.size());
   int nw_id = 0, la_id = 0, next_id = 1;
+  std::vector<int> la_moved;                 // classes the current look-ahead moved to la_id
 
   // ShrtDline(pos, cands, NW + L0): the due set's argmin if any, else ShrtUp (R4, R6).
   auto pick = [&](i64 pos, const std::vector<int> &cands, const Pending *L0) -> int {
@@ -691,41 +773,56 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
       rep[g] = cls_rep[k];
     }
     // a class evaluated on NW (tag nw_id) keeps its result on NW + L0 when L0 = the look-ahead's
-    // reservation costs none of its walk steps more than their slack (send_unchanged); the
-    // others are evaluated again, on the pool when there are enough of them
+    // reservation costs none of its walk steps more than their slack (first_changed); the others
+    // are evaluated again from their first changed component.  Validation and re-evaluation of a
+    // class are one task; the scan's tasks run on the pool when there are enough of them.
     const int tag = L0 ? la_id : nw_id;
     miss.clear();
-    miss_from.clear();
     for (int g : uniq) {
       ClassCache &cc = cache[cls[g]];
-      int from = 0;
-      if (cc.tag != tag && L0 && cc.tag == nw_id) from = first_changed(cc.rec, *L0);
-      if (cc.tag == tag || (L0 && cc.tag == nw_id && from == (int)cc.rec.comps.size())) {
-        cc.tag = tag;
+      if (cc.tag == tag) {
         ok[g] = 1;
         ten[g] = cc.t_en;
       } else {
         miss.push_back(g);
-        miss_from.push_back(from);       // the components before `from` keep their results
       }
     }
-    int work = 0;                                         // component transfers to re-evaluate
-    for (int f : miss_from) work += G - f;
     Pool::get().run(
         (int)miss.size(),
         [&](int i) {
           thread_local Pending local;
           const int g = miss[i];
           ClassCache &cc = cache[cls[g]];
-          Send s;
+          int from = 0;
+          const bool on_nw = L0 && cc.tag == nw_id;
+          cc.moved = on_nw;
+          cc.backed = false;
+          if (on_nw) {
+            cc.takes.clear();
+            from = first_changed(cc.rec, *L0, &cc.takes);
+            if (from == (int)cc.rec.comps.size()) {
+              cc.tag = tag;
+              ok[g] = 1;
+              ten[g] = cc.t_en;
+              return;
+            }
+            cc.backed = true;
+            cc.bk = cc.rec;
+            cc.bk_t_st = cc.t_st;
+            cc.bk_t_en = cc.t_en;
+          }
+          Send s;                                  // the components before `from` keep their results
           ok[g] = send(nw, L0, c, c.servers, batch[g].node, batch[g].size, batch[g].t_avail, s, local, false,
-                       &cc.rec, miss_from[i]);
+                       &cc.rec, from);
           ten[g] = s.t_en;
           cc.tag = ok[g] ? tag : -1;
           cc.t_st = s.t_st;
           cc.t_en = s.t_en;
         },
-        work >= min_parallel_evals() ? 2 : std::numeric_limits<int>::max());
+        (int)miss.size() >= min_parallel_evals() ? 2 : std::numeric_limits<int>::max());
+    if (L0)
+      for (int g : miss)
+        if (cache[cls[g]].moved) la_moved.push_back(cls[g]);
     int best = -1;
     for (int g : pool) {
       ok[g] = ok[rep[g]];
@@ -777,6 +874,7 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
     bool drop = false;
     int g_next = -1;
     la_id = next_id++;
+    la_moved.clear();
     if (!cands.empty()) {
       g_next = pick(p + 1, cands, &star);              // on NetUp(NW, g*)
       if (t_star > ten[g_next]) drop = true;           // Alg. 2 line 10
@@ -784,7 +882,35 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
     unproc.erase(std::find(unproc.begin(), unproc.end(), g_star));
     if (drop) {
       res.reason[g_star] = 2;
+      // back to NW: restore what the look-ahead scan overwrote
+      for (int k : la_moved) {
+        ClassCache &cc = cache[k];
+        if (cc.backed) {
+          std::swap(cc.rec, cc.bk);
+          cc.t_st = cc.bk_t_st;
+          cc.t_en = cc.bk_t_en;
+        }
+        for (const TakeLog &t : cc.takes) cc.rec.walk[t.w].slack[t.k] += t.amount;
+        cc.tag = nw_id;
+      }
       continue;
+    }
+    if (probe) {
+      const int k = (int)res.order.size();               // g*'s position in O(U)
+      if (k % AggProbe::kEvery == 0) probe->snaps.push_back(nw);
+      const i64 tm = k == 0 ? 0 : std::max(probe->tmax[k - 1], res.sends[k - 1].t_en);
+      probe->tmax.push_back(tm);
+      bool dead = false;
+      if (k > 0) {
+        thread_local Transfer tr;
+        const Item &it = batch[g_star];
+        try {
+          dead = !transfer(nw, nullptr, nullptr, it.size, it.node, (*probe->aggs)[0], it.t_avail, tr) || tr.t_en > tm;
+        } catch (const PlanFail &) {
+          dead = false;                                    // the case itself reports it, if it runs
+        }
+      }
+      probe->dead.push_back(dead);
     }
     res.order.push_back(g_star);
     apply_pending(nw, star);
@@ -794,6 +920,13 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
     res.sends.push_back(s_star);
     ++p;
     cached = g_next;
+  }
+  if (probe) {
+    const int N = (int)res.order.size();
+    if (N % AggProbe::kEvery == 0) probe->snaps.push_back(nw);
+    probe->tmax.push_back(N == 0 ? 0 : std::max(probe->tmax[N - 1], res.sends[N - 1].t_en));
+    probe->dead.push_back(0);
+    probe->last = std::make_unique<Net>(std::move(nw));
   }
   return res;
 }
@@ -909,13 +1042,19 @@ static AggCase det_agg(int n, const std::vector<Item> &items, const Net &net0, c
 }
 
 // Alg. 3 lines 21-24: all |U|+1 cases, argmin total, ties -> smallest n (R14).
+static AggCase plan_aggregation_probed(const std::vector<Item> &items, const Ctx &c, const std::vector<int> &dsts,
+                                       const std::vector<int> &aggs, Net *net_out, const PrefixHint &hint,
+                                       AggProbe &pr);
+
 static AggCase plan_aggregation(const std::vector<Item> &items, const Net &net0, const Ctx &c,
                                 const std::vector<int> &dsts, const std::vector<int> &aggs, Net *net_out,
-                                bool record = false, const PrefixHint *hint = nullptr) {
+                                bool record = false, const PrefixHint *hint = nullptr, AggProbe *probe = nullptr) {
   const int N = (int)items.size();
   // no aggregators: every case n < |U| meets aid = 1 > k at its first tail item (R12), so
   // only the all-direct case is feasible
   if (aggs.empty()) return det_agg(N, items, net0, c, dsts, aggs, net_out, record);
+  if (probe && hint && !record && (int)probe->tmax.size() == N + 1)
+    return plan_aggregation_probed(items, c, dsts, aggs, net_out, *hint, *probe);
   std::vector<i64> totals(N + 1, -1);
   // contiguous ranges of n per task; the prefix states at the range starts are built in
   // one sequential pass, then every task extends its own copy incrementally
@@ -1029,6 +1168,78 @@ static AggCase plan_aggregation(const std::vector<Item> &items, const Net &net0,
         return std::move(b.cs);
       }
   return det_agg(best, items, net0, c, dsts, aggs, net_out, record);
+}
+
+// Alg. 3's argmin over n with Alg. 2's networks at hand (AggProbe): only the cases that get past
+// their first tail item run, each from the nearest snapshot plus at most kEvery-1 replayed
+// reservations, all independent (one pool task per case, in increasing n so the pruning bound
+// tightens early).  Same cases, same networks, same pruning rule and tie-break as
+// plan_aggregation, so the same argmin; the argmin's case is run once more for its plan.
+static AggCase plan_aggregation_probed(const std::vector<Item> &items, const Ctx &c, const std::vector<int> &dsts,
+                                       const std::vector<int> &aggs, Net *net_out, const PrefixHint &hint,
+                                       AggProbe &pr) {
+  const int N = (int)items.size();
+  std::vector<int> live;
+  for (int n = 0; n <= N; ++n)
+    if (!pr.dead[n]) live.push_back(n);
+  std::vector<i64> totals(N + 1, -1);
+  totals[N] = pr.tmax[N];                        // all direct: feasible, total = the largest t_en
+  std::atomic<i64> best_total{pr.tmax[N]};
+  std::atomic<bool> failed{false};
+  PlanFail first_err{MLF_OK, ""};
+  std::mutex err_m;
+  // case n on `nw`: the network after its direct prefix, then the tail
+  auto run_case = [&](int n, Net &nw, i64 cut, AggCase &cs) {
+    const int j = n / AggProbe::kEvery;
+    nw = pr.snaps[j];
+    for (int i = j * AggProbe::kEvery; i < n; ++i) apply_pending(nw, (*hint.res)[i]);
+    cs.n = n;
+    cs.commits.clear();
+    for (int i = 0; i < n; ++i) cs.commits.push_back({i, 1, 0, (*hint.sends)[i]});
+    det_agg_tail(cs, nw, pr.tmax[n], items, c, dsts, aggs, cut);
+  };
+  const bool small = (N + 1) * (int)dsts.size() < 256;
+  Pool::get().run(
+      (int)live.size(),
+      [&](int q) {
+        const int n = live[q];
+        if (n == N) return;
+        try {
+          const i64 cut = best_total.load(std::memory_order_relaxed);
+          if (pr.tmax[n] > cut) return;                // total >= tmax[n] > the best so far
+          thread_local std::unique_ptr<Net> nw;
+          if (!nw) nw = std::make_unique<Net>(pr.snaps[0]);
+          AggCase cs;
+          run_case(n, *nw, cut, cs);
+          if (!cs.feasible) return;
+          totals[n] = cs.total;
+          i64 cur = best_total.load(std::memory_order_relaxed);
+          while (cs.total < cur && !best_total.compare_exchange_weak(cur, cs.total, std::memory_order_relaxed)) {
+          }
+        } catch (const PlanFail &e) {
+          std::lock_guard<std::mutex> g(err_m);
+          if (!failed.exchange(true)) first_err = e;
+        }
+      },
+      small ? std::numeric_limits<int>::max() : 2);
+  if (failed.load()) throw first_err;
+  int best = -1;
+  for (int n = 0; n <= N; ++n)
+    if (totals[n] >= 0 && (best < 0 || totals[n] < totals[best])) best = n;
+  AggCase cs;
+  if (best == N) {
+    cs.n = N;
+    for (int i = 0; i < N; ++i) cs.commits.push_back({i, 1, 0, (*hint.sends)[i]});
+    cs.feasible = true;
+    cs.total = pr.tmax[N];
+    if (net_out) *net_out = std::move(*pr.last);
+    return cs;
+  }
+  Net nw(pr.snaps[0]);
+  run_case(best, nw, T_INF, cs);
+  if (!cs.feasible || cs.total != totals[best]) throw PlanFail{MLF_E_INVALID, "internal: aggregation case changed"};
+  if (net_out) *net_out = std::move(nw);
+  return cs;
 }
 
 static std::vector<i64> chained_times(const std::vector<CommitRec> &cm) {
@@ -1166,11 +1377,13 @@ static mlf_status plan_impl(const mlf_net *net, const mlf_batch *batch, const ml
   // 1. ordering
   // (sync mode: no ordering — the list in submission order, nothing dropped)
   OrderRes ores;
+  AggProbe probe;
+  probe.aggs = &c.aggs;
   if (prm->sync_mode) {
     for (int g = 0; g < n; ++g) ores.order.push_back(g);
     ores.reason.assign(n, 0);
   } else {
-    ores = order_final(c, items, prm->tau_max, prm->v_init);
+    ores = order_final(c, items, prm->tau_max, prm->v_init, c.aggs.empty() ? nullptr : &probe);
   }
   std::vector<Item> ordered;
   for (int g : ores.order) ordered.push_back(items[g]);
@@ -1179,7 +1392,7 @@ static mlf_status plan_impl(const mlf_net *net, const mlf_batch *batch, const ml
   Net after(&c.d);
   PrefixHint hint{&ores.res, &ores.sends};
   AggCase cs = plan_aggregation(ordered, net0, c, c.servers, c.aggs, &after, false,
-                                prm->sync_mode ? nullptr : &hint);
+                                prm->sync_mode ? nullptr : &hint, prm->sync_mode ? nullptr : &probe);
   std::vector<i64> times = chained_times(cs.commits);
 
   out->n_commit = (int)ores.order.size();

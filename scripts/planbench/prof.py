@@ -18,7 +18,7 @@ sub('#include "planner.h"', '''#include "planner.h"
 #include <chrono>
 #include <cstdio>
 static long N_tr = 0, N_it = 0, N_tr_ord = 0, N_comb = 0;
-static double T_ord = 0, T_agg = 0, T_rep = 0, T_all = 0;
+static double T_ord = 0, T_agg = 0, T_rep = 0, T_all = 0, T_scan = 0, T_star = 0, T_app = 0, T_pick = 0;
 static int NCALL = 0;
 struct Dump {
   ~Dump() {
@@ -26,16 +26,19 @@ struct Dump {
       fprintf(stderr, "per plan: all %.3f ms = ordering %.3f + aggregation %.3f + replica %.3f + rest; "
               "transfers %ld (ordering %ld), walk steps %ld, profile merges %ld\\n", T_all / NCALL, T_ord / NCALL,
               T_agg / NCALL, T_rep / NCALL, N_tr / NCALL, N_tr_ord / NCALL, N_it / NCALL, N_comb / NCALL);
+    if (NCALL)
+      fprintf(stderr, "  ordering: picks %.3f ms (of which class tasks %.3f), g* reservation %.3f, NetUp+copy %.3f\\n",
+              T_pick / NCALL, T_scan / NCALL, T_star / NCALL, T_app / NCALL);
   }
 } g_dump;
 #define NOW std::chrono::steady_clock::now()
 #define MS(a, b) std::chrono::duration<double, std::milli>(b - a).count()''')
-sub('''    ores = order_final(c, items, prm->tau_max, prm->v_init);''',
-    '''    auto t0 = NOW; long n0 = N_tr; ores = order_final(c, items, prm->tau_max, prm->v_init);
+sub('''    ores = order_final(c, items, prm->tau_max, prm->v_init, c.aggs.empty() ? nullptr : &probe);''',
+    '''    auto t0 = NOW; long n0 = N_tr; ores = order_final(c, items, prm->tau_max, prm->v_init, c.aggs.empty() ? nullptr : &probe);
     T_ord += MS(t0, NOW); N_tr_ord += N_tr - n0;''')
 sub('''  AggCase cs = plan_aggregation(ordered, net0, c, c.servers, c.aggs, &after, false,
-                                prm->sync_mode ? nullptr : &hint);''', '''  auto ta = NOW; AggCase cs = plan_aggregation(ordered, net0, c, c.servers, c.aggs, &after, false,
-                                prm->sync_mode ? nullptr : &hint); T_agg += MS(ta, NOW);''')
+                                prm->sync_mode ? nullptr : &hint, prm->sync_mode ? nullptr : &probe);''', '''  auto ta = NOW; AggCase cs = plan_aggregation(ordered, net0, c, c.servers, c.aggs, &after, false,
+                                prm->sync_mode ? nullptr : &hint, prm->sync_mode ? nullptr : &probe); T_agg += MS(ta, NOW);''')
 sub('''    AggCase rc = plan_aggregation(ritems, after, c, c.replicas, c.raggs, nullptr);''',
     '''    auto tr_ = NOW; AggCase rc = plan_aggregation(ritems, after, c, c.replicas, c.raggs, nullptr); T_rep += MS(tr_, NOW);''')
 sub('''  try {
@@ -51,4 +54,34 @@ sub('''    if (r < 0) throw PlanFail{MLF_E_INVALID, "internal: negative residual
     if (r < 0) throw PlanFail{MLF_E_INVALID, "internal: negative residual"};''')
 sub('''  if (ev.empty()) return;''', '''  __atomic_add_fetch(&N_comb, 1, __ATOMIC_RELAXED);
   if (ev.empty()) return;''')
+# ordering sub-phases (present in the round-2 planner; skipped silently otherwise)
+def opt(old, new):
+    global s
+    if old in s:
+        s = s.replace(old, new, 1)
+opt('''    Pool::get().run(
+        (int)miss.size(),''', '''    auto tsc = NOW;
+    struct ScanT { std::chrono::steady_clock::time_point t; ~ScanT() { T_scan += MS(t, NOW); } };
+    ScanT scan_t{tsc};
+    Pool::get().run(
+        (int)miss.size(),''')
+opt('''    const int g_star = cached >= 0 ? cached : pick(p, unproc, nullptr);''', '''    auto tp0 = NOW;
+    const int g_star = cached >= 0 ? cached : pick(p, unproc, nullptr);
+    T_pick += MS(tp0, NOW);
+    auto tst = NOW;''')
+opt('''    cands.clear();
+    for (int g : unproc)
+      if (g != g_star && dl[g] >= p + 1) cands.push_back(g);''', '''    T_star += MS(tst, NOW);
+    cands.clear();
+    for (int g : unproc)
+      if (g != g_star && dl[g] >= p + 1) cands.push_back(g);''')
+opt('''      g_next = pick(p + 1, cands, &star);              // on NetUp(NW, g*)''', '''      auto tp1 = NOW;
+      g_next = pick(p + 1, cands, &star);              // on NetUp(NW, g*)
+      T_pick += MS(tp1, NOW);''')
+opt('''    res.order.push_back(g_star);
+    apply_pending(nw, star);''', '''    res.order.push_back(g_star);
+    auto tap = NOW;
+    apply_pending(nw, star);''')
+opt('''    res.sends.push_back(s_star);''', '''    res.sends.push_back(s_star);
+    T_app += MS(tap, NOW);''')
 sys.stdout.write(s)

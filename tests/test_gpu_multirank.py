@@ -69,6 +69,14 @@ def test_two_ranks_staged_whole_slices():
         assert "MULTIGPU_OK staged" in out
 
 
+def test_two_ranks_staged_every_third_remote_operand():
+    # MLF_STAGE_EVERY=3: a third of the remote operands staged by the copy engines, the rest read
+    # over the peer mappings by the same kernel
+    out = _run(2, "--cid", "3", "--S", "300007", "--modes", "staged", "--stage-mib", "4", "--workers", "32",
+               extra_env={"MLF_STAGE_EVERY": "3"})
+    assert "MULTIGPU_OK staged" in out
+
+
 def test_two_ranks_staged_minimum_chunk():
     # copy-engine staging with a 2 MiB buffer: 4096-element chunks, many of them, ragged tail
     out = _run(2, "--cid", "3", "--S", "300007", "--modes", "staged", "--stage-mib", "2", "--workers", "32")
