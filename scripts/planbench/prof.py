@@ -1,6 +1,8 @@
 """Print planner.cpp with phase timers (ordering / server aggregation / replica plan) and work
 counters (transfers, walk steps, profile merges) added; planbench links it instead of the real
-planner to show where a plan's time goes.  usage: python scripts/planbench/prof.py > /tmp/planner_prof.cpp"""
+planner to show where a plan's time goes.  usage: python scripts/planbench/prof.py [--light] > /tmp/planner_prof.cpp
+--light: the three phase timers only (no per-transfer counters, no per-scan timers), for
+multi-threaded runs where contended counters would distort the timing."""
 import os
 import sys
 
@@ -46,6 +48,10 @@ sub('''  try {
     return plan_impl(net, batch, params, out);''', '''  try {
     g_plan_err.clear();
     NCALL++; auto t2 = NOW; auto r = plan_impl(net, batch, params, out); T_all += MS(t2, NOW); return r;''')
+LIGHT = "--light" in sys.argv
+if LIGHT:
+    def sub(old, new):  # noqa: F811 — counters and scan timers off
+        pass
 sub('''  const NetDef &d = *net.def;
   out.segs.clear();''', '''  const NetDef &d = *net.def;
   __atomic_add_fetch(&N_tr, 1, __ATOMIC_RELAXED);
@@ -59,6 +65,11 @@ def opt(old, new):
     global s
     if old in s:
         s = s.replace(old, new, 1)
+
+
+if LIGHT:
+    def opt(old, new):  # noqa: F811
+        pass
 opt('''    Pool::get().run(
         (int)miss.size(),''', '''    auto tsc = NOW;
     struct ScanT { std::chrono::steady_clock::time_point t; ~ScanT() { T_scan += MS(t, NOW); } };
