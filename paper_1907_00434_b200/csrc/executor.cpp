@@ -760,9 +760,16 @@ static void staged_commit(mlf_ctx *c, const std::vector<CommitOp> &ops, int boun
     if (ops[q].home >= 0 && ops[q].home != c->cfg.rank && seen_remote++ % every == 0) row[q] = n_remote++;
   constexpr int64_t kAlign = 4096;                 // elements: keeps every row 16-byte (and tile) aligned
   int64_t C = n_remote ? c->cfg.stage_bytes / (2 * n_remote * e) : 0;
-  // at least 4 chunks per shard (the last chunk's fold is not overlapped); larger copies run
-  // closer to the copy engine's peak (measured per-copy: 16 MiB 586, 64 MiB 691, 1 GiB 732 GB/s)
-  C = std::min(C, std::max(kAlign, ((n + 3) / 4 + kAlign - 1) / kAlign * kAlign));
+  // at least 4 chunks per shard (MLF_STAGE_CHUNKS; the last chunk's fold is not overlapped);
+  // larger copies run closer to the copy engine's peak (measured per-copy: 16 MiB 586, 64 MiB
+  // 691, 1 GiB 732 GB/s)
+  const char *sc = getenv("MLF_STAGE_CHUNKS");
+  const int64_t chunks = sc && atoi(sc) > 0 ? atoi(sc) : 4;
+  C = std::min(C, std::max(kAlign, ((n + chunks - 1) / chunks + kAlign - 1) / kAlign * kAlign));
+  // MLF_STAGE_FIRST_DIRECT=1: the first chunk is folded with every operand read over the peer
+  // mappings (nothing to wait for), while the copy engines already pull the second chunk
+  const char *fd = getenv("MLF_STAGE_FIRST_DIRECT");
+  const bool first_direct = fd && atoi(fd) == 1;
   C -= C % kAlign;
   if (n_remote == 0 || n == 0 || C < kAlign) {     // nothing remote, or staging too small: SM peer loads
     launch_ops(c, c->cfg.model_shard, backup, ops, boundary, true);
@@ -779,6 +786,12 @@ static void staged_commit(mlf_ctx *c, const std::vector<CommitOp> &ops, int boun
   int k = 0;
   for (int64_t off = 0; off < n; off += C, ++k) {
     const int64_t len = std::min(C, n - off), src = c->cfg.shard_begin + off;
+    if (k == 0 && first_direct) {
+      launch_ops(c, c->cfg.model_shard, backup, ops, boundary, true, off, len);
+      kdone.push_back(pipe_event(c, ev++));
+      CK(cudaEventRecord(kdone.back(), c->stream));
+      continue;
+    }
     char *base = stage + (size_t)(k % 2) * n_remote * C * e;
     if (k >= 2)                                    // the buffer's previous chunk has been folded
       for (auto s : c->s_copy) CK(cudaStreamWaitEvent(s, kdone[k - 2], 0));
