@@ -74,54 +74,31 @@ class Pool {
     return p;
   }
   int threads() const { return (int)th_.size() + 1; }
-  // the calling thread's index: 0 for any thread outside the pool, 1.. for the workers
-  static int tid() { return t_tid_; }
-  // Idle work: while waiting for the next job a worker calls (*h)(tid) from time to time.  One
-  // hook at a time (install returns false if another is set); remove() returns once no worker
-  // is inside the hook any more.
-  bool install_idle(const std::function<void(int)> *h) {
-    const std::function<void(int)> *none = nullptr;
-    return idle_.compare_exchange_strong(none, h);
-  }
-  void remove_idle(const std::function<void(int)> *h) {
-    const std::function<void(int)> *cur = h;
-    if (!idle_.compare_exchange_strong(cur, nullptr)) return;
-    while (idle_users_.load(std::memory_order_seq_cst) != 0) relax();
-  }
-  // owner (optional): item i runs on thread owner[i] % threads() (0 = the caller), so that data
-  // an item writes stays in one core's cache from one job to the next; used only while every
-  // worker is awake (a sleeping one would hold its items back), else items are claimed
-  void run(int n, const std::function<void(int)> &f, int min_parallel, const int *owner = nullptr) {
+  void run(int n, const std::function<void(int)> &f, int min_parallel) {
     if (n < min_parallel || th_.empty() || !busy_.try_lock()) {
       for (int i = 0; i < n; ++i) f(i);
       return;
     }
     // the job's generations are even; first the state takes the odd one before it, so that no
     // claim still in flight for the previous job can succeed (its CAS compares against a state
-    // word read before this store) while job_, owner_ and n_ are rewritten
+    // word read before this store) while job_ and n_ are rewritten
     gen_ += 2;
     const uint64_t g = gen_;
     state_.store((g - 1) << 32, std::memory_order_seq_cst);
     job_ = &f;
-    const bool aff = owner && sleepers_.load(std::memory_order_seq_cst) == 0;
-    owner_.store(aff ? owner : nullptr, std::memory_order_relaxed);
     n_.store(n, std::memory_order_relaxed);
     // items per claim: few enough claims that the claim word does not bounce between cores for
     // every ~50 ns item, enough chunks to balance uneven items
     chunk_.store(std::max(1, n / (4 * threads())), std::memory_order_relaxed);
     done_.store(0, std::memory_order_relaxed);
-    aff_out_.store(0, std::memory_order_relaxed);
-    state_.store(g << 32 | (aff ? kAffinity : 0), std::memory_order_seq_cst);   // publishes job_, n_, owner_
+    state_.store(g << 32, std::memory_order_seq_cst);     // publishes job_ and n_
     if (sleepers_.load(std::memory_order_seq_cst) > 0) {
       std::lock_guard<std::mutex> lk(m_);
       cv_.notify_all();
     }
-    work(g, 0);
-    // items other workers claimed are still running: they take microseconds; an affinity job
-    // also waits for every worker to have finished reading its owner list
-    while (done_.load(std::memory_order_acquire) < n ||
-           (owner_.load(std::memory_order_relaxed) && aff_out_.load(std::memory_order_acquire) < (int)th_.size()))
-      relax();
+    work(g);
+    // items other workers claimed are still running: they take microseconds
+    while (done_.load(std::memory_order_acquire) < n) relax();
     job_ = nullptr;
     busy_.unlock();
   }
@@ -135,10 +112,7 @@ class Pool {
     if (const char *lw = getenv("LOCAL_WORLD_SIZE")) total = std::max(1, total / std::max(1, atoi(lw)));
     if (const char *pt = getenv("MLF_PLAN_THREADS")) total = std::max(1, std::min(32, atoi(pt)));
     int t = total - 1;
-    for (int i = 0; i < t; ++i) th_.emplace_back([this, i] {
-      t_tid_ = i + 1;
-      loop(i + 1);
-    });
+    for (int i = 0; i < t; ++i) th_.emplace_back([this] { loop(); });
   }
   ~Pool() {
     stop_flag_.store(true, std::memory_order_seq_cst);
@@ -162,25 +136,7 @@ class Pool {
       }
     }
   }
-  void work(uint64_t g, int tid) {
-    // The mode comes from job g's own state word: a worker late for a claim job g may already
-    // see the next job's owner_, job_ and n_ being written.  An affinity job cannot end without
-    // this worker, so while the state says (g, affinity) those fields are g's.
-    const uint64_t s = state_.load(std::memory_order_acquire);
-    if ((s >> 32) != g) return;
-    if (s & kAffinity) {
-      const int *own = owner_.load(std::memory_order_relaxed);
-      const int n = n_.load(std::memory_order_relaxed), T = threads();
-      int mine = 0;
-      for (int q = 0; q < n; ++q)
-        if (own[q] % T == tid) {
-          (*job_)(q);
-          ++mine;
-        }
-      if (mine) done_.fetch_add(mine, std::memory_order_release);
-      if (tid != 0) aff_out_.fetch_add(1, std::memory_order_release);
-      return;
-    }
+  void work(uint64_t g) {
     int i, e;
     while (claim(g, i, e)) {
       for (int q = i; q < e; ++q) (*job_)(q);   // valid: the job cannot end before these are done
@@ -192,7 +148,7 @@ class Pool {
     __builtin_ia32_pause();
 #endif
   }
-  void loop(int tid) {
+  void loop() {
     uint64_t seen = 0;
     for (;;) {
       // spin for the next job (a plan's scans come back to back), then sleep
@@ -202,11 +158,6 @@ class Pool {
         g = state_.load(std::memory_order_acquire) >> 32;
         if (g != seen && !(g & 1)) break;                // odd: a job is being set up
         if (spin < kSpin) {
-          if ((spin & 31) == 31) {
-            idle_users_.fetch_add(1, std::memory_order_seq_cst);
-            if (const std::function<void(int)> *h = idle_.load(std::memory_order_seq_cst)) (*h)(tid);
-            idle_users_.fetch_sub(1, std::memory_order_seq_cst);
-          }
           relax();
           continue;
         }
@@ -220,29 +171,21 @@ class Pool {
         spin = 0;
       }
       seen = g;
-      work(g, tid);
+      work(g);
     }
   }
   static constexpr int kSpin = 4000;               // tens of microseconds of pause instructions
-  static constexpr uint64_t kAffinity = 1ull << 31; // state word: this job's items go by owner
   std::vector<std::thread> th_;
   std::mutex m_, busy_;
   std::condition_variable cv_;
   const std::function<void(int)> *job_ = nullptr;
-  std::atomic<const int *> owner_{nullptr};         // affinity job (see run)
-  static thread_local int t_tid_;
-  std::atomic<const std::function<void(int)> *> idle_{nullptr};
-  std::atomic<int> idle_users_{0};
   uint64_t gen_ = 0;                               // written by the caller holding busy_ only
   alignas(64) std::atomic<uint64_t> state_{0};
   std::atomic<int> n_{0}, chunk_{1};
   alignas(64) std::atomic<int> done_{0};
-  std::atomic<int> aff_out_{0};
   alignas(64) std::atomic<int> sleepers_{0};
   std::atomic<bool> stop_flag_{false};
 };
-
-thread_local int Pool::t_tid_ = 0;
 
 // ---------------------------------------------------------------- network
 struct Seg {
@@ -779,7 +722,7 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
   i64 p = 1;
   std::vector<i64> ten(n);
   std::vector<uint8_t> ok(n);
-  std::vector<int> pool, uniq, miss, owner, rep(n, -1);
+  std::vector<int> pool, uniq, miss, rep(n, -1);
   // t_en is a pure function of (network, node, size, t_avail): updates sharing the triple
   // (virtual workers on one GPU usually share all three) form one class, evaluated once per scan
   std::vector<int> cls(n), cls_rep, cls_stamp;
@@ -820,42 +763,6 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
     std::vector<TakeLog> takes;
   };
   std::vector<ClassCache> cache(cls_rep.size());
-  // Worker replicas of NW.  NetUp rewrites a few profiles every step on this thread; a worker
-  // reading them would pull every rewritten line over from this core.  Instead each worker keeps
-  // its own copy of NW and applies the kept reservations to it itself (the same merges in the
-  // same order, so the same canonical profiles), mostly while it waits for the next scan.
-  // res.res never reallocates (reserved), and `pub` counts the reservations final in it.
-  res.res.reserve(n);
-  const Pending *res_base = res.res.data();
-  std::atomic<int> pub{0};
-  struct alignas(64) Replica {
-    std::unique_ptr<Net> net;
-    int applied = 0;
-  };
-  std::vector<Replica> reps(Pool::get().threads());
-  auto replica = [&](int tid) -> const Net & {
-    if (tid <= 0 || tid >= (int)reps.size()) return nw;
-    Replica &r = reps[tid];
-    if (!r.net) r.net = std::make_unique<Net>(&c.d);     // NW before the first kept update
-    const int upto = pub.load(std::memory_order_acquire);
-    for (; r.applied < upto; ++r.applied) apply_pending(*r.net, res_base[r.applied]);
-    return *r.net;
-  };
-  const std::function<void(int)> idle = [&](int tid) {
-    try {
-      replica(tid);
-    } catch (const PlanFail &) {
-      reps[tid].net.reset();                             // the task redoes it and reports the error
-      reps[tid].applied = 0;
-    }
-  };
-  struct IdleGuard {
-    const std::function<void(int)> *h;
-    bool on;
-    ~IdleGuard() {
-      if (on) Pool::get().remove_idle(h);
-    }
-  } idle_guard{&idle, Pool::get().install_idle(&idle)};
   PlanFail task_err{MLF_OK, ""};
   std::atomic<bool> task_failed{false};
   int nw_id = 0, la_id = 0, next_id = 1;
@@ -899,9 +806,6 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
         miss.push_back(g);
       }
     }
-    // a class is always evaluated on the same thread: its record stays in that core's cache
-    owner.resize(miss.size());
-    for (size_t i = 0; i < miss.size(); ++i) owner[i] = cls[miss[i]];
     Pool::get().run(
         (int)miss.size(),
         [&](int i) {
@@ -928,8 +832,8 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
           }
           Send s;                                  // the components before `from` keep their results
           try {
-            ok[g] = send(replica(Pool::tid()), L0, c, c.servers, batch[g].node, batch[g].size, batch[g].t_avail, s,
-                         local, false, &cc.rec, from);
+            ok[g] = send(nw, L0, c, c.servers, batch[g].node, batch[g].size, batch[g].t_avail, s, local, false,
+                         &cc.rec, from);
           } catch (const PlanFail &e) {
             if (!task_failed.exchange(true)) task_err = e;
             ok[g] = 1;
@@ -940,7 +844,7 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
           cc.t_st = s.t_st;
           cc.t_en = s.t_en;
         },
-        (int)miss.size() >= min_parallel_evals() ? 2 : std::numeric_limits<int>::max(), owner.data());
+        (int)miss.size() >= min_parallel_evals() ? 2 : std::numeric_limits<int>::max());
     if (task_failed.load()) throw task_err;
     if (L0)
       for (int g : miss)
@@ -1050,7 +954,6 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
     nw_id = la_id;
     res.res.emplace_back();
     std::swap(res.res.back(), star);                   // star is rebuilt for the next g*
-    pub.store((int)res.res.size(), std::memory_order_release);
     res.sends.push_back(s_star);
     ++p;
     cached = g_next;

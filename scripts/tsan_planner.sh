@@ -14,3 +14,8 @@ TSAN_LIB=$(g++ -print-file-name=libtsan.so)
 MLF_LIB=$PWD/paper_1907_00434_b200/build/libmlfplan_tsan.so LD_PRELOAD="$TSAN_LIB" \
 TSAN_OPTIONS="halt_on_error=1 report_signal_unsafe=0" python -m pytest tests/test_planner_parity.py \
     tests/test_planner_distribution_parity.py -q -x -k "larger or 64 or box or degraded" -p no:cacheprovider
+# the NEXT-2 Div_max stream (32 classes per scan, replica plans, carried items) with every Alg. 2
+# scan on the pool: the case that exposed a late claim running an item of the next job
+MLF_LIB=$PWD/paper_1907_00434_b200/build/libmlfplan_tsan.so LD_PRELOAD="$TSAN_LIB" MLF_PLAN_THREADS=8 MLF_PLAN_MIN_EVALS=2 \
+TSAN_OPTIONS="halt_on_error=1 report_signal_unsafe=0" python -m pytest tests/test_replica_divmax_trend.py -q -x \
+    -p no:cacheprovider
