@@ -311,6 +311,54 @@ def run_single(a):
         T = sum(r["ms"] for r in recs)
         return cfg, recs, T, ck, kl
 
+    def writeback_inclusive(tau, dtype, kernel, gamma, steps=10):
+        """Kernel time with its deferred write-backs inside the window: events around [execute;
+        a 256 MiB read], minus events around [a one-element memset; the same read] after a flush,
+        plus the memset alone.  The read evicts every line the kernel left dirty in L2; the
+        memset stands in for the kernel so that the launch gap before the read cancels."""
+        os.environ["MLF_COMMIT_IMPL"] = kernel
+        cfg = configs.config(cid, G=1 if cid >= 3 else None, tau=tau, dtype=dtype, gamma=gamma)
+        wl = Workload(cfg, device=0)
+        wl.fill_updates(0)
+        st = torch.cuda.current_stream(dev)
+        tk, tr, tt, alg = [], [], [], []
+        tiny = flush_w[:1]
+        for s in range(3 + steps):
+            draws = wl.submit_all(s)
+            pb = wl.plan(s)
+            pd = pb.to_dict(cfg["W"])
+            l2_flush()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            wl.ctx.execute(pb)
+            flush_r.sum()
+            e1.record(st)
+            wl.ctx.sync()
+            wl.after_commit(pd, draws)
+            l2_flush()
+            e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e2.record(st)
+            tiny.zero_()
+            flush_r.sum()
+            e3.record(st)
+            e4, e5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e4.record(st)
+            tiny.zero_()
+            e5.record(st)
+            torch.cuda.synchronize()
+            if s >= 3:
+                tk.append(e0.elapsed_time(e1))
+                tr.append(e2.elapsed_time(e3))
+                tt.append(e4.elapsed_time(e5))
+                hist = 2 if gamma else 1
+                alg.append(sum(pd["commit_count"]) * wl.shard_elems * cfg["e"] + 2 * hist * wl.shard_elems * 4)
+        wl.ctx.close()
+        ms = (sum(tk) - sum(tr) + sum(tt)) / len(tk)
+        return {"ms_incl_writeback": round(ms, 4),
+                "frac_incl_writeback": round(sum(alg) / len(alg) / (ms / 1e3) / 1e9 / peak, 4),
+                "writeback_how": "events around [execute; 256 MiB read] - [1-element memset; the same read] + "
+                                 "[memset], mean of 10 steps"}
+
     def summarize(recs, T):
         v = sum(r["bytes"] for r in recs) / (T / 1e3) / 1e9
         ach = sum(r["alg"] for r in recs) / (T / 1e3) / 1e9
@@ -326,6 +374,7 @@ def run_single(a):
     alg = sum(r["alg"] for r in recs)
     wbytes = sum(r["wbytes"] for r in recs)
     achieved = alg / (T / 1e3) / 1e9
+    wb = writeback_inclusive(a.tau, a.dtype, a.kernel, a.gamma)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
@@ -350,7 +399,9 @@ def run_single(a):
                      # the copy peak is a 1:1 read/write ceiling and this pass is read-dominated; and
                      # ~4% of w's writes are still dirty in L2 when the kernel ends (drained by the
                      # untimed flush): the two figures below are the ones to read as a fraction
-                     **roofline_extras(alg / len(recs), wbytes / len(recs), T / len(recs), peak, traffic)},
+                     **roofline_extras(alg / len(recs), wbytes / len(recs), T / len(recs), peak, traffic),
+                     # the same kernel with the write-backs it leaves in L2 charged to it
+                     **wb},
         "planner_ms": round(sum(r["plan_ms"] for r in recs) / len(recs), 3),
         "step_ms_p10_p50_p90": [round(float(x), 4) for x in np.percentile([r["ms"] for r in recs], [10, 50, 90])],
         "gpu_launches": int(kl),

@@ -819,7 +819,7 @@ __device__ __forceinline__ void mom_fold_bf16_w(const uint8_t *st, int tid, int 
 }
 
 template <int kTile, int kStages, int kCW>
-__global__ void __launch_bounds__(kCW * 32 + 32, 1) fused_commit_momentum_bh(const __grid_constant__ MomentumArgs a) {
+__global__ void __launch_bounds__(kCW * 32 + 32, kCW <= 8 ? 2 : 1) fused_commit_momentum_bh(const __grid_constant__ MomentumArgs a) {
   constexpr int kCons = kCW * 32;
   constexpr int kStageBytes = kTile * 2;            // one bf16 operand tile
   constexpr int kHalf = kTile / 2;                  // fp32 elements per stage
@@ -1327,6 +1327,21 @@ cudaError_t launch_commit_momentum(const MomentumArgs &a, cudaStream_t s, int sm
   // (4 operands, a third of the stages are w and h) the 8-warp kernel wins, 97.8% vs 92.7%
   const char *wide = getenv("MLF_MOM_WIDE");
   const int wide_min = wide ? atoi(wide) : 6;
+  // MLF_MOM_BH2=1 (A/B knob): two CTAs per SM, each 8 consumer warps over a 12-stage ring of
+  // 8 KB bf16 stages (the same warps per SM, more registers per thread, two producers)
+  const char *bh2 = getenv("MLF_MOM_BH2");
+  if (all_bf16 && wide_min > 0 && a.n_ops >= wide_min && bh2 && atoi(bh2) == 1) {
+    constexpr int kT = 4096, kS = 12, kCW = 8;
+    constexpr size_t smem = (size_t)kS * kT * 2 + 2 * kS * sizeof(uint64_t);
+    static std::atomic<uint64_t> init{0};
+    if (cudaError_t e = ensure_smem(bulk::fused_commit_momentum_bh<kT, kS, kCW>, smem, init); e != cudaSuccess)
+      return e;
+    const int64_t n_tiles = ((a.n & ~int64_t(7)) + kT - 1) / kT;
+    const int ctas = 2 * (sm_count > 0 ? sm_count : 148);
+    const int grid = (int)(n_tiles < ctas ? (n_tiles > 0 ? n_tiles : 1) : ctas);
+    bulk::fused_commit_momentum_bh<kT, kS, kCW><<<grid, kCW * 32 + 32, smem, s>>>(a);
+    return cudaGetLastError();
+  }
   if (all_bf16 && wide_min > 0 && a.n_ops >= wide_min) {
     constexpr int kT = 8192, kS = 12, kCW = 16;
     constexpr size_t smem = (size_t)kS * kT * 2 + 2 * kS * sizeof(uint64_t);

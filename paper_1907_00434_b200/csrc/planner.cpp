@@ -723,6 +723,9 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
   std::vector<i64> ten(n);
   std::vector<uint8_t> ok(n);
   std::vector<int> pool, uniq, miss, rep(n, -1);
+  // with one server a class's send is one transfer (~0.3 us): too little to hand to the pool
+  // (config 2, tau 32: 0.13 ms serial vs 0.22 ms on 8 threads)
+  const bool multi_server = c.servers.size() > 1;
   // t_en is a pure function of (network, node, size, t_avail): updates sharing the triple
   // (virtual workers on one GPU usually share all three) form one class, evaluated once per scan
   std::vector<int> cls(n), cls_rep, cls_stamp;
@@ -844,7 +847,7 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
           cc.t_st = s.t_st;
           cc.t_en = s.t_en;
         },
-        (int)miss.size() >= min_parallel_evals() ? 2 : std::numeric_limits<int>::max());
+        multi_server && (int)miss.size() >= min_parallel_evals() ? 2 : std::numeric_limits<int>::max());
     if (task_failed.load()) throw task_err;
     if (L0)
       for (int g : miss)
