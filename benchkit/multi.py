@@ -367,6 +367,21 @@ def run_bench_multi(a):
     for i, mode in enumerate(modes):
         results[mode] = run(mode, a.steps if i == 0 else max(3, a.steps // 2), a.warmup if i == 0 else 2,
                             clocks=(i == 0))
+    if not a.no_variants:
+        # the mixed transport: every second remote operand pulled by the copy engines, the rest
+        # read over the peer mappings by the same kernel, the first chunk straight from the peers
+        mixed = {"MLF_STAGE_EVERY": "2", "MLF_STAGE_CHUNKS": "4", "MLF_STAGE_FIRST_DIRECT": "1"}
+        saved = {k: os.environ.get(k) for k in mixed}
+        os.environ.update(mixed)
+        try:
+            results["staged_mixed"] = run("staged", max(3, a.steps // 2), 2)
+        finally:
+            for k, v in saved.items():
+                if v is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = v
+        modes.append("staged_mixed")
     nb = None
     cfg0 = cfgs.config(cid, G=world, tau=a.tau, dtype=a.dtype)
     if not a.no_variants and dist.get_backend() == "nccl" and not cfg0["replica"]:

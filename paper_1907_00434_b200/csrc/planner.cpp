@@ -413,64 +413,53 @@ static bool transfer(const Net &net, const Pending *L0, const Pending *L1, i64 s
     return true;
   }
   // one cursor per (link, profile): the link's residual, then the reserved rates of L0 and L1
-  // on it (only those that exist); sign = +1 for a residual, -1 for a reservation.  The walk
-  // keeps each link's residual rks[k] at `cur` and each cursor's next breakpoint nt, and only
-  // advances the cursors whose breakpoint is reached.
+  // on it (only those that exist); cur[c].sign = +1 for a residual, -1 for a reservation
   struct C {
     const Seg *p;
     int n, i, link;
-    i64 sign, nt;
+    i64 sign;
   };
   C cs[9];
   Seg own[3];                 // pair links not reserved yet: their capacity
   int nc = 0;
   const int nk = out.path.nk;
-  i64 rks[3] = {0, 0, 0};
-  auto add = [&](const Seg *p, int n, int k, i64 sign) {
+  auto add = [&](const Profile *pr, int k, i64 sign) {
     C &c = cs[nc++];
-    c.p = p;
-    c.n = n;
-    const Seg *it = std::upper_bound(p, p + n, t_avail, [](i64 v, const Seg &x) { return v < x.t; });
-    c.i = it == p ? 0 : (int)(it - p) - 1;
+    c.p = pr->data();
+    c.n = (int)pr->size();
+    const Seg *it = std::upper_bound(c.p, c.p + c.n, t_avail, [](i64 v, const Seg &x) { return v < x.t; });
+    c.i = it == c.p ? 0 : (int)(it - c.p) - 1;
     c.link = k;
     c.sign = sign;
-    c.nt = c.i + 1 < n ? p[c.i + 1].t : T_INF;
-    rks[k] += sign * p[c.i].r;
   };
   for (int k = 0; k < nk; ++k) {
     const i64 key = out.path.key[k];
     if (const Profile *pr = net.get(key)) {
-      add(pr->data(), (int)pr->size(), k, +1);
+      add(pr, k, +1);
     } else {
       own[k] = Seg{0, std::max<i64>(net.capacity(key), 0)};
-      add(&own[k], 1, k, +1);
+      cs[nc++] = C{&own[k], 1, 0, k, +1};
     }
     if (L0)
-      if (const Profile *u = L0->find(key)) add(u->data(), (int)u->size(), k, -1);
+      if (const Profile *u = L0->find(key)) add(u, k, -1);
     if (L1)
-      if (const Profile *u = L1->find(key)) add(u->data(), (int)u->size(), k, -1);
+      if (const Profile *u = L1->find(key)) add(u, k, -1);
   }
-  // move every cursor to time t (t never decreases; cursors already there stay)
-  auto reach = [&](i64 t) {
-    for (int q = 0; q < nc; ++q) {
-      C &c = cs[q];
-      if (c.nt > t) continue;
-      rks[c.link] -= c.sign * c.p[c.i].r;
-      do ++c.i;
-      while (c.i + 1 < c.n && c.p[c.i + 1].t <= t);
-      rks[c.link] += c.sign * c.p[c.i].r;
-      c.nt = c.i + 1 < c.n ? c.p[c.i + 1].t : T_INF;
-    }
-  };
   i128 need = (i128)size * NS_PER_S;
   i64 cur = t_avail;
   bool started = false;
   for (;;) {
-    // r = the path minimum at cur, nb = its next possible change; while some link is saturated
-    // the path stays at 0 at least until every saturated link's own next change (zjump), so
-    // the walk jumps there instead of stepping through the other links' breakpoints
-    i64 nbk[3] = {T_INF, T_INF, T_INF};
-    for (int q = 0; q < nc; ++q) nbk[cs[q].link] = std::min(nbk[cs[q].link], cs[q].nt);
+    // rks[k] = link k's residual at cur, nbk[k] = its next possible change; r = the path
+    // minimum, nb = its next possible change; while some link is saturated the path stays at 0
+    // at least until every saturated link's own next change (zjump), so the walk jumps there
+    // instead of stepping through the other links' breakpoints
+    i64 rks[3] = {0, 0, 0}, nbk[3] = {T_INF, T_INF, T_INF};
+    for (int q = 0; q < nc; ++q) {
+      C &c = cs[q];
+      while (c.i + 1 < c.n && c.p[c.i + 1].t <= cur) ++c.i;
+      rks[c.link] += c.sign * c.p[c.i].r;
+      if (c.i + 1 < c.n && c.p[c.i + 1].t < nbk[c.link]) nbk[c.link] = c.p[c.i + 1].t;
+    }
     i64 r = T_INF, nb = T_INF, zjump = t_avail;
     for (int k = 0; k < nk; ++k) {
       if (rks[k] == 0) zjump = std::max(zjump, nbk[k]);
@@ -481,7 +470,6 @@ static bool transfer(const Net &net, const Pending *L0, const Pending *L1, i64 s
     if (r == 0) {
       if (zjump == T_INF) return false;          // a link on the path is saturated forever
       cur = zjump;
-      reach(cur);
       continue;
     }
     if (!started) {
@@ -500,7 +488,6 @@ static bool transfer(const Net &net, const Pending *L0, const Pending *L1, i64 s
     out.segs.push_back({cur, nb, r});
     if (rec) rec->push_back({cur, nb, r, {rks[0] - r, nk > 1 ? rks[1] - r : 0, nk > 2 ? rks[2] - r : 0}});
     cur = nb;
-    reach(cur);
   }
 }
 
@@ -514,6 +501,11 @@ static void apply_pending(Net &net, const Pending &P) {
       if (u[q].r) segs.push_back({u[q].t, u[q + 1].t, u[q].r});
     combine(net.mut(P.keys[i]), segs.data(), (int)segs.size(), -1);
   }
+}
+static void copy_pending(Pending &dst, const Pending &src) {
+  dst.nkeys = src.nkeys;
+  dst.keys.assign(src.keys.begin(), src.keys.begin() + src.nkeys);
+  dst.used.assign(src.used.begin(), src.used.begin() + src.nkeys);
 }
 static void apply_transfer(Net &net, const Transfer &tr) {
   for (int k = 0; k < tr.path.nk; ++k) combine(net.mut(tr.path.key[k]), tr.segs.data(), (int)tr.segs.size(), -1);
@@ -886,22 +878,11 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
     const ClassCache &cg = cache[cls[g_star]];
     if (cg.tag == nw_id) {
       // g*'s class was evaluated on exactly this network: its recorded walk is the reservation
-      // (one merge per link: up(src) carries every component's segments, a canonical profile
-      // is the same whatever the grouping)
       thread_local std::vector<TSeg> segs;
-      thread_local std::vector<i64> keys;
       star.clear();
-      keys.clear();
-      for (const CompRec &cr : cg.rec.comps)
-        for (int k = 0; k < cr.path.nk; ++k)
-          if (std::find(keys.begin(), keys.end(), cr.path.key[k]) == keys.end()) keys.push_back(cr.path.key[k]);
-      for (const i64 key : keys) {
-        segs.clear();
-        for (const CompRec &cr : cg.rec.comps)
-          for (int k = 0; k < cr.path.nk; ++k)
-            if (cr.path.key[k] == key)
-              for (int w = cr.w0; w < cr.w1; ++w) segs.push_back({cg.rec.walk[w].t0, cg.rec.walk[w].t1, cg.rec.walk[w].r});
-        combine(star.slot(key), segs.data(), (int)segs.size(), +1);
+      for (const CompRec &cr : cg.rec.comps) {
+        rec_segs(cg.rec, cr, segs);
+        for (int k = 0; k < cr.path.nk; ++k) combine(star.slot(cr.path.key[k]), segs.data(), (int)segs.size(), +1);
       }
       s_star.t_st = cg.t_st;
       s_star.t_en = cg.t_en;
@@ -956,7 +937,7 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
     apply_pending(nw, star);
     nw_id = la_id;
     res.res.emplace_back();
-    std::swap(res.res.back(), star);                   // star is rebuilt for the next g*
+    copy_pending(res.res.back(), star);
     res.sends.push_back(s_star);
     ++p;
     cached = g_next;
