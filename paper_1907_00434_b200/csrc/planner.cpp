@@ -413,53 +413,64 @@ static bool transfer(const Net &net, const Pending *L0, const Pending *L1, i64 s
     return true;
   }
   // one cursor per (link, profile): the link's residual, then the reserved rates of L0 and L1
-  // on it (only those that exist); cur[c].sign = +1 for a residual, -1 for a reservation
+  // on it (only those that exist); sign = +1 for a residual, -1 for a reservation.  The walk
+  // keeps each link's residual rks[k] at `cur` and each cursor's next breakpoint nt, and only
+  // advances the cursors whose breakpoint is reached.
   struct C {
     const Seg *p;
     int n, i, link;
-    i64 sign;
+    i64 sign, nt;
   };
   C cs[9];
   Seg own[3];                 // pair links not reserved yet: their capacity
   int nc = 0;
   const int nk = out.path.nk;
-  auto add = [&](const Profile *pr, int k, i64 sign) {
+  i64 rks[3] = {0, 0, 0};
+  auto add = [&](const Seg *p, int n, int k, i64 sign) {
     C &c = cs[nc++];
-    c.p = pr->data();
-    c.n = (int)pr->size();
-    const Seg *it = std::upper_bound(c.p, c.p + c.n, t_avail, [](i64 v, const Seg &x) { return v < x.t; });
-    c.i = it == c.p ? 0 : (int)(it - c.p) - 1;
+    c.p = p;
+    c.n = n;
+    const Seg *it = std::upper_bound(p, p + n, t_avail, [](i64 v, const Seg &x) { return v < x.t; });
+    c.i = it == p ? 0 : (int)(it - p) - 1;
     c.link = k;
     c.sign = sign;
+    c.nt = c.i + 1 < n ? p[c.i + 1].t : T_INF;
+    rks[k] += sign * p[c.i].r;
   };
   for (int k = 0; k < nk; ++k) {
     const i64 key = out.path.key[k];
     if (const Profile *pr = net.get(key)) {
-      add(pr, k, +1);
+      add(pr->data(), (int)pr->size(), k, +1);
     } else {
       own[k] = Seg{0, std::max<i64>(net.capacity(key), 0)};
-      cs[nc++] = C{&own[k], 1, 0, k, +1};
+      add(&own[k], 1, k, +1);
     }
     if (L0)
-      if (const Profile *u = L0->find(key)) add(u, k, -1);
+      if (const Profile *u = L0->find(key)) add(u->data(), (int)u->size(), k, -1);
     if (L1)
-      if (const Profile *u = L1->find(key)) add(u, k, -1);
+      if (const Profile *u = L1->find(key)) add(u->data(), (int)u->size(), k, -1);
   }
+  // move every cursor to time t (t never decreases; cursors already there stay)
+  auto reach = [&](i64 t) {
+    for (int q = 0; q < nc; ++q) {
+      C &c = cs[q];
+      if (c.nt > t) continue;
+      rks[c.link] -= c.sign * c.p[c.i].r;
+      do ++c.i;
+      while (c.i + 1 < c.n && c.p[c.i + 1].t <= t);
+      rks[c.link] += c.sign * c.p[c.i].r;
+      c.nt = c.i + 1 < c.n ? c.p[c.i + 1].t : T_INF;
+    }
+  };
   i128 need = (i128)size * NS_PER_S;
   i64 cur = t_avail;
   bool started = false;
   for (;;) {
-    // rks[k] = link k's residual at cur, nbk[k] = its next possible change; r = the path
-    // minimum, nb = its next possible change; while some link is saturated the path stays at 0
-    // at least until every saturated link's own next change (zjump), so the walk jumps there
-    // instead of stepping through the other links' breakpoints
-    i64 rks[3] = {0, 0, 0}, nbk[3] = {T_INF, T_INF, T_INF};
-    for (int q = 0; q < nc; ++q) {
-      C &c = cs[q];
-      while (c.i + 1 < c.n && c.p[c.i + 1].t <= cur) ++c.i;
-      rks[c.link] += c.sign * c.p[c.i].r;
-      if (c.i + 1 < c.n && c.p[c.i + 1].t < nbk[c.link]) nbk[c.link] = c.p[c.i + 1].t;
-    }
+    // r = the path minimum at cur, nb = its next possible change; while some link is saturated
+    // the path stays at 0 at least until every saturated link's own next change (zjump), so
+    // the walk jumps there instead of stepping through the other links' breakpoints
+    i64 nbk[3] = {T_INF, T_INF, T_INF};
+    for (int q = 0; q < nc; ++q) nbk[cs[q].link] = std::min(nbk[cs[q].link], cs[q].nt);
     i64 r = T_INF, nb = T_INF, zjump = t_avail;
     for (int k = 0; k < nk; ++k) {
       if (rks[k] == 0) zjump = std::max(zjump, nbk[k]);
@@ -470,6 +481,7 @@ static bool transfer(const Net &net, const Pending *L0, const Pending *L1, i64 s
     if (r == 0) {
       if (zjump == T_INF) return false;          // a link on the path is saturated forever
       cur = zjump;
+      reach(cur);
       continue;
     }
     if (!started) {
@@ -488,6 +500,7 @@ static bool transfer(const Net &net, const Pending *L0, const Pending *L1, i64 s
     out.segs.push_back({cur, nb, r});
     if (rec) rec->push_back({cur, nb, r, {rks[0] - r, nk > 1 ? rks[1] - r : 0, nk > 2 ? rks[2] - r : 0}});
     cur = nb;
+    reach(cur);
   }
 }
 
