@@ -4,7 +4,8 @@
 OUT=${OUT:-gpurun_out/r02_taskprof}
 mkdir -p $OUT
 python scripts/planbench/dump.py /tmp/planinst > $OUT/dump.log 2>&1
-g++ -O2 -std=c++17 -pthread -ffp-contract=off scripts/planbench/planbench.cpp scripts/planbench/taskprof.cpp -Iinclude -Ipaper_1907_00434_b200/csrc -o /tmp/pb_tp
+python scripts/planbench/taskprof.py > /tmp/planner_taskprof.cpp
+g++ -O2 -std=c++17 -pthread -ffp-contract=off scripts/planbench/planbench.cpp /tmp/planner_taskprof.cpp -Iinclude -Ipaper_1907_00434_b200/csrc -o /tmp/pb_tp
 for T in 1 2 4 8; do
   for ME in 2 4 8; do
     [ $T = 1 ] && [ $ME != 8 ] && continue
@@ -12,7 +13,7 @@ for T in 1 2 4 8; do
     MLF_PLAN_MIN_EVALS=$ME MLF_PLAN_THREADS=$T /tmp/pb_tp /tmp/planinst/configs.txt 15 config4_G8 >> $OUT/taskprof.log 2>&1
   done
 done
-for V in scripts/planbench/variants/p6*.cpp; do
+for V in paper_1907_00434_b200/csrc/planner.cpp; do
   n=$(basename $V .cpp)
   g++ -O2 -std=c++17 -pthread -ffp-contract=off scripts/planbench/planbench.cpp $V -Iinclude -Ipaper_1907_00434_b200/csrc -o /tmp/pb_$n
   for T in 1 4 8 16; do
