@@ -752,12 +752,16 @@ static void staged_commit(mlf_ctx *c, const std::vector<CommitOp> &ops, int boun
   // MLF_STAGE_EVERY=k (A/B knob, default 1): only every k-th remote operand is pulled by the
   // copy engines, the others stay SM peer loads in the same kernel — the two transports then
   // share the NVLink ingress
-  const char *se = getenv("MLF_STAGE_EVERY");
-  const int every = se && atoi(se) > 0 ? atoi(se) : 1;
+  // (MLF_STAGE_SKIP=k: the opposite split — every remote operand except every k-th is staged)
+  const char *se = getenv("MLF_STAGE_EVERY"), *sk = getenv("MLF_STAGE_SKIP");
+  const int every = se && atoi(se) > 0 ? atoi(se) : 1, skip = sk && atoi(sk) > 1 ? atoi(sk) : 0;
   std::vector<int> row(ops.size(), -1);
   int n_remote = 0, seen_remote = 0;
-  for (size_t q = 0; q < ops.size(); ++q)
-    if (ops[q].home >= 0 && ops[q].home != c->cfg.rank && seen_remote++ % every == 0) row[q] = n_remote++;
+  for (size_t q = 0; q < ops.size(); ++q) {
+    if (ops[q].home < 0 || ops[q].home == c->cfg.rank) continue;
+    const int r = seen_remote++;
+    if (skip ? r % skip != 0 : r % every == 0) row[q] = n_remote++;
+  }
   constexpr int64_t kAlign = 4096;                 // elements: keeps every row 16-byte (and tile) aligned
   int64_t C = n_remote ? c->cfg.stage_bytes / (2 * n_remote * e) : 0;
   // at least 4 chunks per shard (MLF_STAGE_CHUNKS; the last chunk's fold is not overlapped);
