@@ -301,6 +301,17 @@ mlf_status mlf_init(const mlf_config *cfg, int64_t v0, mlf_ctx **out);
 mlf_status mlf_submit_update(mlf_ctx *ctx, int32_t worker, int64_t version,
                              int64_t t_avail_ns, double norm, int32_t *index_in_batch);
 
+/* push for n workers in one call (Table 1; the batch of pushes a batching window
+ * collects): the same as mlf_submit_update(ctx, worker[i], version[i],
+ * t_avail_ns[i], norm[i], NULL) for i = 0..n-1 in that order — the updates take batch indices
+ * (current batch size) + i — except that it is all or nothing: every descriptor is checked
+ * first and on any error (the codes of mlf_submit_update; a worker twice in `worker` ->
+ * MLF_E_STATE) nothing is appended.  worker / version: host arrays of n (borrowed for the
+ * call); t_avail_ns / norm: host arrays of n, or NULL for all 0.  n = 0 is a no-op. */
+mlf_status mlf_submit_batch(mlf_ctx *ctx, int32_t n, const int32_t *worker,
+                            const int64_t *version, const int64_t *t_avail_ns,
+                            const double *norm);
+
 /* Optional: worker `worker`'s update lives in pinned host memory `host_ptr`;
  * mlf_execute copies it to the worker's device slot only if the plan commits
  * it (dropped updates are "dropped at the worker itself", and move

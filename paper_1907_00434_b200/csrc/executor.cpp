@@ -299,6 +299,43 @@ extern "C" mlf_status mlf_submit_update(mlf_ctx *c, int32_t worker, int64_t vers
   });
 }
 
+// push for n workers in one call (include/mlfabric.h): every descriptor is checked before any
+// is appended, so on error the batch is unchanged.
+extern "C" mlf_status mlf_submit_batch(mlf_ctx *c, int32_t n, const int32_t *worker, const int64_t *version,
+                                       const int64_t *t_avail_ns, const double *norm) {
+  return guard([&] {
+    check_ctx(c);
+    if (n < 0 || (n > 0 && (!worker || !version))) throw Fail{MLF_E_INVALID, "n / worker / version"};
+    if (c->phase1_done) throw Fail{MLF_E_STATE, "batch is being executed (phase 1 done)"};
+    release_if_done(c);
+    for (int32_t i = 0; i < n; ++i) {
+      const int32_t w = worker[i];
+      const char *why = nullptr;
+      mlf_status st = MLF_E_INVALID;
+      if (w < 0 || w >= c->cfg.n_workers) why = "worker out of range";
+      else if ((t_avail_ns && t_avail_ns[i] < 0) || (norm && !(norm[i] >= 0))) why = "t_avail / norm";
+      else if (c->in_batch[w]) st = MLF_E_STATE, why = "worker already submitted in this batch";
+      else if (c->in_flight[w]) st = MLF_E_STATE, why = "worker slot still in flight (call mlf_sync)";
+      if (why) {
+        for (int32_t q = 0; q < i; ++q) c->in_batch[worker[q]] = 0;   // undo this call's marks
+        throw Fail{st, why};
+      }
+      c->in_batch[w] = 2;                        // also catches a duplicate inside this call
+    }
+    const int64_t bytes = c->cfg.model_elems * (int64_t)c->elem_bytes;
+    for (int32_t i = 0; i < n; ++i) {
+      const int32_t w = worker[i];
+      c->in_batch[w] = 1;
+      c->b_worker.push_back(w);
+      c->b_node.push_back(c->worker_node[w]);
+      c->b_bytes.push_back(bytes);
+      c->b_version.push_back(version[i]);
+      c->b_tavail.push_back(t_avail_ns ? t_avail_ns[i] : 0);
+      c->b_norm.push_back(norm ? norm[i] : 0.0);
+    }
+  });
+}
+
 extern "C" mlf_status mlf_set_pull_host(mlf_ctx *c, void *host_dst) {
   return guard([&] {
     check_ctx(c);

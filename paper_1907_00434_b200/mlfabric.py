@@ -21,7 +21,7 @@ MLF_PHASE_AGGREGATE, MLF_PHASE_COMMIT = 1, 2
 
 # every symbol include/mlfabric.h declares
 EXPORTS = (
-    "mlf_plan", "mlf_init", "mlf_submit_update", "mlf_set_update_host", "mlf_set_pull_host", "mlf_batch_view",
+    "mlf_plan", "mlf_init", "mlf_submit_update", "mlf_submit_batch", "mlf_set_update_host", "mlf_set_pull_host", "mlf_batch_view",
     "mlf_version",
     "mlf_execute", "mlf_execute_phase", "mlf_sync", "mlf_pull_model", "mlf_stats", "mlf_destroy",
     "mlf_last_error", "mlf_ipc_export", "mlf_ipc_open", "mlf_ipc_close", "mlf_phase_event_export",
@@ -118,6 +118,7 @@ _lib.mlf_distribute_phase.argtypes = [_p, C.POINTER(MlfDistOut), C.c_int32, _i32
                                       _i64p, _i64p, C.c_int32, _i32p]
 _lib.mlf_init.argtypes = [C.POINTER(MlfConfig), C.c_int64, C.POINTER(_p)]
 _lib.mlf_submit_update.argtypes = [_p, C.c_int32, C.c_int64, C.c_int64, C.c_double, _i32p]
+_lib.mlf_submit_batch.argtypes = [_p, C.c_int32, _i32p, _i64p, _i64p, C.POINTER(C.c_double)]
 _lib.mlf_set_update_host.argtypes = [_p, C.c_int32, _p]
 _lib.mlf_set_pull_host.argtypes = [_p, _p]
 _lib.mlf_batch_view.argtypes = [_p, C.POINTER(MlfBatch)]
@@ -401,6 +402,15 @@ class Context:
         idx = C.c_int32()
         _check(_lib.mlf_submit_update(self._h, worker, int(version), int(t_avail_ns), float(norm), C.byref(idx)))
         return idx.value
+
+    def submit_batch(self, workers, versions, t_avail_ns=None, norms=None):
+        """mlf_submit_batch: one push per worker, in order, all or nothing (int32 / int64 /
+        int64 / float64 arrays; t_avail_ns, norms None -> 0)."""
+        w, v = _arr(workers, np.int32), _arr(versions, np.int64)
+        t = _arr(t_avail_ns, np.int64) if t_avail_ns is not None else None
+        nr = _arr(norms, np.float64) if norms is not None else None
+        _check(_lib.mlf_submit_batch(self._h, len(w), _ptr(w, C.c_int32), _ptr(v, C.c_int64), _ptr(t, C.c_int64),
+                                     _ptr(nr, C.c_double)))
 
     def set_update_host(self, worker: int, host_ptr: int | None):
         _check(_lib.mlf_set_update_host(self._h, worker, host_ptr))

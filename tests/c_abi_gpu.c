@@ -55,7 +55,15 @@ int main(int argc, char **argv) {
   mlf_ctx *ctx = NULL;
   const int64_t v0 = 40;
   CK(mlf_init(&cfg, v0, &ctx) == MLF_OK);
-  for (int i = 0; i < W; ++i) CK(mlf_submit_update(ctx, i, v0, 0, 1.0, NULL) == MLF_OK);
+  /* worker 0 by mlf_submit_update, the others in one mlf_submit_batch call */
+  CK(mlf_submit_update(ctx, 0, v0, 0, 1.0, NULL) == MLF_OK);
+  {
+    int32_t ws[W - 1];
+    int64_t vs[W - 1];
+    double ns[W - 1];
+    for (int i = 1; i < W; ++i) ws[i - 1] = i, vs[i - 1] = v0, ns[i - 1] = 1.0;
+    CK(mlf_submit_batch(ctx, W - 1, ws, vs, NULL, ns) == MLF_OK);
+  }
 
   int64_t up[NODES] = {10 * MB, 5 * MB, 10 * MB, 5 * MB / 2, 10 * MB, 1 * MB, 0};
   int64_t down[NODES] = {0, 0, 0, 0, 0, 0, 10 * MB};

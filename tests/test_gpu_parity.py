@@ -490,6 +490,46 @@ def test_invalid_plan_rejected_without_device_work():
     ctx.close()
 
 
+def test_submit_batch_equals_single_submits_and_is_all_or_nothing():
+    """mlf_submit_batch = mlf_submit_update per worker in order (Table 1 push); a bad
+    descriptor anywhere leaves the batch unchanged."""
+    dev = torch.device("cuda", 0)
+    S = 64
+    slots = [torch.zeros(S, device=dev) for _ in range(6)]
+    wt = torch.ones(S, device=dev)
+
+    def view(c):
+        b = c.batch_view()
+        return [(b.node[i], b.bytes[i], b.version[i], b.t_avail_ns[i], b.norm[i]) for i in range(b.n)]
+
+    kw = dict(device=0, model_shard=wt, update_slots=slots, lr=0.5, model_elems=S, worker_node=[3, 1, 4, 1, 5, 9],
+              n_nodes=10, stream=torch.cuda.current_stream().cuda_stream)
+    one, many = m.Context(**kw), m.Context(**kw)
+    ws, vs, ts, ns = [4, 0, 2], [7, 5, 6], [10, 0, 30], [1.5, 0.25, 2.0]
+    for w, v, t, nr in zip(ws, vs, ts, ns):
+        one.submit(w, v, t, nr)
+    many.submit_batch(ws, vs, ts, ns)
+    assert view(one) == view(many) and len(view(many)) == 3
+    for bad, code in (([1, 1], m.MLF_E_STATE),          # twice in one call
+                      ([5, 0], m.MLF_E_STATE),          # already in the batch
+                      ([5, 6], m.MLF_E_INVALID)):       # out of range
+        with pytest.raises(m.MlfError) as e:
+            many.submit_batch(bad, [0] * len(bad))
+        assert e.value.code == code
+        assert view(many) == view(one)
+    with pytest.raises(m.MlfError) as e:                # negative t_avail
+        many.submit_batch([1, 3], [0, 0], [0, -1])
+    assert e.value.code == m.MLF_E_INVALID
+    many.submit_batch([1, 3], [8, 9])                   # marks of the failed calls were undone
+    one.submit(1, 8)
+    one.submit(3, 9)
+    assert view(one) == view(many) and len(view(many)) == 5
+    many.submit_batch([], [])
+    assert view(one) == view(many)
+    one.close()
+    many.close()
+
+
 def test_executor_rejects_a_plan_beyond_the_delay_bound():
     """registerAsServer(tau_max) (Table 1): the executor re-checks (v + p) - v(g) <= tau_max for
     every committed update (R1) and rejects a stale plan before any device work."""
