@@ -505,14 +505,14 @@ static bool transfer(const Net &net, const Pending *L0, const Pending *L1, i64 s
 }
 
 // O2: NetUp — subtract reservations from the residual profiles.
-static void apply_pending(Net &net, const Pending &P) {
+static void apply_pending(Net &net, const Pending &P, int sign = -1) {
   std::vector<TSeg> &segs = scratch().segs_apply;
   for (int i = 0; i < P.nkeys; ++i) {
     const Profile &u = P.used[i];
     segs.clear();
     for (size_t q = 0; q + 1 < u.size(); ++q)
       if (u[q].r) segs.push_back({u[q].t, u[q + 1].t, u[q].r});
-    combine(net.mut(P.keys[i]), segs.data(), (int)segs.size(), -1);
+    combine(net.mut(P.keys[i]), segs.data(), (int)segs.size(), sign);
   }
 }
 static void copy_pending(Pending &dst, const Pending &src) {
@@ -777,7 +777,11 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
   std::vector<int> la_moved;                 // classes the current look-ahead moved to la_id
 
   // ShrtDline(pos, cands, NW + L0): the due set's argmin if any, else ShrtUp (R4, R6).
-  auto pick = [&](i64 pos, const std::vector<int> &cands, const Pending *L0) -> int {
+  // side: work that must not wait for the scan but only reads NW and L0 (see the look-ahead
+  // below); when the scan's classes go to the pool it runs there as one more item, else it is
+  // not run and *side_ran stays false.
+  auto pick = [&](i64 pos, const std::vector<int> &cands, const Pending *L0,
+                  const std::function<void()> *side = nullptr, bool *side_ran = nullptr) -> int {
     bool any_due = false;
     for (int g : cands)
       if (dl[g] == pos) {
@@ -814,11 +818,23 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
         miss.push_back(g);
       }
     }
+    const int ms = (int)miss.size();
+    const bool par = multi_server && (ms >= min_parallel_evals() || (side && ms >= 1));
+    const int off = par && side ? 1 : 0;
+    if (side_ran) *side_ran = off == 1;
     Pool::get().run(
-        (int)miss.size(),
+        ms + off,
         [&](int i) {
+          if (i < off) {
+            try {
+              (*side)();
+            } catch (const PlanFail &e) {
+              if (!task_failed.exchange(true)) task_err = e;
+            }
+            return;
+          }
           thread_local Pending local;
-          const int g = miss[i];
+          const int g = miss[i - off];
           ClassCache &cc = cache[cls[g]];
           int from = 0;
           const bool on_nw = L0 && cc.tag == nw_id;
@@ -852,7 +868,7 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
           cc.t_st = s.t_st;
           cc.t_en = s.t_en;
         },
-        multi_server && (int)miss.size() >= min_parallel_evals() ? 2 : std::numeric_limits<int>::max());
+        par ? 2 : std::numeric_limits<int>::max());
     if (task_failed.load()) throw task_err;
     if (L0)
       for (int g : miss)
@@ -874,6 +890,47 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
   // reusing it halves the scans without changing any decision.
   int cached = -1;
   std::vector<int> keep, cands;
+  // What a kept g* costs after its decision (Alg. 3's probe of NW, NetUp, the copy of its
+  // reservation) only reads NW and g*'s reservation, which the look-ahead scan also only reads,
+  // so it runs as a side job of that scan, speculatively (a dropped g* discards it):
+  //  * nw2 is a second copy of NW, brought up to date and given g*'s reservation in the side
+  //    job, so a kept g* swaps the two (NetUp off the critical path); `lag` lists the
+  //    reservations nw2 still has to apply (sign -1) or take back (sign +1) to equal NW —
+  //    canonical profiles make the result independent of that order;
+  //  * spec_res / spec_snap / spec_tm / spec_dead: the reservation's copy and the probe of NW.
+  res.res.reserve(n);                       // lag keeps pointers into res.res
+  std::unique_ptr<Net> nw2;
+  std::vector<std::pair<const Pending *, int>> lag;
+  Pending spec_res;
+  std::unique_ptr<Net> spec_snap;
+  i64 spec_tm = 0;
+  bool spec_dead = false, spec_has_snap = false;
+  auto probe_now = [&](const Net &net, int g, i64 &tm, bool &dead, bool &has_snap, std::unique_ptr<Net> &snap) {
+    const int k = (int)res.order.size();               // g*'s position in O(U)
+    has_snap = k % AggProbe::kEvery == 0;
+    if (has_snap) {
+      if (snap) *snap = net;
+      else snap = std::make_unique<Net>(net);
+    }
+    tm = k == 0 ? 0 : std::max(probe->tmax[k - 1], res.sends[k - 1].t_en);
+    dead = false;
+    if (k > 0) {
+      thread_local Transfer tr;
+      const Item &it = batch[g];
+      try {
+        dead = !transfer(net, nullptr, nullptr, it.size, it.node, (*probe->aggs)[0], it.t_avail, tr) || tr.t_en > tm;
+      } catch (const PlanFail &) {
+        dead = false;                                    // the case itself reports it, if it runs
+      }
+    }
+  };
+  int side_g = -1;
+  const std::function<void()> side = [&] {
+    for (const auto &op : lag) apply_pending(*nw2, *op.first, op.second);
+    apply_pending(*nw2, star);
+    copy_pending(spec_res, star);
+    if (probe) probe_now(nw, side_g, spec_tm, spec_dead, spec_has_snap, spec_snap);
+  };
   for (;;) {
     keep.clear();
     for (int g : unproc) {
@@ -905,12 +962,14 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
     cands.clear();
     for (int g : unproc)
       if (g != g_star && dl[g] >= p + 1) cands.push_back(g);
-    bool drop = false;
+    bool drop = false, side_ran = false;
     int g_next = -1;
     la_id = next_id++;
     la_moved.clear();
     if (!cands.empty()) {
-      g_next = pick(p + 1, cands, &star);              // on NetUp(NW, g*)
+      if (multi_server && !nw2) nw2 = std::make_unique<Net>(nw);
+      side_g = g_star;
+      g_next = pick(p + 1, cands, &star, multi_server ? &side : nullptr, &side_ran);   // on NetUp(NW, g*)
       if (t_star > ten[g_next]) drop = true;           // Alg. 2 line 10
     }
     unproc.erase(std::find(unproc.begin(), unproc.end(), g_star));
@@ -927,30 +986,40 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
         for (const TakeLog &t : cc.takes) cc.rec.walk[t.w].slack[t.k] += t.amount;
         cc.tag = nw_id;
       }
+      if (side_ran) {                                   // nw2 took g*'s reservation: take it back
+        lag.clear();
+        lag.push_back({&spec_res, +1});
+      }
       continue;
     }
-    if (probe) {
-      const int k = (int)res.order.size();               // g*'s position in O(U)
-      if (k % AggProbe::kEvery == 0) probe->snaps.push_back(nw);
-      const i64 tm = k == 0 ? 0 : std::max(probe->tmax[k - 1], res.sends[k - 1].t_en);
-      probe->tmax.push_back(tm);
-      bool dead = false;
-      if (k > 0) {
-        thread_local Transfer tr;
-        const Item &it = batch[g_star];
-        try {
-          dead = !transfer(nw, nullptr, nullptr, it.size, it.node, (*probe->aggs)[0], it.t_avail, tr) || tr.t_en > tm;
-        } catch (const PlanFail &) {
-          dead = false;                                    // the case itself reports it, if it runs
-        }
+    if (side_ran) {
+      if (probe) {
+        if (spec_has_snap) probe->snaps.push_back(std::move(*spec_snap));
+        probe->tmax.push_back(spec_tm);
+        probe->dead.push_back(spec_dead);
       }
-      probe->dead.push_back(dead);
+      std::swap(nw, *nw2);                              // NW := NW + g*; nw2 lags by g*
+      res.res.emplace_back();
+      std::swap(res.res.back(), spec_res);
+      lag.clear();
+      lag.push_back({&res.res.back(), -1});
+    } else {
+      if (probe) {
+        i64 tm;
+        bool dead, has_snap;
+        std::unique_ptr<Net> snap;
+        probe_now(nw, g_star, tm, dead, has_snap, snap);
+        if (has_snap) probe->snaps.push_back(std::move(*snap));
+        probe->tmax.push_back(tm);
+        probe->dead.push_back(dead);
+      }
+      apply_pending(nw, star);
+      res.res.emplace_back();
+      copy_pending(res.res.back(), star);
+      if (nw2) lag.push_back({&res.res.back(), -1});
     }
     res.order.push_back(g_star);
-    apply_pending(nw, star);
     nw_id = la_id;
-    res.res.emplace_back();
-    copy_pending(res.res.back(), star);
     res.sends.push_back(s_star);
     ++p;
     cached = g_next;
