@@ -356,16 +356,41 @@ struct Pending {
       if (keys[i] == key) return &used[i];
     return nullptr;
   }
-  Profile &slot(i64 key) {
+  Profile &slot(i64 key, bool *fresh = nullptr) {
     for (int i = 0; i < nkeys; ++i)
-      if (keys[i] == key) return used[i];
+      if (keys[i] == key) {
+        if (fresh) *fresh = false;
+        return used[i];
+      }
     if (nkeys == (int)keys.size()) {
       keys.push_back(key);
       used.emplace_back();
     }
     keys[nkeys] = key;
     used[nkeys].assign(1, Seg{0, 0});
+    if (fresh) *fresh = true;
     return used[nkeys++];
+  }
+  // add segments s[0, m) — in time order, disjoint — to the link's reserved rate: into a fresh
+  // slot (the zero profile) they are written out directly as the canonical profile combine()
+  // would build; otherwise merged by combine()
+  void add(i64 key, const TSeg *s, int m) {
+    bool fresh;
+    Profile &p = slot(key, &fresh);
+    if (!fresh) {
+      combine(p, s, m, +1);
+      return;
+    }
+    for (int i = 0; i < m; ++i) {
+      if (s[i].r == 0 || s[i].a >= s[i].b) continue;
+      if (p.back().t == s[i].a) {                 // a breakpoint (value 0) where this segment starts
+        if (p.size() > 1 && p[p.size() - 2].r == s[i].r) p.pop_back();
+        else p.back().r = s[i].r;
+      } else {                                    // p.back().t < s[i].a, value 0 up to s[i].a
+        p.push_back({s[i].a, s[i].r});
+      }
+      p.push_back({s[i].b, 0});
+    }
   }
 };
 
@@ -591,9 +616,9 @@ static bool send(const Net &net, const Pending *L0, const Ctx &c, const std::vec
   const bool all = record_all || c.dup_dsts;
   auto reserve = [&](size_t j, const Path &path, const std::vector<TSeg> &sg) {
     if (j + 1 < dsts.size() ? all : record_all) {
-      for (int k = 0; k < path.nk; ++k) combine(local.slot(path.key[k]), sg.data(), (int)sg.size(), +1);
+      for (int k = 0; k < path.nk; ++k) local.add(path.key[k], sg.data(), (int)sg.size());
     } else if (j + 1 < dsts.size() && path.nk && path.key[0] < n) {   // up(src) is always the first path link
-      combine(local.slot(path.key[0]), sg.data(), (int)sg.size(), +1);
+      local.add(path.key[0], sg.data(), (int)sg.size());
     }
   };
   if (rec) {
@@ -781,7 +806,7 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
   // below); when the scan's classes go to the pool it runs there as one more item, else it is
   // not run and *side_ran stays false.
   auto pick = [&](i64 pos, const std::vector<int> &cands, const Pending *L0,
-                  const std::function<void()> *side = nullptr, bool *side_ran = nullptr) -> int {
+                  const std::function<void(int)> *side = nullptr, bool *side_ran = nullptr) -> int {
     bool any_due = false;
     for (int g : cands)
       if (dl[g] == pos) {
@@ -820,14 +845,14 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
     }
     const int ms = (int)miss.size();
     const bool par = multi_server && (ms >= min_parallel_evals() || (side && ms >= 1));
-    const int off = par && side ? 1 : 0;
-    if (side_ran) *side_ran = off == 1;
+    const int off = par && side ? 2 : 0;
+    if (side_ran) *side_ran = off > 0;
     Pool::get().run(
         ms + off,
         [&](int i) {
           if (i < off) {
             try {
-              (*side)();
+              (*side)(i);
             } catch (const PlanFail &e) {
               if (!task_failed.exchange(true)) task_err = e;
             }
@@ -901,7 +926,7 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
   res.res.reserve(n);                       // lag keeps pointers into res.res
   std::unique_ptr<Net> nw2;
   std::vector<std::pair<const Pending *, int>> lag;
-  Pending spec_res;
+  Pending spec_res, undo_res;
   std::unique_ptr<Net> spec_snap;
   i64 spec_tm = 0;
   bool spec_dead = false, spec_has_snap = false;
@@ -925,9 +950,13 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
     }
   };
   int side_g = -1;
-  const std::function<void()> side = [&] {
-    for (const auto &op : lag) apply_pending(*nw2, *op.first, op.second);
-    apply_pending(*nw2, star);
+  // two independent side items: nw2's NetUps; the reservation's copy and the probe of NW
+  const std::function<void(int)> side = [&](int j) {
+    if (j == 0) {
+      for (const auto &op : lag) apply_pending(*nw2, *op.first, op.second);
+      apply_pending(*nw2, star);
+      return;
+    }
     copy_pending(spec_res, star);
     if (probe) probe_now(nw, side_g, spec_tm, spec_dead, spec_has_snap, spec_snap);
   };
@@ -952,7 +981,7 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
       star.clear();
       for (const CompRec &cr : cg.rec.comps) {
         rec_segs(cg.rec, cr, segs);
-        for (int k = 0; k < cr.path.nk; ++k) combine(star.slot(cr.path.key[k]), segs.data(), (int)segs.size(), +1);
+        for (int k = 0; k < cr.path.nk; ++k) star.add(cr.path.key[k], segs.data(), (int)segs.size());
       }
       s_star.t_st = cg.t_st;
       s_star.t_en = cg.t_en;
@@ -987,8 +1016,9 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
         cc.tag = nw_id;
       }
       if (side_ran) {                                   // nw2 took g*'s reservation: take it back
+        std::swap(spec_res, undo_res);                  // (the next side items rewrite spec_res)
         lag.clear();
-        lag.push_back({&spec_res, +1});
+        lag.push_back({&undo_res, +1});
       }
       continue;
     }

@@ -41,10 +41,12 @@ def init_dist():
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", rank))
     if rank == 0:
-        # rank 0 plans for the whole box (ShardedWorkload.plan_once): its planner pool may use up
-        # to 8 of the host's cores instead of this rank's 1/LOCAL_WORLD_SIZE share (read when the
-        # library's pool starts, i.e. at the first plan)
-        os.environ.setdefault("MLF_PLAN_THREADS", str(max(1, min(8, os.cpu_count() or 1))))
+        # rank 0 plans for the whole box (ShardedWorkload.plan_once): its planner pool may use
+        # all of the host's cores (up to 16) instead of this rank's 1/LOCAL_WORLD_SIZE share (read
+        # when the library's pool starts, i.e. at the first plan); the other ranks only wait for
+        # the broadcast plan.  Box host, config 4 / G = 8: 16 threads 1.58-1.61 ms, 8 threads
+        # 1.62-1.64 (profiles/r02/planner_side/)
+        os.environ.setdefault("MLF_PLAN_THREADS", str(max(1, min(16, os.cpu_count() or 1))))
     if not dist.is_initialized():
         # NCCL when every rank has its own GPU; ranks sharing a device (tests) use gloo only
         use_nccl = torch.cuda.is_available() and torch.cuda.device_count() >= world
