@@ -86,13 +86,17 @@ opt('''    cands.clear();
     cands.clear();
     for (int g : unproc)
       if (g != g_star && dl[g] >= p + 1) cands.push_back(g);''')
-opt('''      g_next = pick(p + 1, cands, &star);              // on NetUp(NW, g*)''', '''      auto tp1 = NOW;
-      g_next = pick(p + 1, cands, &star);              // on NetUp(NW, g*)
+opt('''      g_next = pick(p + 1, cands, &star, multi_server ? &side : nullptr, &side_ran);   // on NetUp(NW, g*)''',
+    '''      auto tp1 = NOW;
+      g_next = pick(p + 1, cands, &star, multi_server ? &side : nullptr, &side_ran);   // on NetUp(NW, g*)
       T_pick += MS(tp1, NOW);''')
-opt('''    res.order.push_back(g_star);
-    apply_pending(nw, star);''', '''    res.order.push_back(g_star);
-    auto tap = NOW;
-    apply_pending(nw, star);''')
+opt('''    if (stream) probe->ord.push_back(batch[g_star]);
+    if (side_ran) {''', '''    auto tap = NOW;
+    if (side_ran) {''')
+opt('''    if (side_ran) {
+      if (probe) {''', '''    auto tap = NOW;
+    if (side_ran) {
+      if (probe) {''')
 opt('''    res.sends.push_back(s_star);''', '''    res.sends.push_back(s_star);
     T_app += MS(tap, NOW);''')
 sys.stdout.write(s)
