@@ -279,13 +279,15 @@ def run_single(a):
         torch.cuda.synchronize()
         recs = []
         ck = Clocks(0)
+        if clocks:
+            ck.start()
         kl0 = 0
         for s in range(warmup + steps):
             timed = s >= warmup
             if timed and s == warmup:
                 kl0 = wl.ctx.stats()[0]
                 if clocks:
-                    ck.__enter__()
+                    ck.mark()
             draws = wl.submit_all(s)
             t0 = time.perf_counter()
             pb = wl.plan(s)

@@ -22,17 +22,24 @@ def hbm_peak():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line).
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    start() launches the sampler (100 ms period) before the warm-up, because nvidia-smi takes a
+    few hundred ms to print its first line and a short timed region would otherwise get none;
+    mark() opens the timed window and __exit__ closes it; summary() keeps the samples whose
+    nvidia-smi timestamp falls inside the window (widened by one sampling period at each end),
+    else the nearest ones after the window opened (flagged)."""
+
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
         self.index = index
         self.p = None
+        self.t0 = self.t1 = None
 
-    def __enter__(self):
+    def start(self):
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                                        "--format=csv,noheader,nounits", "-lms", "100"],
@@ -41,7 +48,17 @@ class Clocks:
             self.p = None
         return self
 
+    def mark(self):
+        self.t0 = time.time()
+
+    def __enter__(self):
+        if self.p is None:
+            self.start()
+        self.mark()
+        return self
+
     def __exit__(self, *a):
+        self.t1 = time.time()
         self.lines = []
         if self.p is not None:
             time.sleep(0.25)
@@ -53,22 +70,26 @@ class Clocks:
             self.lines = [l for l in out.splitlines() if l.strip()]
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
+        import datetime
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        rows = []
         for l in getattr(self, "lines", []):
             f = [x.strip() for x in l.split(",")]
-            if len(f) < 9:
+            if len(f) < 10:
                 continue
             try:
-                sm.append(float(f[1]))
-                mx = float(f[2])
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                rows.append((ts, float(f[2]), float(f[3]), f[6:10]))
             except ValueError:
                 continue
-            for nm, v in zip(names, f[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        sm.sort()
-        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
-
-
+        lo = (self.t0 or 0) - 0.1
+        hi = (self.t1 or float("inf")) + 0.1
+        win = [r for r in rows if lo <= r[0] <= hi]
+        where = "timed window"
+        if not win:
+            win = [r for r in rows if r[0] >= lo][:2]
+            where = "first samples after the timed window opened (window shorter than the sampler's start-up)"
+        sm = sorted(r[1] for r in win)
+        reasons = {nm for r in win for nm, v in zip(names, r[3]) if v.lower().startswith("active")}
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": win[-1][2] if win else None,
+                "reasons": sorted(reasons), "samples": len(sm), "from": where}

@@ -338,13 +338,15 @@ def run_bench_multi(a):
         sw = ShardedWorkload(cfg, rank, world, local, ctrl, mode=mode)
         sw.fill(0)
         ck = Clocks(local)
+        if clocks:
+            ck.start()
         recs = []
         kl0 = 0
         for s in range(warmup + steps):
             if s == warmup:
                 kl0 = sw.wl.ctx.stats()[0]
                 if clocks:
-                    ck.__enter__()
+                    ck.mark()
             pd, ms = sw.step(s, flush=l2_flush)
             ms_max = max_over_ranks(ms, ctrl)
             if s >= warmup:
