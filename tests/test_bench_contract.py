@@ -43,3 +43,28 @@ def test_gpu_line():
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     e = d["e2e"]
     assert e["unit"] == "GB/s" and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+
+
+def test_clock_samples_are_taken_from_the_timed_window():
+    """The clocks line keeps only nvidia-smi samples timestamped inside the timed window (widened
+    by one 100 ms period); a window shorter than the sampler's start-up falls back to the first
+    samples after it opened, and says so."""
+    import datetime
+
+    sys.path.insert(0, ROOT)
+    from benchkit.common import Clocks
+
+    def row(t, mhz, slow="Not Active", cap="Not Active"):
+        ts = datetime.datetime.fromtimestamp(t).strftime("%Y/%m/%d %H:%M:%S.%f")[:-3]
+        return f"{ts}, 0, {mhz}, 1965, 700.0, 0x0, {slow}, Not Active, Not Active, {cap}"
+
+    ck = Clocks(0)
+    ck.t0, ck.t1 = 1000.0, 1001.0
+    ck.lines = [row(999.5, 900, slow="Active"), row(1000.2, 1965), row(1000.5, 1950, cap="Active"),
+                row(1000.8, 1965), row(1002.0, 800)]
+    s = ck.summary()
+    assert s["samples"] == 3 and s["sm_mhz"] == 1965.0 and s["reasons"] == ["sw_power_cap"]
+    assert s["from"] == "timed window"
+    ck.t0, ck.t1 = 1001.5, 1001.6                       # nothing inside: the next samples
+    s = ck.summary()
+    assert s["samples"] == 1 and s["sm_mhz"] == 800.0 and s["from"].startswith("first samples")
