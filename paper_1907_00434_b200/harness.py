@@ -106,8 +106,8 @@ class Workload:
 
     def submit_all(self, iteration: int):
         draws = cfgs.batch_draws(self.cfg, iteration, self.v_init, self.v_prev)
-        for w, d in enumerate(draws):
-            self.ctx.submit(w, d["version"], d["t_avail"], d["norm"])
+        self.ctx.submit_batch(range(len(draws)), [d["version"] for d in draws], [d["t_avail"] for d in draws],
+                              [d["norm"] for d in draws])
         return draws
 
     def plan(self, iteration: int):
