@@ -802,9 +802,9 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
   std::vector<int> la_moved;                 // classes the current look-ahead moved to la_id
 
   // ShrtDline(pos, cands, NW + L0): the due set's argmin if any, else ShrtUp (R4, R6).
-  // side: work that must not wait for the scan but only reads NW and L0 (see the look-ahead
-  // below); when the scan's classes go to the pool it runs there as one more item, else it is
-  // not run and *side_ran stays false.
+  // side(0), side(1): work that must not wait for the scan but only reads NW and L0 (see the
+  // look-ahead below); when the scan's classes go to the pool it runs there as two more items,
+  // else it is not run and *side_ran stays false.
   auto pick = [&](i64 pos, const std::vector<int> &cands, const Pending *L0,
                   const std::function<void(int)> *side = nullptr, bool *side_ran = nullptr) -> int {
     bool any_due = false;
