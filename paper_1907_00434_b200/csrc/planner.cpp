@@ -690,6 +690,18 @@ struct OrderRes {
 // a scan has ~7 such classes, ~4 of them re-evaluated (~2.5 us each); with the claim-word pool
 // a hand-off costs ~0.2 us, and config 4 / G = 8 plans fastest at a threshold of 4 (1.87 ms on
 // 8 threads vs 1.97 at 8 and 2.2 at 32).
+// Servers from which a look-ahead scan takes the side items (MLF_PLAN_SIDE_MIN_SERVERS overrides):
+// they pay where a class's send and g*'s NetUp are long (G = 8: 1.88 -> 1.63 ms at config 4 on the
+// box host) but cost hand-offs where both are short (G = 4: 0.78 vs 0.73 ms; G = 2, rank 0 in the
+// 2-GPU bench: 0.87 vs 0.37 ms), since they also send scans with a single changed class to the pool
+static int side_min_servers() {
+  static const int v = [] {
+    const char *e = getenv("MLF_PLAN_SIDE_MIN_SERVERS");
+    return e && atoi(e) > 0 ? atoi(e) : 8;
+  }();
+  return v;
+}
+
 static int min_parallel_evals() {
   static const int v = [] {
     const char *e = getenv("MLF_PLAN_MIN_EVALS");
@@ -756,6 +768,7 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
   // with one server a class's send is one transfer (~0.3 us): too little to hand to the pool
   // (config 2, tau 32: 0.13 ms serial vs 0.22 ms on 8 threads)
   const bool multi_server = c.servers.size() > 1;
+  const bool use_side = multi_server && (int)c.servers.size() >= side_min_servers();
   // t_en is a pure function of (network, node, size, t_avail): updates sharing the triple
   // (virtual workers on one GPU usually share all three) form one class, evaluated once per scan
   std::vector<int> cls(n), cls_rep, cls_stamp;
@@ -996,9 +1009,9 @@ static OrderRes order_final(const Ctx &c, const std::vector<Item> &batch, i64 ta
     la_id = next_id++;
     la_moved.clear();
     if (!cands.empty()) {
-      if (multi_server && !nw2) nw2 = std::make_unique<Net>(nw);
+      if (use_side && !nw2) nw2 = std::make_unique<Net>(nw);
       side_g = g_star;
-      g_next = pick(p + 1, cands, &star, multi_server ? &side : nullptr, &side_ran);   // on NetUp(NW, g*)
+      g_next = pick(p + 1, cands, &star, use_side ? &side : nullptr, &side_ran);   // on NetUp(NW, g*)
       if (t_star > ten[g_next]) drop = true;           // Alg. 2 line 10
     }
     unproc.erase(std::find(unproc.begin(), unproc.end(), g_star));

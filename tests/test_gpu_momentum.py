@@ -113,27 +113,7 @@ def test_momentum_config2_every_element_vs_sequential_eq2(dtype):
           f"norm-relative {max_dw / max_w:.2e}")
 
 
-@pytest.mark.parametrize("pack_max", ["0", "40"])
-def test_momentum_packed_sum_fold_bitwise(pack_max, monkeypatch):
-    """The 16-warp bf16 kernel with and without the packed-sum fold (exact FFMA2 products with a
-    -0 addend + FADD2, bulk.cu prod2; MLF_MOM_PACK_MAX = 40 forces it for every list length,
-    0 never): bitwise the pinned order (weighted_f32) for 6..24 operands, ragged lengths."""
-    monkeypatch.setenv("MLF_MOM_PACK_MAX", pack_max)
-    rng = np.random.default_rng(77 + int(pack_max))
-    for trial in range(5):
-        S = int(rng.choice([8, 8200, 65_544, 200_003]))
-        W = int(rng.integers(6, 25))
-        p = random_plan(rng, W, n_commit=W)
-        (w, h, b, bh), h0 = run_momentum(S, W, sg.DTYPE_BF16, p, 0.9)
-        idx = np.arange(S)
-        commits = commits_from_plan(p, lambda g: sg.update_values(SEED, g, 0, idx, sg.DTYPE_BF16))
-        wr, hr, bkr = weighted_f32(sg.w0_values(SEED, idx), h0, commits, 0.01, 0.9, p["replica_boundary_commit"])
-        assert np.array_equal(bits(w), bits(wr)) and np.array_equal(bits(h), bits(hr)), (trial, S, W)
-        if p["replica_boundary_commit"] >= 0:
-            assert np.array_equal(bits(b), bits(bkr[0])) and np.array_equal(bits(bh), bits(bkr[1]))
-
-
-@pytest.mark.parametrize("dtype,tau", [("f32", 32), ("bf16", 32), ("bf16", 8), ("bf16", 4)])
+@pytest.mark.parametrize("dtype,tau", [("f32", 32), ("bf16", 32), ("bf16", 4)])
 def test_momentum_config2_full_size(dtype, tau):
     # fp32 takes the generic fold, all-bf16 operand lists the branch-free one (both kernels:
     # dynamic tiles at tau 4, round-robin at tau 32)
