@@ -86,9 +86,9 @@ opt('''    cands.clear();
     cands.clear();
     for (int g : unproc)
       if (g != g_star && dl[g] >= p + 1) cands.push_back(g);''')
-opt('''      g_next = pick(p + 1, cands, &star, multi_server ? &side : nullptr, &side_ran);   // on NetUp(NW, g*)''',
+opt('''      g_next = pick(p + 1, cands, &star, use_side ? &side : nullptr, &side_ran);   // on NetUp(NW, g*)''',
     '''      auto tp1 = NOW;
-      g_next = pick(p + 1, cands, &star, multi_server ? &side : nullptr, &side_ran);   // on NetUp(NW, g*)
+      g_next = pick(p + 1, cands, &star, use_side ? &side : nullptr, &side_ran);   // on NetUp(NW, g*)
       T_pick += MS(tp1, NOW);''')
 opt('''    if (stream) probe->ord.push_back(batch[g_star]);
     if (side_ran) {''', '''    auto tap = NOW;
