@@ -370,9 +370,11 @@ def run_bench_multi(a):
         results[mode] = run(mode, a.steps if i == 0 else max(3, a.steps // 2), a.warmup if i == 0 else 2,
                             clocks=(i == 0))
     if not a.no_variants:
-        # the mixed transport: every second remote operand pulled by the copy engines, the rest
-        # read over the peer mappings by the same kernel, the first chunk straight from the peers
-        mixed = {"MLF_STAGE_EVERY": "2", "MLF_STAGE_CHUNKS": "4", "MLF_STAGE_FIRST_DIRECT": "1"}
+        # the mixed transport: the copy engines pull 3 of every 4 remote operands in 3 chunks, the
+        # kernel reads the rest over the peer mappings, the first chunk straight from the peers
+        # (config 3 at 2 GPUs: 90.2% of the NVLink roofline vs 89.7% with every second operand in
+        # 4 chunks and 87.9% for fold; profiles/r02/hybrid/skip/)
+        mixed = {"MLF_STAGE_SKIP": "4", "MLF_STAGE_CHUNKS": "3", "MLF_STAGE_FIRST_DIRECT": "1"}
         saved = {k: os.environ.get(k) for k in mixed}
         os.environ.update(mixed)
         try:

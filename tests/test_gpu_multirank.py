@@ -80,6 +80,10 @@ def test_two_ranks_staged_every_third_remote_operand():
     out = _run(2, "--cid", "3", "--S", "300007", "--modes", "staged", "--workers", "32",
                extra_env={"MLF_STAGE_EVERY": "2", "MLF_STAGE_FIRST_DIRECT": "1", "MLF_STAGE_CHUNKS": "8"})
     assert "MULTIGPU_OK staged" in out
+    # ... and the bench's mixed variant: 3 of every 4 remote operands staged, 3 chunks
+    out = _run(2, "--cid", "3", "--S", "300007", "--modes", "staged", "--workers", "32",
+               extra_env={"MLF_STAGE_SKIP": "4", "MLF_STAGE_FIRST_DIRECT": "1", "MLF_STAGE_CHUNKS": "3"})
+    assert "MULTIGPU_OK staged" in out
 
 
 def test_two_ranks_staged_minimum_chunk():
