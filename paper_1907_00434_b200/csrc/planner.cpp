@@ -1345,6 +1345,11 @@ static AggCase plan_aggregation_probed(const std::vector<Item> &items, const Ctx
     det_agg_tail(cs, nw, pr.tmax[n], items, c, dsts, aggs, cut);
   };
   const bool small = (N + 1) * (int)dsts.size() < 256;
+  // a feasible case keeps its plan and network (few cases are feasible), so the argmin's needs
+  // no second run: a feasible case never exceeded the bound it ran with, so it is exactly the
+  // unbounded DetAgg(n)
+  std::vector<AggCase> fcase(live.size());
+  std::vector<std::unique_ptr<Net>> fnet(live.size());
   Pool::get().run(
       (int)live.size(),
       [&](int q) {
@@ -1359,6 +1364,8 @@ static AggCase plan_aggregation_probed(const std::vector<Item> &items, const Ctx
           run_case(n, *nw, cut, cs);
           if (!cs.feasible) return;
           totals[n] = cs.total;
+          fcase[q] = cs;
+          fnet[q] = std::move(nw);                     // the next case on this thread makes a new one
           i64 cur = best_total.load(std::memory_order_relaxed);
           while (cs.total < cur && !best_total.compare_exchange_weak(cur, cs.total, std::memory_order_relaxed)) {
           }
@@ -1381,11 +1388,11 @@ static AggCase plan_aggregation_probed(const std::vector<Item> &items, const Ctx
     if (net_out) *net_out = std::move(*pr.last);
     return cs;
   }
-  Net nw(pr.snaps[0]);
-  run_case(best, nw, T_INF, cs);
-  if (!cs.feasible || cs.total != totals[best]) throw PlanFail{MLF_E_INVALID, "internal: aggregation case changed"};
-  if (net_out) *net_out = std::move(nw);
-  return cs;
+  const int qb = (int)(std::lower_bound(live.begin(), live.end(), best) - live.begin());
+  if (qb >= (int)live.size() || live[qb] != best || !fnet[qb] || fcase[qb].total != totals[best])
+    throw PlanFail{MLF_E_INVALID, "internal: aggregation case lost"};
+  if (net_out) *net_out = std::move(*fnet[qb]);
+  return std::move(fcase[qb]);
 }
 
 static std::vector<i64> chained_times(const std::vector<CommitRec> &cm) {
